@@ -1,0 +1,116 @@
+/*
+ * flowplace_b200 — C ABI of the B200-native DOPPLER rollout hot path.
+ *
+ * Plain C types only (pointers + sizes); device pointers are raw CUDA
+ * allocations owned by the caller (torch tensors in the Python host), the
+ * stream argument is a cudaStream_t passed as void*.  Every entry point
+ * returns an FP_* status; fp_last_error() gives the message.  No call
+ * allocates device memory except *_create (one-time, per graph / policy)
+ * and the host-array drop-in fp_run_packed.
+ *
+ * Reference interfaces replaced (paths relative to the reference pkg/src):
+ *   fp_run_packed      <- flowplace/_simcore.pyx:39-45   run_packed(...)  (Python->Cython FFI)
+ *   fp_problem_create  <- flowplace/simulate.py:194-237 _pack(...)       (packed once per graph)
+ *   fp_sim_batch       <- flowplace/simulate.py:251-266 exec_time(...)   (batched over assignments)
+ *   fp_policy_*        <- flowplace/policy.py:149-402   gnn_encode / sel_forward / plc_forward /
+ *                                                        PolicyContext.rollout
+ *   fp_pg_*            <- flowplace/training.py:181-216 _rl_stage update (+ nn.py:184-277)
+ */
+#ifndef FLOWPLACE_B200_H
+#define FLOWPLACE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* call status */
+#define FP_OK 0
+#define FP_ERR_INVALID 1
+#define FP_ERR_CUDA 2
+#define FP_ERR_UNSUPPORTED 3
+#define FP_ERR_DEADLOCK 4
+#define FP_ERR_OVERFLOW 5
+
+/* simulator strategies (flowplace/simulate.py:37-38) */
+#define FP_STRATEGY_FIFO 0
+#define FP_STRATEGY_DEPTH_FIRST 1
+#define FP_STRATEGY_BREADTH_FIRST 2
+
+/* per-episode status codes written by batched kernels */
+#define FP_EP_OK 0
+#define FP_EP_DEADLOCK 1        /* makespan slot holds the deadlock time   */
+#define FP_EP_TRACE_OVERFLOW 2  /* trace_cap too small; makespan still valid */
+#define FP_EP_BAD_ACTION 3      /* forced action outside candidates / devices */
+
+/* One schedule event, the reference's (tkind, v, a, b, time, etype) record
+ * (flowplace/_simpy.py:7-9): kind 0 exec (a = device, b = -1), 1 transfer
+ * (a = src, b = dst); etype 0 beg, 1 end.  16 bytes. */
+typedef struct fp_event {
+    double time;
+    int32_t v;
+    int8_t kind;
+    int8_t etype;
+    int8_t a;
+    int8_t b;
+} fp_event;
+
+/* The packed problem of flowplace/simulate.py:194-237, host pointers. */
+typedef struct fp_graph_desc {
+    int32_t n, d;
+    const int32_t *pred_indptr, *pred_indices; /* [n+1], [E] sorted preds */
+    const int32_t *succ_indptr, *succ_indices; /* [n+1], [E] sorted succs */
+    const uint8_t *is_entry;                   /* [n] */
+    const double *flops, *obytes;              /* [n] */
+    const double *rates, *bw;                  /* [d], [d*d] */
+    const int32_t *eslots, *tslots;            /* [d], [d*d] */
+    const double *tlev, *blev;                 /* [n] or NULL (zeros) */
+    double comm_factor;
+} fp_graph_desc;
+
+typedef struct fp_problem fp_problem;
+
+const char *fp_last_error(void);
+int fp_version(void);
+
+/* Upload one graph + cluster to the current CUDA device (once per graph). */
+int fp_problem_create(const fp_graph_desc *g, fp_problem **out);
+int fp_problem_destroy(fp_problem *p);
+/* Shared memory the simulator needs per in-flight episode (bytes). */
+int fp_problem_sim_smem(const fp_problem *p, int64_t *bytes_per_episode);
+
+/* Work-conserving simulation of B assignments (device pointers).
+ *   assign   [B][n] int32 device ids
+ *   jitter   NULL, or per-task duration factors [n*d + n*d*d] per episode
+ *            (exec (v,a) at v*d+a; transfer (v,a,b) at n*d+(v*d+a)*d+b),
+ *            episode b reads jitter + b*jitter_stride (stride 0 = shared)
+ *   makespan [B] out; status [B] out (FP_EP_*)
+ *   trace    NULL, or [B][trace_cap] events out; trace_len [B] out
+ *   blocked  NULL, or [B][n] uint8 out: blocked frontier on deadlock */
+int fp_sim_batch(const fp_problem *p, const int32_t *assign, int32_t B, int32_t strategy,
+                 const double *jitter, int64_t jitter_stride, double *makespan,
+                 int32_t *status, fp_event *trace, int32_t trace_cap, int32_t *trace_len,
+                 uint8_t *blocked, void *stream);
+
+/* Drop-in for flowplace/_simcore.pyx:39-45 run_packed: host arrays in, host
+ * events out (events[0..*n_events)).  Jitter factors are computed on the host
+ * with the reference's splitmix64 + libm recipe (_simcore.pyx:15-36).
+ * Returns FP_ERR_DEADLOCK with *makespan = deadlock time and blocked[v] set
+ * for the blocked frontier (_simcore.pyx:204-207). */
+int fp_run_packed(int32_t n, int32_t d, const int32_t *pred_indptr, const int32_t *pred_indices,
+                  const int32_t *succ_indptr, const int32_t *succ_indices,
+                  const uint8_t *is_entry, const double *flops, const double *obytes,
+                  const int32_t *assign, const double *rates, const double *bw,
+                  const int32_t *eslots, const int32_t *tslots, const double *tlev,
+                  const double *blev, int32_t strategy, double comm_factor, double sigma,
+                  int64_t seed, double *makespan, fp_event *events, int64_t events_cap,
+                  int64_t *n_events, uint8_t *blocked);
+
+/* Host libm jitter tables (the exact reference factors), layout as above. */
+int fp_jitter_tables(int32_t n, int32_t d, double sigma, int64_t seed, double *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLOWPLACE_B200_H */

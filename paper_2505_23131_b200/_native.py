@@ -1,0 +1,87 @@
+"""ctypes binding of the C ABI in include/flowplace_b200.h.
+
+This is the binding a maintainer of the reference would add next to
+``flowplace/_simcore``.  There is no fallback: if the
+CUDA library is missing or no GPU is visible the calls raise.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+import numpy as np
+
+from ._build import LIB as _LIB_PATH
+
+FP_OK, FP_ERR_INVALID, FP_ERR_CUDA, FP_ERR_UNSUPPORTED, FP_ERR_DEADLOCK, FP_ERR_OVERFLOW = range(6)
+EP_OK, EP_DEADLOCK, EP_TRACE_OVERFLOW, EP_BAD_ACTION = range(4)
+
+_lib = None
+
+
+class NativeError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        self.code = code
+        super().__init__(f"flowplace_b200 error {code}: {msg}")
+
+
+class FpEvent(ctypes.Structure):
+    _fields_ = [("time", ctypes.c_double), ("v", ctypes.c_int32), ("kind", ctypes.c_int8),
+                ("etype", ctypes.c_int8), ("a", ctypes.c_int8), ("b", ctypes.c_int8)]
+
+
+EVENT_DTYPE = np.dtype([("time", "<f8"), ("v", "<i4"), ("kind", "i1"), ("etype", "i1"),
+                        ("a", "i1"), ("b", "i1")])
+assert EVENT_DTYPE.itemsize == ctypes.sizeof(FpEvent) == 16
+
+
+class FpGraphDesc(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("d", ctypes.c_int32)] + [
+        (name, ctypes.c_void_p) for name in (
+            "pred_indptr", "pred_indices", "succ_indptr", "succ_indices", "is_entry", "flops",
+            "obytes", "rates", "bw", "eslots", "tslots", "tlev", "blev")] + [
+        ("comm_factor", ctypes.c_double)]
+
+
+def lib() -> ctypes.CDLL:
+    global _lib
+    if _lib is None:
+        path = Path(_LIB_PATH)
+        if not path.exists():
+            raise RuntimeError(
+                f"CUDA library {path} is not built; run `python -m paper_2505_23131_b200._build`"
+                " (or __graft_entry__.build()). There is no CPU fallback.")
+        _lib = ctypes.CDLL(str(path))
+        _lib.fp_last_error.restype = ctypes.c_char_p
+        for name in dir(_lib):
+            pass
+    return _lib
+
+
+def check(rc: int) -> int:
+    if rc != FP_OK:
+        raise NativeError(rc, lib().fp_last_error().decode())
+    return rc
+
+
+def ptr(x) -> ctypes.c_void_p:
+    """Raw pointer of a numpy array or torch tensor (None -> NULL)."""
+    if x is None:
+        return ctypes.c_void_p(0)
+    if isinstance(x, np.ndarray):
+        return ctypes.c_void_p(x.ctypes.data)
+    return ctypes.c_void_p(x.data_ptr())
+
+
+def stream_ptr(stream=None) -> ctypes.c_void_p:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+EXPORTED = (
+    "fp_last_error", "fp_version", "fp_problem_create", "fp_problem_destroy",
+    "fp_problem_sim_smem", "fp_sim_batch", "fp_run_packed", "fp_jitter_tables",
+)

@@ -1,0 +1,321 @@
+// C-ABI: problem lifecycle, batched simulator entry, run_packed drop-in.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "fp_problem.cuh"
+#include "fp_sim.cuh"
+
+namespace fp {
+
+static thread_local std::string g_err;
+
+void set_error(const std::string &msg) { g_err = msg; }
+
+#define FP_CUDA(call)                                                                     \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess) {                                                          \
+            set_error(std::string(#call) + ": " + cudaGetErrorString(e_));                \
+            return FP_ERR_CUDA;                                                           \
+        }                                                                                 \
+    } while (0)
+
+// Bump allocator over one device arena.
+struct Arena {
+    std::vector<std::pair<size_t, std::vector<uint8_t>>> parts;
+    size_t size = 0;
+    template <typename T>
+    size_t put(const T *src, size_t count) {
+        size = (size + 255) / 256 * 256;
+        size_t off = size;
+        std::vector<uint8_t> bytes(sizeof(T) * count);
+        if (count) std::memcpy(bytes.data(), src, bytes.size());
+        parts.emplace_back(off, std::move(bytes));
+        size += sizeof(T) * count;
+        return off;
+    }
+};
+
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
+sim_batch_kernel(DevProblem P, const int32_t *__restrict__ assign, int B, int strategy,
+                 const double *__restrict__ jit, long long jit_stride,
+                 double *__restrict__ makespan, int32_t *__restrict__ status,
+                 fp_event *__restrict__ trace, int trace_cap, int32_t *__restrict__ trace_len,
+                 uint8_t *__restrict__ blocked, int64_t smem_per_ep) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int warp = threadIdx.x >> 5;
+    const int ep = blockIdx.x * WARPS + warp;
+    if (ep >= B) return;
+    SimSmem S = sim_carve(smem + warp * smem_per_ep, P);
+    const int32_t *row = assign + (size_t)ep * P.n;
+    for (int v = lane_id(); v < P.n; v += 32) S.assign[v] = (uint8_t)row[v];
+    __syncwarp();
+    SimOut o = sim_episode(P, S, strategy, jit ? jit + (size_t)ep * jit_stride : nullptr,
+                           trace ? trace + (size_t)ep * trace_cap : nullptr, trace_cap,
+                           blocked ? blocked + (size_t)ep * P.n : nullptr);
+    if (lane_id() == 0) {
+        makespan[ep] = o.makespan;
+        status[ep] = o.status;
+        if (trace_len) trace_len[ep] = o.n_events;
+    }
+}
+
+static int launch_sim(const fp_problem *p, const int32_t *assign, int B, int strategy,
+                      const double *jit, long long jstride, double *mk, int32_t *st,
+                      fp_event *trace, int cap, int32_t *tlen, uint8_t *blocked,
+                      cudaStream_t stream) {
+    constexpr int WARPS = 4;
+    const int64_t per = p->sim_smem;
+    const int64_t smem = per * WARPS;
+    if (smem > 227 * 1024) {
+        set_error("simulator state exceeds shared memory (n/d too large for the smem core)");
+        return FP_ERR_UNSUPPORTED;
+    }
+    auto kern = sim_batch_kernel<WARPS>;
+    FP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int grid = (B + WARPS - 1) / WARPS;
+    kern<<<grid, WARPS * 32, smem, stream>>>(p->dev, assign, B, strategy, jit, jstride, mk, st,
+                                             trace, cap, tlen, blocked, per);
+    FP_CUDA(cudaGetLastError());
+    return FP_OK;
+}
+
+}  // namespace fp
+
+using namespace fp;
+
+extern "C" {
+
+const char *fp_last_error(void) { return g_err.c_str(); }
+int fp_version(void) { return 1; }
+
+int fp_problem_create(const fp_graph_desc *g, fp_problem **out) {
+    if (!g || !out) { set_error("null argument"); return FP_ERR_INVALID; }
+    const int n = g->n, d = g->d;
+    if (n < 0 || d < 1 || d > kMaxDevices) {
+        set_error("need n >= 0 and 1 <= d <= 32");
+        return FP_ERR_UNSUPPORTED;
+    }
+    const int E = g->pred_indptr[n];
+    if (g->succ_indptr[n] != E) { set_error("pred/succ edge counts differ"); return FP_ERR_INVALID; }
+    for (int v = 0; v < E; ++v) {
+        if (g->pred_indices[v] < 0 || g->pred_indices[v] >= n || g->succ_indices[v] < 0 ||
+            g->succ_indices[v] >= n) {
+            set_error("edge endpoint out of range");
+            return FP_ERR_INVALID;
+        }
+    }
+    const int R = d + d * d;
+    std::vector<int> slots(R, 0), pool_off(R + 1, 0);
+    for (int a = 0; a < d; ++a) slots[a] = g->eslots[a];
+    for (int a = 0; a < d; ++a)
+        for (int b = 0; b < d; ++b) slots[d + a * d + b] = a == b ? 0 : g->tslots[a * d + b];
+    for (int r = 0; r < R; ++r) {
+        if (slots[r] < 0) { set_error("negative slot count"); return FP_ERR_INVALID; }
+        pool_off[r + 1] = pool_off[r] + slots[r];
+    }
+    std::vector<double> tl(n, 0.0), bl(n, 0.0);
+    if (g->tlev) std::copy(g->tlev, g->tlev + n, tl.begin());
+    if (g->blev) std::copy(g->blev, g->blev + n, bl.begin());
+    // strategy orders: fifo = id; depth_first = tlev desc; breadth_first = blev asc; ties by id
+    std::vector<int> rpos(3 * n), rvert(3 * n), krank(3 * n, 0);
+    for (int s = 0; s < 3; ++s) {
+        std::vector<int> ord(n);
+        std::iota(ord.begin(), ord.end(), 0);
+        if (s == 1)
+            std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return tl[x] > tl[y]; });
+        if (s == 2)
+            std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return bl[x] < bl[y]; });
+        int k = 0;
+        for (int i = 0; i < n; ++i) {
+            const int v = ord[i];
+            if (i > 0 && s != 0) {
+                const double kv = s == 1 ? tl[v] : bl[v];
+                const double ku = s == 1 ? tl[ord[i - 1]] : bl[ord[i - 1]];
+                if (kv != ku) ++k;
+            }
+            rpos[s * n + v] = i;
+            rvert[s * n + i] = v;
+            krank[s * n + v] = k;
+        }
+    }
+    int nonentry = 0;
+    for (int v = 0; v < n; ++v) nonentry += !g->is_entry[v];
+
+    Arena A;
+    const int nn = std::max(n, 1);
+    std::vector<uint8_t> entry(g->is_entry, g->is_entry + n);
+    entry.resize(nn, 0);
+    size_t o_pp = A.put(g->pred_indptr, n + 1), o_pi = A.put(g->pred_indices, E),
+           o_sp = A.put(g->succ_indptr, n + 1), o_si = A.put(g->succ_indices, E),
+           o_en = A.put(entry.data(), nn), o_fl = A.put(g->flops, n), o_ob = A.put(g->obytes, n),
+           o_ra = A.put(g->rates, d), o_bw = A.put(g->bw, (size_t)d * d),
+           o_tl = A.put(tl.data(), n), o_bl = A.put(bl.data(), n),
+           o_sl = A.put(slots.data(), R), o_po = A.put(pool_off.data(), R + 1),
+           o_rp = A.put(rpos.data(), 3 * n), o_rv = A.put(rvert.data(), 3 * n),
+           o_kr = A.put(krank.data(), 3 * n);
+    fp_problem *p = new fp_problem();
+    FP_CUDA(cudaGetDevice(&p->device));
+    if (cudaMalloc(&p->arena, std::max<size_t>(A.size, 256)) != cudaSuccess) {
+        set_error("cudaMalloc failed for problem arena");
+        delete p;
+        return FP_ERR_CUDA;
+    }
+    uint8_t *base = (uint8_t *)p->arena;
+    for (auto &part : A.parts)
+        if (!part.second.empty())
+            FP_CUDA(cudaMemcpy(base + part.first, part.second.data(), part.second.size(),
+                               cudaMemcpyHostToDevice));
+    DevProblem &D = p->dev;
+    D.n = n; D.d = d; D.W = (n + 31) / 32; D.R = R; D.P = pool_off[R];
+    D.n_nonentry = nonentry;
+    D.comm_factor = g->comm_factor;
+    D.pred_ptr = (const int *)(base + o_pp); D.pred_idx = (const int *)(base + o_pi);
+    D.succ_ptr = (const int *)(base + o_sp); D.succ_idx = (const int *)(base + o_si);
+    D.is_entry = base + o_en;
+    D.flops = (const double *)(base + o_fl); D.obytes = (const double *)(base + o_ob);
+    D.rates = (const double *)(base + o_ra); D.bw = (const double *)(base + o_bw);
+    D.tlev = (const double *)(base + o_tl); D.blev = (const double *)(base + o_bl);
+    D.slots = (const int *)(base + o_sl); D.pool_off = (const int *)(base + o_po);
+    D.rank_pos = (const int *)(base + o_rp); D.rank_vert = (const int *)(base + o_rv);
+    D.krank = (const int *)(base + o_kr);
+    p->sim_smem = sim_smem_bytes(n, d, D.W, R, D.P);
+    *out = p;
+    return FP_OK;
+}
+
+int fp_problem_destroy(fp_problem *p) {
+    if (!p) return FP_OK;
+    if (p->arena) cudaFree(p->arena);
+    delete p;
+    return FP_OK;
+}
+
+int fp_problem_sim_smem(const fp_problem *p, int64_t *bytes) {
+    if (!p || !bytes) { set_error("null argument"); return FP_ERR_INVALID; }
+    *bytes = p->sim_smem;
+    return FP_OK;
+}
+
+int fp_sim_batch(const fp_problem *p, const int32_t *assign, int32_t B, int32_t strategy,
+                 const double *jitter, int64_t jitter_stride, double *makespan, int32_t *status,
+                 fp_event *trace, int32_t trace_cap, int32_t *trace_len, uint8_t *blocked,
+                 void *stream) {
+    if (!p || !assign || !makespan || !status) { set_error("null argument"); return FP_ERR_INVALID; }
+    if (strategy < 0 || strategy > 2) { set_error("unknown strategy"); return FP_ERR_INVALID; }
+    if (B <= 0) return FP_OK;
+    return launch_sim(p, assign, B, strategy, jitter, jitter_stride, makespan, status, trace,
+                      trace_cap, trace_len, blocked, (cudaStream_t)stream);
+}
+
+// ---- host libm jitter (the reference recipe, _simcore.pyx:15-36) ----------
+static uint64_t h_mix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+static double h_jitter(uint64_t seed, int kind, int a, int b, int c, double sigma) {
+    uint64_t h = h_mix64(seed ^ 0xD1B54A32D192ED03ULL);
+    h = h_mix64(h ^ (uint64_t)(int64_t)(kind + 1));
+    h = h_mix64(h ^ (uint64_t)(int64_t)(a + 1));
+    h = h_mix64(h ^ (uint64_t)(int64_t)(b + 2));
+    h = h_mix64(h ^ (uint64_t)(int64_t)(c + 2));
+    const double s53 = std::ldexp(1.0, -53);
+    volatile double u1 = ((double)(h >> 11) + 0.5) * s53;
+    h = h_mix64(h);
+    volatile double u2 = ((double)(h >> 11) + 0.5) * s53;
+    volatile double two_pi_u2 = 2.0 * M_PI * u2;
+    volatile double r = std::sqrt(-2.0 * std::log(u1));
+    volatile double z = r * std::cos(two_pi_u2);
+    return std::exp(sigma * z);
+}
+
+int fp_jitter_tables(int32_t n, int32_t d, double sigma, int64_t seed, double *out) {
+    if (!out || n < 0 || d < 1) { set_error("bad jitter table arguments"); return FP_ERR_INVALID; }
+    const size_t base = (size_t)n * d;
+    for (size_t i = 0; i < base + base * d; ++i) out[i] = 1.0;
+    if (sigma <= 0.0) return FP_OK;
+    for (int v = 0; v < n; ++v)
+        for (int a = 0; a < d; ++a) {
+            out[(size_t)v * d + a] = h_jitter((uint64_t)seed, 0, v, a, 0, sigma);
+            for (int b = 0; b < d; ++b)
+                if (b != a)
+                    out[base + ((size_t)v * d + a) * d + b] =
+                        h_jitter((uint64_t)seed, 1, v, a, b, sigma);
+        }
+    return FP_OK;
+}
+
+int fp_run_packed(int32_t n, int32_t d, const int32_t *pred_indptr, const int32_t *pred_indices,
+                  const int32_t *succ_indptr, const int32_t *succ_indices,
+                  const uint8_t *is_entry, const double *flops, const double *obytes,
+                  const int32_t *assign, const double *rates, const double *bw,
+                  const int32_t *eslots, const int32_t *tslots, const double *tlev,
+                  const double *blev, int32_t strategy, double comm_factor, double sigma,
+                  int64_t seed, double *makespan, fp_event *events, int64_t events_cap,
+                  int64_t *n_events, uint8_t *blocked) {
+    for (int v = 0; v < n; ++v)
+        if (assign[v] < 0 || assign[v] >= d) { set_error("assignment names a device outside the cluster"); return FP_ERR_INVALID; }
+    fp_graph_desc g{n, d, pred_indptr, pred_indices, succ_indptr, succ_indices, is_entry, flops,
+                    obytes, rates, bw, eslots, tslots, tlev, blev, comm_factor};
+    fp_problem *p = nullptr;
+    int rc = fp_problem_create(&g, &p);
+    if (rc) return rc;
+    const size_t jn = sigma > 0.0 ? (size_t)n * d * (d + 1) : 0;
+    std::vector<double> jt(jn);
+    if (jn) fp_jitter_tables(n, d, sigma, seed, jt.data());
+    const int cap = (int)std::min<int64_t>(events_cap, 2LL * (n + (int64_t)n * d) + 2);
+    // one device block: assign | jitter | makespan | status | len | blocked | trace
+    size_t off_j = ((size_t)n * 4 + 255) / 256 * 256;
+    size_t off_m = off_j + (jn * 8 + 255) / 256 * 256;
+    size_t off_b = off_m + 256;
+    size_t off_t = off_b + ((size_t)n + 255) / 256 * 256;
+    size_t total = off_t + (size_t)std::max(cap, 1) * sizeof(fp_event);
+    uint8_t *dmem = nullptr;
+    if (cudaMalloc(&dmem, total) != cudaSuccess) { fp_problem_destroy(p); set_error("cudaMalloc failed"); return FP_ERR_CUDA; }
+    auto fail = [&](int code) { cudaFree(dmem); fp_problem_destroy(p); return code; };
+    if (cudaMemcpy(dmem, assign, (size_t)n * 4, cudaMemcpyHostToDevice) != cudaSuccess ||
+        (jn && cudaMemcpy(dmem + off_j, jt.data(), jn * 8, cudaMemcpyHostToDevice) != cudaSuccess)) {
+        set_error("upload failed");
+        return fail(FP_ERR_CUDA);
+    }
+    double *d_mk = (double *)(dmem + off_m);
+    int32_t *d_st = (int32_t *)(dmem + off_m + 64), *d_len = (int32_t *)(dmem + off_m + 128);
+    rc = launch_sim(p, (const int32_t *)dmem, 1, strategy, jn ? (const double *)(dmem + off_j) : nullptr,
+                    0, d_mk, d_st, events ? (fp_event *)(dmem + off_t) : nullptr, cap, d_len,
+                    dmem + off_b, 0);
+    if (rc) return fail(rc);
+    double mk = 0.0;
+    int32_t st = 0, len = 0;
+    if (cudaMemcpy(&mk, d_mk, 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(&st, d_st, 4, cudaMemcpyDeviceToHost) != cudaSuccess ||
+        cudaMemcpy(&len, d_len, 4, cudaMemcpyDeviceToHost) != cudaSuccess) {
+        set_error(std::string("simulator kernel failed: ") + cudaGetErrorString(cudaGetLastError()));
+        return fail(FP_ERR_CUDA);
+    }
+    if (events && len > 0 &&
+        cudaMemcpy(events, dmem + off_t, (size_t)std::min(len, cap) * sizeof(fp_event),
+                   cudaMemcpyDeviceToHost) != cudaSuccess) {
+        set_error("event download failed");
+        return fail(FP_ERR_CUDA);
+    }
+    if (blocked && st == FP_EP_DEADLOCK)
+        cudaMemcpy(blocked, dmem + off_b, (size_t)n, cudaMemcpyDeviceToHost);
+    *makespan = mk;
+    if (n_events) *n_events = len;
+    cudaFree(dmem);
+    fp_problem_destroy(p);
+    if (st == FP_EP_DEADLOCK) { set_error("deadlock"); return FP_ERR_DEADLOCK; }
+    if (st == FP_EP_TRACE_OVERFLOW) { set_error("event buffer too small"); return FP_ERR_OVERFLOW; }
+    return FP_OK;
+}
+
+}  // extern "C"

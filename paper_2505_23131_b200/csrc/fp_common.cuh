@@ -1,0 +1,76 @@
+// Shared device helpers for the flowplace B200 kernels (sm_100a).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define FP_FULL_MASK 0xffffffffu
+
+namespace fp {
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FP_FULL_MASK, v, o);
+    return v;
+}
+
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(FP_FULL_MASK, v, o));
+    return v;
+}
+
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(FP_FULL_MASK, v, o));
+    return v;
+}
+
+// Inclusive prefix sum across the warp (lane order).
+template <typename T>
+__device__ __forceinline__ T warp_inclusive_scan(T v) {
+    const int l = lane_id();
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T u = __shfl_up_sync(FP_FULL_MASK, v, o);
+        if (l >= o) v += u;
+    }
+    return v;
+}
+
+// ---------------------------------------------------------------------------
+// Philox4x32-10 (Salmon et al., SC'11).  Counter = (episode, step, head, 0),
+// key = (seed lo, seed hi).  Known-answer vectors checked in the tests.
+// ---------------------------------------------------------------------------
+struct U4 { uint32_t x, y, z, w; };
+
+__host__ __device__ __forceinline__ void mulhilo32(uint32_t a, uint32_t b, uint32_t& hi,
+                                                   uint32_t& lo) {
+    uint64_t p = (uint64_t)a * (uint64_t)b;
+    hi = (uint32_t)(p >> 32);
+    lo = (uint32_t)p;
+}
+
+__host__ __device__ __forceinline__ U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+        uint32_t hi0, lo0, hi1, lo1;
+        mulhilo32(0xD2511F53u, c.x, hi0, lo0);
+        mulhilo32(0xCD9E8D57u, c.z, hi1, lo1);
+        c = U4{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};
+    }
+    return c;
+}
+
+// Two uniforms in [0, 1) with 53 random bits each.
+__host__ __device__ __forceinline__ void uniform2(U4 r, double& u1, double& u2) {
+    const double s = 1.0 / 9007199254740992.0;  // 2^-53
+    u1 = (double)((((uint64_t)r.y << 32) | r.x) >> 11) * s;
+    u2 = (double)((((uint64_t)r.w << 32) | r.z) >> 11) * s;
+}
+
+}  // namespace fp

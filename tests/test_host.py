@@ -1,0 +1,68 @@
+"""CPU: host-side mirror of the reference API (builders, features, JSON) and
+the C-ABI library surface (loads, exports every symbol include/*.h declares)."""
+import ctypes
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2505_23131_b200 import builders, graph as G
+from paper_2505_23131_b200.features import static_features
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def test_builder_golden_counts():
+    # reference tests/test_builders.py:74-117
+    g = builders.build_chainmm(8, 2)
+    assert (len(g), len(g.edges), len(g.meta_ops)) == (60, 80, 4)
+    g = builders.build_ffnn(8, 4, 16, 4, 2)
+    assert (len(g), len(g.edges), len(g.meta_ops)) == (64, 92, 9)
+    assert len(builders.build_chainmm(8, 1)) == 9
+    assert len(builders.build_ffnn(8, 4, 16, 4, 1)) == 14
+
+
+def test_llama_builders_golden_counts():
+    b = builders.build_llama_block()
+    assert (len(b), len(b.edges), len(b.meta_ops), len(b.entry_vertices())) == (208, 324, 27, 36)
+    layer = builders.build_llama_layer()
+    assert (len(layer), len(layer.edges), len(layer.meta_ops)) == (248, 392, 35)
+    for g in (b, layer):
+        assert G.validate(g) == []
+        assert G.graph_from_dict(G.graph_to_dict(g)).edges == g.edges
+
+
+def test_builders_match_reference_graphs(sim_golden):
+    want = {c["tag"].split("#")[0]: c["graph"] for c in sim_golden
+            if c["tag"].startswith(("chainmm60", "ffnn64"))}
+    assert G.graph_to_dict(builders.build_chainmm(64, 2)) == want["chainmm60"]
+    assert G.graph_to_dict(builders.build_ffnn(8, 4, 16, 4, 2)) == want["ffnn64"]
+
+
+def test_sparse_dag_is_valid_and_sparse():
+    g = builders.sparse_dag(2000, seed=0)
+    assert G.validate(g) == []
+    assert len(g.edges) < 2.1 * len(g)
+    assert len(g.entry_vertices()) == 100
+
+
+def test_graph_json_errors():
+    with pytest.raises(G.GraphFormatError, match="missing field: edges"):
+        G.graph_from_dict({"vertices": [], "meta_ops": []})
+    with pytest.raises(G.GraphValidationError, match="empty-graph"):
+        G.graph_from_dict({"vertices": [], "edges": [], "meta_ops": []})
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2505_23131_b200 import _build, _native
+    header = (ROOT / "include" / "flowplace_b200.h").read_text()
+    declared = set(re.findall(r"^\s*(?:int|const char \*|void)\s*\*?\s*(fp_\w+)\s*\(", header,
+                              re.M))
+    assert {"fp_run_packed", "fp_sim_batch", "fp_problem_create"} <= declared
+    if not _build.LIB.exists():
+        _build.build()
+    lib = ctypes.CDLL(str(_build.LIB))
+    for sym in sorted(declared):
+        assert hasattr(lib, sym), sym
+    assert set(_native.EXPORTED) <= declared
