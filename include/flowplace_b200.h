@@ -110,6 +110,94 @@ int fp_run_packed(int32_t n, int32_t d, const int32_t *pred_indptr, const int32_
 /* Host libm jitter tables (the exact reference factors), layout as above. */
 int fp_jitter_tables(int32_t n, int32_t d, double sigma, int64_t seed, double *out);
 
+/* ------------------------------------------------------------------------
+ * Policy: GNN encoder + SEL/PLC heads (flowplace/policy.py:40-251).
+ * Parameters live in ONE flat float64 device vector; param_offsets maps each
+ * role to its offset (-1 = absent).  Role index for GNN tensors:
+ *   ((enc * 8 + k) * 4 + r), enc 0 = "sel" / shared "enc", 1 = "plc",
+ *   r: 0 psi.w, 1 psi.b, 2 phi.w, 3 phi.b;
+ * then FP_ROLE_SEL_Z_W .. FP_ROLE_PLC_Y_B below.  Tensors are row-major with
+ * the reference's shapes (policy.py:74-98).
+ * ------------------------------------------------------------------------ */
+#define FP_ROLE_SEL_Z_W 64
+#define FP_ROLE_SEL_Z_B 65
+#define FP_ROLE_SEL_H1_W 66
+#define FP_ROLE_SEL_H1_B 67
+#define FP_ROLE_SEL_H2_W 68
+#define FP_ROLE_SEL_H2_B 69
+#define FP_ROLE_PLC_Z_W 70
+#define FP_ROLE_PLC_Z_B 71
+#define FP_ROLE_PLC_H1_W 72
+#define FP_ROLE_PLC_H1_B 73
+#define FP_ROLE_PLC_H2_W 74
+#define FP_ROLE_PLC_H2_B 75
+#define FP_ROLE_PLC_Y_W 76
+#define FP_ROLE_PLC_Y_B 77
+#define FP_PARAM_ROLES 78
+
+/* rollout decision modes */
+#define FP_MODE_SAMPLE 0  /* epsilon-mixture draws from Philox4x32-10 */
+#define FP_MODE_GREEDY 1  /* argmax of the softmax (policy.py:308-309) */
+#define FP_MODE_FORCED 2  /* replay given (vertex, device) per step */
+#define FP_MODE_TEACHER 3 /* CriticalPathRule actions (heuristics.py:76-91) */
+
+/* device tables readable through fp_policy_table (parity / debugging) */
+#define FP_TABLE_H_SEL 0
+#define FP_TABLE_H_PLC 1
+#define FP_TABLE_SEL_LOGIT 2
+#define FP_TABLE_PLC_A 3
+#define FP_TABLE_PLC_G 4
+#define FP_TABLE_PLC_M 5
+#define FP_TABLE_PLC_C 6
+
+typedef struct fp_policy_desc {
+    int32_t hidden, k_rounds, shared_encoder;
+    double leaky_slope;
+    const double *x_static;               /* [n*5] standardized (policy.py:123) */
+    const int32_t *adj_ptr, *adj_src;     /* [n+1], [M]: messages INTO each vertex */
+    const double *adj_edge;               /* [M] standardized edge cost (policy.py:124-143) */
+    const int32_t *bpath_ptr, *bpath_idx; /* [n+1], SEL b-paths (features.py:88-95) */
+    const int32_t *tpath_ptr, *tpath_idx; /* [n+1], SEL t-paths */
+    const int64_t *param_offsets;         /* [FP_PARAM_ROLES] */
+    int64_t n_params;
+} fp_policy_desc;
+
+typedef struct fp_policy fp_policy;
+
+typedef struct fp_rollout_args {
+    int32_t B;               /* episodes in the batch */
+    int32_t mode;            /* FP_MODE_* */
+    double epsilon;          /* exploration mixture weight */
+    uint64_t seed;           /* Philox key */
+    uint32_t episode_base;   /* Philox counter of episode 0 (rank offset) */
+    int32_t strategy;        /* simulator strategy for the reward */
+    int32_t simulate;        /* 1: score every episode with the WC simulator */
+    const int32_t *forced;   /* [B][n][2] (vertex, device) per step, FORCED */
+    int32_t *assign;         /* [B][n] out: device of each vertex */
+    int32_t *step_vd;        /* [B][n][2] out or NULL */
+    double *step_lp;         /* [B][n][2] out or NULL: (sel, plc) log-prob */
+    double *step_ent;        /* [B][n][2] out or NULL: (sel, plc) entropy */
+    int32_t *step_argmax;    /* [B][n][2] out or NULL: greedy (vertex, device) */
+    int32_t *step_ncand;     /* [B][n] out or NULL: candidate-set size */
+    double *makespan;        /* [B] out (simulate = 1) */
+    int32_t *status;         /* [B] out: FP_EP_* */
+    double *grad_rows;       /* [B][n][4][hidden] out or NULL: REINFORCE rows */
+    double *grad_ep;         /* [B][fp_grad_ep_stride] out (with grad_rows) */
+    fp_event *trace;         /* optional simulator trace [B][trace_cap] */
+    int32_t trace_cap;
+    int32_t *trace_len;
+} fp_rollout_args;
+
+int fp_policy_create(const fp_problem *p, const fp_policy_desc *desc, fp_policy **out);
+int fp_policy_destroy(fp_policy *pol);
+/* GNN encode + head tables for one parameter snapshot (params: device flat). */
+int fp_policy_prepare(fp_policy *pol, const double *params, void *stream);
+int fp_policy_table(const fp_policy *pol, int32_t which, const double **ptr, int64_t *count);
+/* Batched SEL/PLC episodes (+ fused WC simulation) — one warp per episode. */
+int fp_rollout_batch(const fp_problem *p, const fp_policy *pol, const fp_rollout_args *args,
+                     void *stream);
+int fp_grad_ep_stride(const fp_policy *pol, int32_t d, int64_t *stride);
+
 #ifdef __cplusplus
 }
 #endif

@@ -85,3 +85,41 @@ EXPORTED = (
     "fp_last_error", "fp_version", "fp_problem_create", "fp_problem_destroy",
     "fp_problem_sim_smem", "fp_sim_batch", "fp_run_packed", "fp_jitter_tables",
 )
+
+
+PARAM_ROLES = 78
+ROLE_BY_HEAD = {
+    "sel.z.w": 64, "sel.z.b": 65, "sel.head1.w": 66, "sel.head1.b": 67, "sel.head2.w": 68,
+    "sel.head2.b": 69, "plc.z.w": 70, "plc.z.b": 71, "plc.head1.w": 72, "plc.head1.b": 73,
+    "plc.head2.w": 74, "plc.head2.b": 75, "plc.y.w": 76, "plc.y.b": 77,
+}
+MODE = {"sample": 0, "greedy": 1, "forced": 2, "teacher": 3}
+TABLE = {"H_sel": 0, "H_plc": 1, "sel_logit": 2, "A": 3, "G": 4, "M": 5, "c": 6}
+
+
+def gnn_role(enc: int, k: int, r: int) -> int:
+    return (enc * 8 + k) * 4 + r
+
+
+class FpPolicyDesc(ctypes.Structure):
+    _fields_ = [("hidden", ctypes.c_int32), ("k_rounds", ctypes.c_int32),
+                ("shared_encoder", ctypes.c_int32), ("leaky_slope", ctypes.c_double)] + [
+        (name, ctypes.c_void_p) for name in (
+            "x_static", "adj_ptr", "adj_src", "adj_edge", "bpath_ptr", "bpath_idx",
+            "tpath_ptr", "tpath_idx", "param_offsets")] + [("n_params", ctypes.c_int64)]
+
+
+class FpRolloutArgs(ctypes.Structure):
+    _fields_ = [("B", ctypes.c_int32), ("mode", ctypes.c_int32), ("epsilon", ctypes.c_double),
+                ("seed", ctypes.c_uint64), ("episode_base", ctypes.c_uint32),
+                ("strategy", ctypes.c_int32), ("simulate", ctypes.c_int32)] + [
+        (name, ctypes.c_void_p) for name in (
+            "forced", "assign", "step_vd", "step_lp", "step_ent", "step_argmax", "step_ncand",
+            "makespan", "status", "grad_rows", "grad_ep", "trace")] + [
+        ("trace_cap", ctypes.c_int32), ("trace_len", ctypes.c_void_p)]
+
+
+EXPORTED = EXPORTED + (
+    "fp_policy_create", "fp_policy_destroy", "fp_policy_prepare", "fp_policy_table",
+    "fp_rollout_batch", "fp_grad_ep_stride",
+)

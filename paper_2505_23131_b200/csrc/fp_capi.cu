@@ -42,7 +42,7 @@ struct Arena {
 };
 
 template <int WARPS>
-__global__ void __launch_bounds__(WARPS * 32)
+__global__ void __launch_bounds__(WARPS * 32, 1)
 sim_batch_kernel(DevProblem P, const int32_t *__restrict__ assign, int B, int strategy,
                  const double *__restrict__ jit, long long jit_stride,
                  double *__restrict__ makespan, int32_t *__restrict__ status,

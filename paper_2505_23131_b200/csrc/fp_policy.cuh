@@ -1,0 +1,78 @@
+// Device-side policy state: parameter roles in the flat float64 vector, the
+// per-graph encoding constants, and the per-snapshot tables the rollout
+// kernel consumes:
+//   s[v]          SEL logit of vertex v (static per snapshot in per_episode mode)
+//   A[v], G[v]    PLC pre-activation tables: pre(v, d) = A[v] + S_d + xn_d @ M + c,
+//                 S_d = sum of G[u] over vertices already placed on d
+//   M (5 x h), c  device-feature and bias terms folded through head1
+#pragma once
+
+#include <cstdint>
+
+#include "fp_problem.cuh"
+
+namespace fp {
+
+constexpr int kMaxRounds = 8;
+constexpr int kMaxHidden = 64;
+
+// Parameter roles.  GNN role index: ((enc * kMaxRounds + k) * 4 + r), enc 0 =
+// "sel" (or the shared "enc"), 1 = "plc"; r: 0 psi.w, 1 psi.b, 2 phi.w, 3 phi.b.
+enum : int {
+    PR_GNN_BASE = 0,
+    PR_SEL_Z_W = 2 * kMaxRounds * 4,
+    PR_SEL_Z_B,
+    PR_SEL_H1_W,
+    PR_SEL_H1_B,
+    PR_SEL_H2_W,
+    PR_SEL_H2_B,
+    PR_PLC_Z_W,
+    PR_PLC_Z_B,
+    PR_PLC_H1_W,
+    PR_PLC_H1_B,
+    PR_PLC_H2_W,
+    PR_PLC_H2_B,
+    PR_PLC_Y_W,
+    PR_PLC_Y_B,
+    PR_COUNT
+};
+
+__host__ __device__ inline int gnn_role(int enc, int k, int r) {
+    return PR_GNN_BASE + (enc * kMaxRounds + k) * 4 + r;
+}
+
+struct DevPolicy {
+    int n, h, K, n_enc;  // n_enc = 1 (shared) or 2
+    double slope;
+    const double *params;          // flat float64 (set by prepare)
+    double *grad;                  // flat float64 gradient (backward)
+    int64_t off[PR_COUNT];
+    // per-graph encoding constants
+    const double *x;               // [n][5] standardized static features
+    const int *adj_ptr, *adj_nbr;  // messages INTO v: source vertices, message order
+    const double *adj_e;           // standardized edge cost per message
+    const int *bp_ptr, *bp_idx, *tp_ptr, *tp_idx;     // SEL b/t paths
+    const int *ibp_ptr, *ibp_idx, *itp_ptr, *itp_idx; // inverse paths (u -> v with u in path(v))
+    // workspace (per snapshot)
+    double *H[2][kMaxRounds + 1];  // layer inputs/outputs; H[e][0] is [n][7]
+    double *Pm[2][kMaxRounds];     // H[e][k] @ psi.w rows [0, d)
+    double *Qm[2][kMaxRounds];     // H[e][k] @ psi.w rows [d, 2d)
+    double *U[2][kMaxRounds];      // phi pre-activations
+    double *Zs, *emb, *hidpre, *s; // SEL tables
+    double *Zp, *A, *G, *M, *c;    // PLC tables
+    // backward workspace
+    double *dH[2], *dHn[2], *dU, *Dsrc, *Ddst, *dagg;
+    double *ds, *dA, *dG, *dsmall; // reduced gradient tables
+    double *partial;               // block partials for weight gradients
+    int partial_rows;
+
+    __device__ __forceinline__ const double *W(int role) const { return params + off[role]; }
+};
+
+}  // namespace fp
+
+struct fp_policy {
+    fp::DevPolicy dev;
+    void *arena = nullptr;
+    const fp_problem *problem = nullptr;
+};

@@ -87,7 +87,7 @@ __device__ __forceinline__ uint64_t sim_task_key(int krank, int kind, int v, int
 
 // Runs one episode.  S.assign must hold the assignment (written by the caller
 // and made visible with __syncwarp).  All 32 lanes must call.
-__device__ SimOut sim_episode(const DevProblem &P, const SimSmem &S, int strategy,
+static __device__ SimOut sim_episode(const DevProblem &P, const SimSmem &S, int strategy,
                               const double *__restrict__ jit, fp_event *__restrict__ trace,
                               int trace_cap, uint8_t *__restrict__ blocked) {
     const int lane = lane_id();

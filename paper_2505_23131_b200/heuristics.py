@@ -1,0 +1,70 @@
+"""Assignments and the critical-path rule (mirror of reference
+``heuristics.py:35-91``).  ``CriticalPathRule`` is the imitation teacher; the
+CUDA rollout executes it natively (FP_MODE_TEACHER), so here it only carries
+identity and the host-side reference semantics for single calls."""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+@dataclass(frozen=True)
+class Assignment:
+    device_of: tuple[int, ...]
+    engine: str = ""
+
+    def __getitem__(self, v: int) -> int:
+        return self.device_of[v]
+
+    def __iter__(self):
+        return iter(self.device_of)
+
+    def __len__(self) -> int:
+        return len(self.device_of)
+
+
+def validate_assignment(graph, assignment, device_count: int) -> list[str]:
+    devs = list(assignment)
+    if len(devs) != len(graph):
+        return [f"not-total: {len(devs)} entries for {len(graph)} vertices"]
+    return [f"bad-device: vertex {v} on device {d} of {device_count}"
+            for v, d in enumerate(devs) if not 0 <= d < device_count]
+
+
+def single_device_assign(graph) -> Assignment:
+    return Assignment((0,) * len(graph), "single")
+
+
+def random_assign(graph, devices: int, seed: int = 0) -> Assignment:
+    rng = np.random.default_rng(seed)
+    return Assignment(tuple(int(d) for d in rng.integers(0, devices, size=len(graph))), "random")
+
+
+class CriticalPathRule:
+    """Select the candidate with the largest t-level (ties: smallest id);
+    place on the earliest-start device (ties: smallest id).  Executed on the
+    GPU inside the rollout kernel when passed as ``teacher``."""
+
+    def __init__(self, graph, cluster, features):
+        self.graph = graph
+        self.cluster = cluster
+        self.features = features
+
+    def select(self, candidates, rng=None) -> int:
+        tlev = self.features.t_level
+        best = max(tlev[v] for v in candidates)
+        top = [v for v in candidates if tlev[v] == best]
+        if rng is None or len(top) == 1:
+            return top[0]
+        return top[int(rng.integers(len(top)))]
+
+
+class ForcedActions:
+    """Teacher that replays a recorded (vertex, device) sequence — the
+    teacher-forced parity harness of north_star (one list per episode, or a
+    [B, n, 2] array for batches)."""
+
+    def __init__(self, actions):
+        self.actions = np.asarray(actions, dtype=np.int32)

@@ -1,0 +1,159 @@
+"""GPU: CUDA policy path (encode + fused rollout/simulation) vs the reference
+(golden traces, teacher-forced actions bit-exact) and the numpy oracle
+(same Philox draws -> same sampled actions; log-probs within 1e-9)."""
+import numpy as np
+import pytest
+
+from helpers import graph_from_golden
+from oracle import policy as OP
+from oracle import sim as osim
+from paper_2505_23131_b200 import builders
+from paper_2505_23131_b200.cluster import ClusterSpec
+from paper_2505_23131_b200.heuristics import CriticalPathRule, ForcedActions
+from paper_2505_23131_b200.params import init_policy_params
+from paper_2505_23131_b200.policy import PolicyConfig, PolicyContext, TeacherActionError
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available()
+    return torch
+
+
+def _ctx(case):
+    g = graph_from_golden(case["graph"])
+    cl = ClusterSpec.from_dict(case["cluster"])
+    pc = PolicyConfig.from_dict(case["policy"])
+    return g, cl, pc, PolicyContext(g, cl, pc)
+
+
+def _close(a, b, tol=TOL):
+    return abs(a - b) <= tol * max(1.0, abs(b))
+
+
+def _check_steps(trace, want, actions=True):
+    assert len(trace.steps) == len(want)
+    for s, w in zip(trace.steps, want):
+        if actions:
+            assert list(s.candidates) == w["candidates"]
+            assert (s.vertex, s.device) == (w["vertex"], w["device"])
+        for k in ("sel_logprob", "plc_logprob", "sel_entropy", "plc_entropy"):
+            assert _close(getattr(s, k), w[k]), (k, getattr(s, k), w[k])
+        assert (s.sel_argmax, s.plc_argmax) == (w["sel_argmax"], w["plc_argmax"])
+
+
+def test_encoder_tables_match_reference(policy_golden, torch_cuda):
+    for case in policy_golden["cases"]:
+        g, cl, pc, ctx = _ctx(case)
+        ctx.prepare(init_policy_params(pc, seed=0))
+        for name, key in (("H_sel", "H_sel"), ("H_plc", "H_plc")):
+            np.testing.assert_allclose(ctx.read_table(name), np.asarray(case[key]),
+                                       rtol=1e-11, atol=1e-12, err_msg=case["tag"])
+
+
+def test_teacher_greedy_and_forced_match_reference(policy_golden, torch_cuda):
+    for case in policy_golden["cases"]:
+        g, cl, pc, ctx = _ctx(case)
+        params = init_policy_params(pc, seed=0)
+        teacher = CriticalPathRule(g, cl, ctx.features)
+        a, tr = ctx.rollout(params, case["teacher"]["epsilon"], 0, teacher=teacher)
+        _check_steps(tr, case["teacher"]["trace"])
+        assert tr.encode_invocations == 2
+        a, tr = ctx.rollout(params, 0.0, 0, greedy=True)
+        _check_steps(tr, case["greedy"]["trace"])
+        for s in case["sampled"]:
+            acts = [(x["vertex"], x["device"]) for x in s["trace"]]
+            a, tr = ctx.rollout(params, s["epsilon"], 0, teacher=ForcedActions(acts))
+            assert list(a) == s["assign"]
+            _check_steps(tr, s["trace"])
+
+
+def test_bad_forced_action_raises(policy_golden, torch_cuda):
+    case = policy_golden["cases"][0]
+    g, cl, pc, ctx = _ctx(case)
+    acts = [(999, 0)] * len(g)
+    with pytest.raises(TeacherActionError):
+        ctx.rollout(init_policy_params(pc, seed=0), 0.0, 0, teacher=ForcedActions(acts))
+
+
+def _oracle_ctx(ctx):
+    pc = ctx.config
+    return OP.Ctx(ctx.graph, ctx.cluster, pc.hidden, pc.k_rounds, pc.leaky_slope,
+                  pc.shared_encoder, ctx.features)
+
+
+@pytest.mark.parametrize("which", ["ffnn", "chainmm", "llama"])
+def test_sampled_batch_matches_oracle_draws(which, torch_cuda):
+    if which == "ffnn":
+        g, cl, pc = builders.build_ffnn(8, 4, 16, 4, 2), ClusterSpec.uniform(8, 1e6, 1e5), \
+            PolicyConfig()
+    elif which == "chainmm":
+        g, cl, pc = builders.build_chainmm(64, 2), ClusterSpec.uniform(4, 1e6, 1e5), \
+            PolicyConfig(hidden=16, k_rounds=1, shared_encoder=True)
+    else:
+        g, cl, pc = builders.build_llama_block(), ClusterSpec.uniform(8, 1e9, 1e7), PolicyConfig()
+    params = init_policy_params(pc, seed=3)
+    ctx = PolicyContext(g, cl, pc)
+    B, seed, base = 64, 1234, 7
+    rb = ctx.rollout_batch(params, B, 0.2, seed, trace_steps=True, episode_base=base)
+    st = rb.status.cpu().numpy()
+    assert (st == 0).all()
+    vd = rb.step_vd.cpu().numpy()
+    lp = rb.step_lp.cpu().numpy()
+    ent = rb.step_ent.cpu().numpy()
+    mk = rb.makespan.cpu().numpy()
+    assign = rb.assign.cpu().numpy()
+    octx = _oracle_ctx(ctx)
+    P = OP.leaves(params, need=False)
+    check = range(B) if which != "llama" else range(0, B, 16)
+    for b in check:
+        ro = OP.rollout(P, octx, 0.2, mode="uniform", seed=seed, episode=base + b)
+        got = [(int(vd[b, t, 0]), int(vd[b, t, 1])) for t in range(len(g))]
+        want = [(s["vertex"], s["device"]) for s in ro["steps"]]
+        assert got == want, (which, b)
+        for t, s in enumerate(ro["steps"]):
+            assert _close(lp[b, t, 0], s["sel_logprob"]) and _close(lp[b, t, 1], s["plc_logprob"])
+            assert _close(ent[b, t, 0], s["sel_entropy"]) and _close(ent[b, t, 1], s["plc_entropy"])
+        assert list(assign[b]) == ro["assign"]
+        omk, _ = osim.exec_time(g, assign[b], cl)
+        assert mk[b] == omk
+
+
+def test_fused_simulation_trace_bit_exact(torch_cuda):
+    from paper_2505_23131_b200.simulate import decode_events
+    g, cl = builders.build_ffnn(8, 4, 16, 4, 2), ClusterSpec.uniform(8, 1e6, 1e5)
+    pc = PolicyConfig()
+    ctx = PolicyContext(g, cl, pc)
+    for strat in ("fifo", "depth_first", "breadth_first"):
+        rb = ctx.rollout_batch(init_policy_params(pc, 0), 32, 0.5, 99, strategy=strat,
+                               sim_trace=True)
+        assign = rb.assign.cpu().numpy()
+        tr = rb.trace.cpu().numpy()
+        tl = rb.trace_len.cpu().numpy()
+        mk = rb.makespan.cpu().numpy()
+        for b in range(32):
+            omk, oev = osim.exec_time(g, assign[b], cl, strat)
+            assert mk[b] == omk
+            assert decode_events(tr[b], int(tl[b])) == oev
+
+
+def test_epsilon_one_is_uniform(torch_cuda):
+    from paper_2505_23131_b200.graph import DataflowGraph, OpKind, Vertex
+    g = DataflowGraph((Vertex(0, OpKind.MATMUL, 10, 8, "a"), Vertex(1, OpKind.MATMUL, 10, 8, "b")),
+                      ())
+    cl = ClusterSpec.uniform(2, 1000.0, 256.0)
+    pc = PolicyConfig(hidden=8)
+    ctx = PolicyContext(g, cl, pc)
+    B = 20000
+    rb = ctx.rollout_batch(init_policy_params(pc, 0), B, 1.0, 5, trace_steps=True)
+    a = rb.assign.cpu().numpy()
+    counts = np.zeros((2, 2))
+    np.add.at(counts, (a[:, 0], a[:, 1]), 1)
+    sigma = np.sqrt(B * 0.25 * 0.75)
+    assert np.all(np.abs(counts - B / 4) <= 4 * sigma)
+    lp = rb.step_lp.cpu().numpy()
+    assert np.allclose(lp[:, :, 1], np.log(0.5), atol=1e-12)
