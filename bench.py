@@ -1,0 +1,358 @@
+"""Throughput bench for the DOPPLER rollout hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload ffnn]
+                    [--batch B] [--mode rollout|train] [--impl ours|reference]
+
+One step = one pass of the hot path over one batch: encode the graph for the
+parameter snapshot (GNN + head tables), run B SEL/PLC episodes (epsilon 0.2
+Philox sampling) each scored by the work-conserving simulator (config 2 of
+BASELINE.json: FFNN graph, 8 simulated devices, 1024 episodes per GPU).
+``--mode train`` adds the Stage-II REINFORCE update (reduction, backward,
+NCCL allreduce of the gradient, SGD).  N>1: one process per GPU (torchrun),
+episodes sharded (weak scaling), time = max over ranks.
+
+``--impl reference`` times the reference algorithm's CPU implementation (the
+oracle port: numpy rollout structured like flowplace/policy.py + the C
+restatement of flowplace/_simcore.pyx) on all host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import multiprocessing as mp
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "simulated placement episodes/sec"
+UNIT = "episodes/s"
+EPSILON = 0.2
+
+
+def workload(name: str):
+    from paper_2505_23131_b200 import builders
+    from paper_2505_23131_b200.cluster import ClusterSpec
+    if name == "ffnn":
+        return (builders.build_ffnn(8, 4, 16, 4, 2),
+                ClusterSpec.uniform(8, rate=1e6, bandwidth=1e5, comm_factor=4),
+                "FFNN build_ffnn(8,4,16,4,2): 64 ops / 92 edges, 8 devices")
+    if name == "chainmm":
+        return (builders.build_chainmm(64, 2),
+                ClusterSpec.uniform(4, rate=1e6, bandwidth=1e5, comm_factor=4),
+                "ChainMM build_chainmm(64,2): 60 ops / 80 edges, 4 devices")
+    if name == "llama_block":
+        return (builders.build_llama_block(), ClusterSpec.uniform(8, rate=1e9, bandwidth=1e7),
+                "Llama-7B block (shard_grid 2): 208 ops / 324 edges, 8 devices")
+    if name == "llama_layer":
+        return (builders.build_llama_layer(), ClusterSpec.uniform(8, rate=1e9, bandwidth=1e7),
+                "Llama-7B layer + LM head (shard_grid 2): 248 ops / 392 edges, 8 devices")
+    if name.startswith("dag"):
+        n = int(name[3:].replace("k", "000"))
+        return (builders.sparse_dag(n, seed=0), ClusterSpec.uniform(8, rate=1e9, bandwidth=1e7),
+                f"sparse DAG {n} ops, 8 devices")
+    raise SystemExit(f"unknown workload {name}")
+
+
+# --------------------------------------------------------------------------- CPU
+def _cpu_worker(args):
+    """Reference-algorithm episodes on one core until the deadline."""
+    wl, seed0, deadline, train = args
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from oracle import policy as OP
+    from oracle import sim as osim
+    from paper_2505_23131_b200.params import init_policy_params
+    from paper_2505_23131_b200.policy import PolicyConfig
+    g, cl, _ = workload(wl)
+    pc = PolicyConfig()
+    params = init_policy_params(pc, seed=0)
+    ctx = OP.Ctx(g, cl, pc.hidden, pc.k_rounds, pc.leaky_slope, pc.shared_encoder)
+    packed = osim.pack(g, [0] * len(g), cl, ctx.f, "fifo", 0)
+    done = 0
+    t0 = time.perf_counter()
+    while time.perf_counter() < deadline or done == 0:
+        if train:
+            _, ro = OP.rl_gradients(params, ctx, EPSILON, -1.0, 1e-2, mode="uniform",
+                                    seed=seed0, episode=done)
+        else:
+            ro = OP.rollout(OP.leaves(params), ctx, EPSILON, mode="uniform", seed=seed0,
+                            episode=done)
+        osim.sim_batch(packed, np.asarray([ro["assign"]], dtype=np.int32))
+        done += 1
+    return done, time.perf_counter() - t0
+
+
+def cpu_throughput(wl: str, seconds: float, procs: int, train: bool = False):
+    deadline = time.perf_counter() + seconds
+    if procs == 1:
+        res = [_cpu_worker((wl, 1000, deadline, train))]
+    else:
+        with mp.get_context("fork").Pool(procs) as pool:
+            res = pool.map(_cpu_worker, [(wl, 1000 + i, deadline, train) for i in range(procs)])
+    eps = sum(r[0] for r in res)
+    wall = max(r[1] for r in res)
+    return eps / wall, eps, wall
+
+
+# --------------------------------------------------------------------------- clocks
+class Clocks:
+    def __init__(self, path: Path):
+        self.path = path
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self, gpu_index: int):
+        try:
+            rows = [r.split(", ") for r in self.path.read_text().strip().splitlines()]
+        except OSError:
+            return None
+        rows = [r for r in rows if len(r) >= 9 and r[0].strip() == str(gpu_index)]
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].strip() == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(rows[0][2]) if rows[0][2].strip().replace(".", "").isdigit()
+                else None, "reasons": reasons, "samples": len(rows)}
+
+
+# --------------------------------------------------------------------------- GPU
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2505_23131_b200.params import init_policy_params
+    from paper_2505_23131_b200.policy import PolicyConfig, PolicyContext
+
+    g, cl, desc = workload(args.workload)
+    n = len(g)
+    pc = PolicyConfig()
+    params = init_policy_params(pc, seed=0)
+    ctx = PolicyContext(g, cl, pc)
+    B = args.batch
+    train = args.mode == "train"
+    trainer = None
+    if train:
+        from paper_2505_23131_b200.training import BatchedTrainer, TrainConfig
+        trainer = BatchedTrainer(ctx, params, TrainConfig(episodes=10 ** 6), batch_size=B,
+                                 world=world, rank=rank)
+    flat = ctx.flat_params(params)
+    out = ctx.alloc_batch(B, grad=train)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    ep_base = rank * B
+
+    def step(i):
+        seed = 0x5EED0000 + i
+        if train:
+            trainer.step(seed=seed, out=out)
+        else:
+            ctx.rollout_batch(flat, B, EPSILON, seed, episode_base=ep_base, out=out)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+
+    # ---- device-timed steps (L2 flushed between steps, outside the events) ----
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    clk = Clocks(ROOT / "gpurun_out" / f"clocks_rank{rank}.csv") if rank == 0 else None
+    (ROOT / "gpurun_out").mkdir(exist_ok=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    if clk:
+        clk.__enter__()
+        time.sleep(0.3)
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        ev[i][0].record(stream)
+        if train:
+            trainer.step(seed=0x7000 + i, out=out, kernel_events=kev[i])
+        else:
+            ctx.prepare(flat)
+            kev[i][0].record(stream)
+            ctx.rollout_batch(flat, B, EPSILON, 0x7000 + i, episode_base=ep_base, out=out,
+                              prepare=False)
+            kev[i][1].record(stream)
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    if clk:
+        clk.__exit__()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    kern_ms = [a.elapsed_time(b) for a, b in kev]
+    tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    total_ms = float(tot.item())
+    ms_per_step = total_ms / args.steps
+    value = B * world * args.steps / (total_ms / 1e3)
+    st = out.status.cpu().numpy()
+    assert (st == 0).all(), "episode failures in the timed region"
+
+    # ---- end-to-end through the public API with host buffers ----
+    host_params = torch.from_numpy(ctx.layout.flatten(params)).pin_memory()
+    host_assign = torch.empty((B, n), dtype=torch.int32).pin_memory()
+    host_mk = torch.empty(B, dtype=torch.float64).pin_memory()
+    dev_params = torch.empty_like(flat)
+    e2e_ms = []
+    for i in range(args.warmup + args.steps):
+        flush.fill_(float(i))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        dev_params.copy_(host_params, non_blocking=True)
+        if train:
+            trainer.load_flat(dev_params)
+            trainer.step(seed=0x9000 + i, out=out)
+        else:
+            ctx.rollout_batch(dev_params, B, EPSILON, 0x9000 + i, episode_base=ep_base, out=out)
+        host_assign.copy_(out.assign, non_blocking=True)
+        host_mk.copy_(out.makespan, non_blocking=True)
+        torch.cuda.synchronize()
+        if i >= args.warmup:
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e_t = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_value = B * world * args.steps / (float(e2e_t.item()) / 1e3)
+
+    if rank == 0:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (
+            ROOT / "MEASURED_PEAKS.json").exists() else {}
+        peak = peaks.get("hbm_gbs", 6650.0)
+        kms = float(np.mean(kern_ms))
+        # algorithmic bytes of one rollout launch: per episode
+        # 4n (assign out) + 12 (makespan, status out); per launch the graph
+        # CSR + policy tables read once: (n+1)*8 + E*8 + 16n + n*8 + 2*n*h*8
+        E = len(g.edges)
+        h = pc.hidden
+        per_ep = 4 * n + 12
+        per_launch = (n + 1) * 8 + E * 8 + 16 * n + 8 * n + 2 * n * h * 8
+        alg = B * per_ep + per_launch
+        if train:
+            alg += B * n * 4 * h * 8  # REINFORCE rows written
+        achieved = alg / (kms * 1e-3) / 1e9
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (builder graph; random-init policy seed 0; Philox episodes)",
+            "config": {"workload": desc, "episodes_per_gpu": B, "global_batch": B * world,
+                       "mode": args.mode, "epsilon": EPSILON, "policy": "hidden 32, K 2",
+                       "parallelism": f"episode-dp{world}",
+                       "l2": "flushed between timed steps (256 MiB write)"},
+            "e2e": {"value": e2e_value, "unit": UNIT,
+                    "h2d_bytes_per_step": int(host_params.numel() * 8),
+                    "d2h_bytes_per_step": int(B * n * 4 + B * 8)},
+            "gpu_launches": args.steps * ((pc.k_rounds + 2) if not train else
+                                          trainer.launches_per_step()),
+            "roofline": {"bound": "hbm", "kernel": "rollout_kernel" if not train else
+                         "rollout_kernel(grad)", "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                         "kernel_ms": kms, "alg_bytes_per_launch": alg,
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
+        }
+        if clk:
+            line["clocks"] = clk.summary(local)
+        if world == 1 and not args.no_cpu:
+            v, eps_done, wall = cpu_throughput(args.workload, args.cpu_seconds, os.cpu_count(),
+                                               train)
+            line["cpu_baseline"] = {
+                "value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                "sample": f"{eps_done} episodes in {wall:.1f}s across {os.cpu_count()} "
+                          f"processes (oracle numpy rollout + C simulator)"}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    procs = os.cpu_count() or 1
+    vals = []
+    total_eps = 0
+    wall = 0.0
+    for _ in range(args.warmup):
+        cpu_throughput(args.workload, 1.0, procs, args.mode == "train")
+    for _ in range(args.steps):
+        v, e, w = cpu_throughput(args.workload, args.ref_step_seconds, procs,
+                                 args.mode == "train")
+        vals.append(v)
+        total_eps += e
+        wall += w
+    value = total_eps / wall
+    _, _, desc = workload(args.workload)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0, "impl": "reference",
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": desc, "mode": args.mode,
+                                        "epsilon": EPSILON, "policy": "hidden 32, K 2"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port",
+                         "sample": f"{total_eps} episodes over {args.steps} steps of "
+                                   f"{args.ref_step_seconds}s on {procs} processes"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="ffnn")
+    ap.add_argument("--batch", type=int, default=1024)
+    ap.add_argument("--mode", default="rollout", choices=("rollout", "train"))
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-step-seconds", type=float, default=5.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

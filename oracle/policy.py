@@ -406,7 +406,8 @@ def rollout(P, ctx, eps, mode="uniform", seed=0, episode=0, forced=None, teacher
                           sel_logprob=float(lps_.v[0, 0]), plc_logprob=float(lpp.v[0, 0]),
                           sel_entropy=float(ents_.v[0, 0]), plc_entropy=float(entp.v[0, 0]),
                           sel_argmax=cand[int(np.argmax(ps.v[0]))],
-                          plc_argmax=int(np.argmax(pp.v[0])), xd=xd))
+                          plc_argmax=int(np.argmax(pp.v[0])), xd=xd,
+                          sel_probs=ps.v[0].copy(), plc_probs=pp.v[0].copy()))
         lps += [lps_, lpp]
         ents += [ents_, entp]
     return dict(assign=list(tl.dev), steps=steps, lps=lps, ents=ents)
