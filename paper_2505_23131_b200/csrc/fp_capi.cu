@@ -41,24 +41,26 @@ struct Arena {
     }
 };
 
-template <int WARPS>
+template <int RPL, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32, 1)
-sim_batch_kernel(DevProblem P, const int32_t *__restrict__ assign, int B, int strategy,
-                 const double *__restrict__ jit, long long jit_stride,
+sim_batch_kernel(DevProblem P, EpLayout L, const int32_t *__restrict__ assign, int B,
+                 int strategy, const double *__restrict__ jit, long long jit_stride,
                  double *__restrict__ makespan, int32_t *__restrict__ status,
                  fp_event *__restrict__ trace, int trace_cap, int32_t *__restrict__ trace_len,
-                 uint8_t *__restrict__ blocked, int64_t smem_per_ep) {
+                 uint8_t *__restrict__ blocked) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int warp = threadIdx.x >> 5;
     const int ep = blockIdx.x * WARPS + warp;
     if (ep >= B) return;
-    SimSmem S = sim_carve(smem + warp * smem_per_ep, P);
+    uint8_t *base = smem + (size_t)warp * L.bytes;
+    uint8_t *as = base + L.assign;
     const int32_t *row = assign + (size_t)ep * P.n;
-    for (int v = lane_id(); v < P.n; v += 32) S.assign[v] = (uint8_t)row[v];
+    for (int v = lane_id(); v < P.n; v += 32) as[v] = (uint8_t)row[v];
     __syncwarp();
-    SimOut o = sim_episode(P, S, strategy, jit ? jit + (size_t)ep * jit_stride : nullptr,
-                           trace ? trace + (size_t)ep * trace_cap : nullptr, trace_cap,
-                           blocked ? blocked + (size_t)ep * P.n : nullptr);
+    SimOut o = sim_episode<RPL>(P, base, L, strategy,
+                                jit ? jit + (size_t)ep * jit_stride : nullptr,
+                                trace ? trace + (size_t)ep * trace_cap : nullptr, trace_cap,
+                                blocked ? blocked + (size_t)ep * P.n : nullptr);
     if (lane_id() == 0) {
         makespan[ep] = o.makespan;
         status[ep] = o.status;
@@ -66,24 +68,36 @@ sim_batch_kernel(DevProblem P, const int32_t *__restrict__ assign, int B, int st
     }
 }
 
-static int launch_sim(const fp_problem *p, const int32_t *assign, int B, int strategy,
-                      const double *jit, long long jstride, double *mk, int32_t *st,
-                      fp_event *trace, int cap, int32_t *tlen, uint8_t *blocked,
-                      cudaStream_t stream) {
+template <int RPL>
+static int launch_sim_t(const fp_problem *p, const int32_t *assign, int B, int strategy,
+                        const double *jit, long long jstride, double *mk, int32_t *st,
+                        fp_event *trace, int cap, int32_t *tlen, uint8_t *blocked,
+                        cudaStream_t stream) {
     constexpr int WARPS = 4;
-    const int64_t per = p->sim_smem;
-    const int64_t smem = per * WARPS;
+    const EpLayout L = make_layout(p->dev.n, p->dev.W, p->dev.R, p->dev.SM, false);
+    const int64_t smem = (int64_t)L.bytes * WARPS;
     if (smem > 227 * 1024) {
         set_error("simulator state exceeds shared memory (n/d too large for the smem core)");
         return FP_ERR_UNSUPPORTED;
     }
-    auto kern = sim_batch_kernel<WARPS>;
+    auto kern = sim_batch_kernel<RPL, WARPS>;
     FP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int grid = (B + WARPS - 1) / WARPS;
-    kern<<<grid, WARPS * 32, smem, stream>>>(p->dev, assign, B, strategy, jit, jstride, mk, st,
-                                             trace, cap, tlen, blocked, per);
+    kern<<<grid, WARPS * 32, smem, stream>>>(p->dev, L, assign, B, strategy, jit, jstride, mk,
+                                             st, trace, cap, tlen, blocked);
     FP_CUDA(cudaGetLastError());
     return FP_OK;
+}
+
+static int launch_sim(const fp_problem *p, const int32_t *assign, int B, int strategy,
+                      const double *jit, long long jstride, double *mk, int32_t *st,
+                      fp_event *trace, int cap, int32_t *tlen, uint8_t *blocked,
+                      cudaStream_t stream) {
+    const int R = p->dev.R;
+    if (R <= 32) return launch_sim_t<1>(p, assign, B, strategy, jit, jstride, mk, st, trace, cap, tlen, blocked, stream);
+    if (R <= 96) return launch_sim_t<3>(p, assign, B, strategy, jit, jstride, mk, st, trace, cap, tlen, blocked, stream);
+    if (R <= 288) return launch_sim_t<9>(p, assign, B, strategy, jit, jstride, mk, st, trace, cap, tlen, blocked, stream);
+    return launch_sim_t<33>(p, assign, B, strategy, jit, jstride, mk, st, trace, cap, tlen, blocked, stream);
 }
 
 }  // namespace fp
@@ -112,14 +126,18 @@ int fp_problem_create(const fp_graph_desc *g, fp_problem **out) {
         }
     }
     const int R = d + d * d;
-    std::vector<int> slots(R, 0), pool_off(R + 1, 0);
+    std::vector<int> slots(R, 0);
     for (int a = 0; a < d; ++a) slots[a] = g->eslots[a];
     for (int a = 0; a < d; ++a)
         for (int b = 0; b < d; ++b) slots[d + a * d + b] = a == b ? 0 : g->tslots[a * d + b];
+    int SM = 1;
     for (int r = 0; r < R; ++r) {
         if (slots[r] < 0) { set_error("negative slot count"); return FP_ERR_INVALID; }
-        pool_off[r + 1] = pool_off[r] + slots[r];
+        SM = std::max(SM, slots[r]);
     }
+    // a resource can never run more tasks at once than it has candidates
+    SM = std::min(SM, std::max(n, 1));
+    for (int r = 0; r < R; ++r) slots[r] = std::min(slots[r], SM);
     std::vector<double> tl(n, 0.0), bl(n, 0.0);
     if (g->tlev) std::copy(g->tlev, g->tlev + n, tl.begin());
     if (g->blev) std::copy(g->blev, g->blev + n, bl.begin());
@@ -157,7 +175,7 @@ int fp_problem_create(const fp_graph_desc *g, fp_problem **out) {
            o_en = A.put(entry.data(), nn), o_fl = A.put(g->flops, n), o_ob = A.put(g->obytes, n),
            o_ra = A.put(g->rates, d), o_bw = A.put(g->bw, (size_t)d * d),
            o_tl = A.put(tl.data(), n), o_bl = A.put(bl.data(), n),
-           o_sl = A.put(slots.data(), R), o_po = A.put(pool_off.data(), R + 1),
+           o_sl = A.put(slots.data(), R),
            o_rp = A.put(rpos.data(), 3 * n), o_rv = A.put(rvert.data(), 3 * n),
            o_kr = A.put(krank.data(), 3 * n);
     fp_problem *p = new fp_problem();
@@ -173,7 +191,7 @@ int fp_problem_create(const fp_graph_desc *g, fp_problem **out) {
             FP_CUDA(cudaMemcpy(base + part.first, part.second.data(), part.second.size(),
                                cudaMemcpyHostToDevice));
     DevProblem &D = p->dev;
-    D.n = n; D.d = d; D.W = (n + 31) / 32; D.R = R; D.P = pool_off[R];
+    D.n = n; D.d = d; D.W = (n + 31) / 32; D.R = R; D.SM = SM; D.P = R * SM;
     D.n_nonentry = nonentry;
     D.comm_factor = g->comm_factor;
     D.pred_ptr = (const int *)(base + o_pp); D.pred_idx = (const int *)(base + o_pi);
@@ -182,10 +200,10 @@ int fp_problem_create(const fp_graph_desc *g, fp_problem **out) {
     D.flops = (const double *)(base + o_fl); D.obytes = (const double *)(base + o_ob);
     D.rates = (const double *)(base + o_ra); D.bw = (const double *)(base + o_bw);
     D.tlev = (const double *)(base + o_tl); D.blev = (const double *)(base + o_bl);
-    D.slots = (const int *)(base + o_sl); D.pool_off = (const int *)(base + o_po);
+    D.slots = (const int *)(base + o_sl);
     D.rank_pos = (const int *)(base + o_rp); D.rank_vert = (const int *)(base + o_rv);
     D.krank = (const int *)(base + o_kr);
-    p->sim_smem = sim_smem_bytes(n, d, D.W, R, D.P);
+    p->sim_smem = make_layout(n, D.W, R, SM, false).bytes;
     *out = p;
     return FP_OK;
 }

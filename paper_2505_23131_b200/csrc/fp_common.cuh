@@ -29,6 +29,44 @@ __device__ __forceinline__ double warp_max(double v) {
     return v;
 }
 
+// Order-preserving map double -> uint64 (total order for non-NaN values).
+__device__ __forceinline__ uint64_t f64_key(double x) {
+    const uint64_t b = (uint64_t)__double_as_longlong(x);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ULL);
+}
+__device__ __forceinline__ double f64_unkey(uint64_t k) {
+    return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffULL) : ~k));
+}
+
+// Exact fp64 min / max across the warp with two integer REDUX steps
+// (hi word, then lo word among lanes holding the extreme hi word).
+__device__ __forceinline__ double warp_min_redux(double x) {
+    const uint64_t k = f64_key(x);
+    const unsigned hi = __reduce_min_sync(FP_FULL_MASK, (unsigned)(k >> 32));
+    const unsigned lo = __reduce_min_sync(FP_FULL_MASK, (unsigned)(k >> 32) == hi ? (unsigned)k
+                                                                               : 0xffffffffu);
+    return f64_unkey(((uint64_t)hi << 32) | lo);
+}
+__device__ __forceinline__ double warp_max_redux(double x) {
+    const uint64_t k = f64_key(x);
+    const unsigned hi = __reduce_max_sync(FP_FULL_MASK, (unsigned)(k >> 32));
+    const unsigned lo = __reduce_max_sync(FP_FULL_MASK, (unsigned)(k >> 32) == hi ? (unsigned)k : 0u);
+    return f64_unkey(((uint64_t)hi << 32) | lo);
+}
+
+// Inclusive prefix sum over the first 2^LOG lanes (lane order).
+template <int LOG, typename T>
+__device__ __forceinline__ T warp_scan_pow2(T v) {
+    const int l = lane_id();
+#pragma unroll
+    for (int i = 0; i < LOG; ++i) {
+        const int o = 1 << i;
+        T u = __shfl_up_sync(FP_FULL_MASK, v, o);
+        if ((l & ((1 << LOG) - 1)) >= o) v += u;
+    }
+    return v;
+}
+
 // Inclusive prefix sum across the warp (lane order).
 template <typename T>
 __device__ __forceinline__ T warp_inclusive_scan(T v) {

@@ -20,6 +20,9 @@
 //   * Durations are the reference's fp64 expressions with explicit _rn
 //     intrinsics (no FMA contraction): flops/rate, (bytes*cf)/bw (:183,:189),
 //     then * jitter factor when a table is given.
+// Lane l owns resources l, l+32, ... (RPL per lane): their free-slot counts
+// live in registers and their in-flight slots (r*SM + i) are only touched by
+// that lane; pending bitsets / counts are shared (atomic pushes).
 // Event order in the optional trace is the reference's: starts of an instant
 // sorted by the global enumeration key, completions by start sequence.
 #pragma once
@@ -29,43 +32,9 @@
 
 namespace fp {
 
-struct SimSmem {
-    uint32_t *rdy;      // [n] device mask where v's output is materialised
-    int *missing;       // [n] preds not ready on assign[v]
-    uint32_t *cons;     // [n] devices hosting v's successors
-    uint8_t *assign;    // [n]
-    uint32_t *bits;     // [R][W] pending tasks per resource (strategy-order bit index)
-    int *cnt;           // [R] pending count
-    int *freec;         // [R] free slots
-    double *pend;       // [P] in-flight end time
-    uint64_t *skey;     // [P] start-sort keys
-    int *pv;            // [P] in-flight vertex (-1 empty)
-    int *pseq;          // [P] start sequence number
-    int *sidx;          // [P] started pool entries / retiring vertices (this instant)
-    int *elist;         // [P] retiring pool entries
-    int *ctr;           // [4] counters
-};
-
-__device__ __forceinline__ SimSmem sim_carve(uint8_t *base, const DevProblem &P) {
-    SimSmem s;
-    const int n = P.n;
-    uint8_t *p = base;
-    s.rdy = (uint32_t *)p; p += 4 * n;
-    s.missing = (int *)p; p += 4 * n;
-    s.cons = (uint32_t *)p; p += 4 * n;
-    s.assign = p; p += (n + 15) / 16 * 16;
-    s.bits = (uint32_t *)p; p += 4 * P.R * P.W;
-    s.cnt = (int *)p; p += 4 * P.R;
-    s.freec = (int *)p; p += 4 * P.R;
-    p = (uint8_t *)(((uintptr_t)p + 7) & ~(uintptr_t)7);
-    s.pend = (double *)p; p += 8 * P.P;
-    s.skey = (uint64_t *)p; p += 8 * P.P;
-    s.pv = (int *)p; p += 4 * P.P;
-    s.pseq = (int *)p; p += 4 * P.P;
-    s.sidx = (int *)p; p += 4 * P.P;
-    s.elist = (int *)p; p += 4 * P.P;
-    s.ctr = (int *)p;
-    return s;
+__device__ __forceinline__ uint64_t sim_task_key(int krank, int kind, int v, int b) {
+    return ((uint64_t)krank << 40) | ((uint64_t)(kind == 0 ? 1 : 0) << 39) |
+           ((uint64_t)v << 8) | (uint64_t)(b & 0xff);
 }
 
 struct SimOut {
@@ -74,46 +43,66 @@ struct SimOut {
     int n_events;
 };
 
-__device__ __forceinline__ void sim_push(const SimSmem &S, const DevProblem &P, int r, int pos) {
-    atomicOr(&S.bits[r * P.W + (pos >> 5)], 1u << (pos & 31));
-    atomicAdd(&S.cnt[r], 1);
-}
-
-// Global enumeration key of a started task (see header comment).
-__device__ __forceinline__ uint64_t sim_task_key(int krank, int kind, int v, int b) {
-    return ((uint64_t)krank << 40) | ((uint64_t)(kind == 0 ? 1 : 0) << 39) |
-           ((uint64_t)v << 8) | (uint64_t)(b & 0xff);
-}
-
-// Runs one episode.  S.assign must hold the assignment (written by the caller
-// and made visible with __syncwarp).  All 32 lanes must call.
-static __device__ SimOut sim_episode(const DevProblem &P, const SimSmem &S, int strategy,
-                              const double *__restrict__ jit, fp_event *__restrict__ trace,
-                              int trace_cap, uint8_t *__restrict__ blocked) {
+// base: this episode's shared-memory slice; L.assign must hold the
+// assignment (made visible with __syncwarp).  All 32 lanes must call.
+template <int RPL>
+__device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *base,
+                                              const EpLayout &L, int strategy,
+                                              const double *__restrict__ jit,
+                                              fp_event *__restrict__ trace, int trace_cap,
+                                              uint8_t *__restrict__ blocked) {
     const int lane = lane_id();
-    const int n = P.n, d = P.d, W = P.W, R = P.R;
+    const int n = P.n, d = P.d, W = P.W, R = P.R, SM = P.SM;
+    uint32_t *rdy = (uint32_t *)(base + L.rdy);
+    int *missing = (int *)(base + L.missing);
+    uint32_t *cons = (uint32_t *)(base + L.cons);
+    const uint8_t *assign = base + L.assign;
+    uint32_t *bits = (uint32_t *)(base + L.bits);
+    int *cnt = (int *)(base + L.cnt);
+    double *pend = (double *)(base + L.pend);
+    int *pv = (int *)(base + L.pv);
+    int *pseq = (int *)(base + L.pseq);
+    uint64_t *skey = (uint64_t *)(base + L.skey);
+    int *sidx = (int *)(base + L.sidx);
+    int *elist = (int *)(base + L.elist);
+    int *ctr = (int *)(base + L.ctr);
     const uint32_t dmask = d >= 32 ? 0xffffffffu : ((1u << d) - 1u);
-    const int *rpos = P.rank_pos + strategy * n;
-    const int *rvert = P.rank_vert + strategy * n;
-    const int *krk = P.krank + strategy * n;
+    const int *__restrict__ rpos = P.rank_pos + strategy * n;
+    const int *__restrict__ rvert = P.rank_vert + strategy * n;
+    const int *__restrict__ krk = P.krank + strategy * n;
+    const int *__restrict__ sp = P.succ_ptr;
+    const int *__restrict__ si = P.succ_idx;
+    const uint8_t *__restrict__ ent = P.is_entry;
 
     // ---- init (_simcore.pyx:71-105) ----
     for (int v = lane; v < n; v += 32) {
-        const bool entry = P.is_entry[v];
-        S.rdy[v] = entry ? dmask : 0u;
+        const bool e = ent[v];
+        rdy[v] = e ? dmask : 0u;
         uint32_t c = 0;
-        for (int j = P.succ_ptr[v]; j < P.succ_ptr[v + 1]; ++j) c |= 1u << S.assign[P.succ_idx[j]];
-        S.cons[v] = c;
+        for (int j = sp[v]; j < sp[v + 1]; ++j) c |= 1u << assign[si[j]];
+        cons[v] = c;
         int miss = 0;
-        for (int j = P.pred_ptr[v]; j < P.pred_ptr[v + 1]; ++j) miss += !P.is_entry[P.pred_idx[j]];
-        S.missing[v] = miss;
+        for (int j = P.pred_ptr[v]; j < P.pred_ptr[v + 1]; ++j) miss += !ent[P.pred_idx[j]];
+        missing[v] = miss;
     }
-    for (int i = lane; i < R * W; i += 32) S.bits[i] = 0u;
-    for (int r = lane; r < R; r += 32) { S.cnt[r] = 0; S.freec[r] = P.slots[r]; }
-    for (int i = lane; i < P.P; i += 32) S.pv[i] = -1;
+    for (int i = lane; i < R * W; i += 32) bits[i] = 0u;
+    int fr[RPL];
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) {
+        const int r = lane + 32 * q;
+        fr[q] = r < R ? P.slots[r] : 0;
+        if (r < R) {
+            cnt[r] = 0;
+            for (int i = 0; i < SM; ++i) pv[r * SM + i] = -1;
+        }
+    }
     __syncwarp();
     for (int v = lane; v < n; v += 32)
-        if (!P.is_entry[v] && S.missing[v] == 0) sim_push(S, P, S.assign[v], rpos[v]);
+        if (!ent[v] && missing[v] == 0) {
+            const int pos = rpos[v];
+            atomicOr(&bits[assign[v] * W + (pos >> 5)], 1u << (pos & 31));
+            atomicAdd(&cnt[assign[v]], 1);
+        }
     __syncwarp();
 
     SimOut out{0.0, FP_EP_OK, 0};
@@ -123,66 +112,73 @@ static __device__ SimOut sim_episode(const DevProblem &P, const SimSmem &S, int 
     const bool tracing = trace != nullptr;
 
     while (remaining > 0) {
-        // ---------------- start phase: each lane serves its resources ----------
-        int nstart = 0;  // per-lane count (for deadlock detection)
-        if (tracing && lane == 0) S.ctr[0] = 0;
+        // ---------------- start phase: each lane serves its resources --------
+        if (tracing && lane == 0) ctr[0] = 0;
         __syncwarp();
-        for (int r = lane; r < R; r += 32) {
-            int fr = S.freec[r];
-            int c = S.cnt[r];
-            if (fr <= 0 || c <= 0) continue;
-            uint32_t *wb = S.bits + r * W;
-            int w = 0;
-            const int po = P.pool_off[r], pe = P.pool_off[r + 1];
-            int slot = po;
-            while (fr > 0 && c > 0) {
-                uint32_t word = wb[w];
-                while (word == 0u) word = wb[++w];
-                const int b = __ffs(word) - 1;
-                wb[w] = word & ~(1u << b);
-                const int v = rvert[(w << 5) + b];
-                double dur;
-                int ta, tb, kind;
-                if (r < d) {
-                    kind = 0; ta = r; tb = -1;
-                    dur = __ddiv_rn(P.flops[v], P.rates[r]);
-                    if (jit) dur = __dmul_rn(dur, jit[v * d + r]);
-                } else {
-                    kind = 1; ta = (r - d) / d; tb = (r - d) % d;
-                    dur = __ddiv_rn(__dmul_rn(P.obytes[v], P.comm_factor), P.bw[ta * d + tb]);
-                    if (jit) dur = __dmul_rn(dur, jit[n * d + (v * d + ta) * d + tb]);
+        int live = 0;
+        double lmin = __longlong_as_double(0x7ff0000000000000LL);  // +inf
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) {
+            const int r = lane + 32 * q;
+            if (r >= R) continue;
+            int c = cnt[r];
+            if (fr[q] > 0 && c > 0) {
+                uint32_t *wb = bits + r * W;
+                int w = 0;
+                int slot = r * SM;
+                int f = fr[q];
+                while (f > 0 && c > 0) {
+                    uint32_t word = wb[w];
+                    while (word == 0u) word = wb[++w];
+                    const int b = __ffs(word) - 1;
+                    wb[w] = word & ~(1u << b);
+                    const int v = rvert[(w << 5) + b];
+                    double dur;
+                    int kind, tb;
+                    if (r < d) {
+                        kind = 0; tb = -1;
+                        dur = __ddiv_rn(P.flops[v], P.rates[r]);
+                        if (jit) dur = __dmul_rn(dur, jit[v * d + r]);
+                    } else {
+                        const int ta = (r - d) / d;
+                        kind = 1; tb = (r - d) - ta * d;
+                        dur = __ddiv_rn(__dmul_rn(P.obytes[v], P.comm_factor), P.bw[ta * d + tb]);
+                        if (jit) dur = __dmul_rn(dur, jit[n * d + (v * d + ta) * d + tb]);
+                    }
+                    while (pv[slot] >= 0) ++slot;
+                    pend[slot] = __dadd_rn(t, dur);
+                    pv[slot] = v;
+                    if (tracing) {
+                        const int k = atomicAdd(&ctr[0], 1);
+                        skey[k] = sim_task_key(krk[v], kind, v, tb);
+                        sidx[k] = slot;
+                    }
+                    --f;
+                    --c;
                 }
-                while (S.pv[slot] >= 0) ++slot;
-                S.pend[slot] = __dadd_rn(t, dur);
-                S.pv[slot] = v;
-                if (tracing) {
-                    const int k = atomicAdd(&S.ctr[0], 1);
-                    S.skey[k] = sim_task_key(krk[v], kind, v, tb);
-                    S.sidx[k] = slot;
-                }
-                --fr; --c; ++nstart;
-                (void)pe; (void)ta;
+                fr[q] = f;
+                cnt[r] = c;
             }
-            S.freec[r] = fr;
-            S.cnt[r] = c;
+            // in-flight scan of this resource's slots (the wait phase's min)
+            for (int i = 0; i < SM; ++i) {
+                const int s = r * SM + i;
+                if (pv[s] >= 0) { lmin = fmin(lmin, pend[s]); ++live; }
+            }
         }
         __syncwarp();
         if (tracing) {
-            // order this instant's starts by the global enumeration key
-            const int k = S.ctr[0];
+            const int k = ctr[0];
             for (int i = lane; i < k; i += 32) {
-                const uint64_t key = S.skey[i];
+                const uint64_t key = skey[i];
                 int rank = 0;
-                for (int j = 0; j < k; ++j) rank += S.skey[j] < key;
-                const int slot = S.sidx[i];
-                S.pseq[slot] = seq + rank;
+                for (int j = 0; j < k; ++j) rank += skey[j] < key;
+                const int slot = sidx[i];
+                pseq[slot] = seq + rank;
                 const int pos = out.n_events + rank;
                 if (pos < trace_cap) {
-                    // recover (kind, a, b) from the slot's resource
-                    int r = 0;
-                    while (P.pool_off[r + 1] <= slot) ++r;
+                    const int r = slot / SM;
                     fp_event e;
-                    e.time = t; e.v = S.pv[slot]; e.etype = 0;
+                    e.time = t; e.v = pv[slot]; e.etype = 0;
                     if (r < d) { e.kind = 0; e.a = (int8_t)r; e.b = -1; }
                     else { e.kind = 1; e.a = (int8_t)((r - d) / d); e.b = (int8_t)((r - d) % d); }
                     trace[pos] = e;
@@ -193,75 +189,76 @@ static __device__ SimOut sim_episode(const DevProblem &P, const SimSmem &S, int 
             __syncwarp();
         }
 
-        // ---------------- wait phase: earliest completion ----------------------
-        double lmin = __longlong_as_double(0x7ff0000000000000LL);  // +inf
-        int live = 0;
-        for (int r = lane; r < R; r += 32)
-            for (int s = P.pool_off[r]; s < P.pool_off[r + 1]; ++s)
-                if (S.pv[s] >= 0) { lmin = fmin(lmin, S.pend[s]); ++live; }
-        live = warp_sum(live);
-        if (live == 0) {
+        // ---------------- wait phase: earliest completion -----------------
+        if (__reduce_add_sync(FP_FULL_MASK, live) == 0) {
             out.status = FP_EP_DEADLOCK;
             out.makespan = t;
             if (blocked)
                 for (int v = lane; v < n; v += 32)
-                    blocked[v] = !P.is_entry[v] && !((S.rdy[v] >> S.assign[v]) & 1u);
+                    blocked[v] = !ent[v] && !((rdy[v] >> assign[v]) & 1u);
             return out;
         }
-        const double tmin = warp_min(lmin);
-        if (tracing && lane == 0) S.ctr[1] = 0;
+        const double tmin = warp_min_redux(lmin);
+        if (tracing && lane == 0) ctr[1] = 0;
         __syncwarp();
         int done_exec = 0;
-        for (int r = lane; r < R; r += 32) {
-            for (int s = P.pool_off[r]; s < P.pool_off[r + 1]; ++s) {
-                const int v = S.pv[s];
-                if (v < 0 || S.pend[s] != tmin) continue;
-                S.pv[s] = -1;
-                S.freec[r] += 1;
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) {
+            const int r = lane + 32 * q;
+            if (r >= R) continue;
+            for (int i = 0; i < SM; ++i) {
+                const int s = r * SM + i;
+                const int v = pv[s];
+                if (v < 0 || pend[s] != tmin) continue;
+                pv[s] = -1;
+                fr[q] += 1;
                 if (tracing) {
-                    const int k = atomicAdd(&S.ctr[1], 1);
-                    S.elist[k] = s;
-                    S.sidx[k] = v;  // start list is consumed; reuse for the vertex
+                    const int k = atomicAdd(&ctr[1], 1);
+                    elist[k] = s;
+                    sidx[k] = v;  // start list is consumed; reuse for the vertex
                 }
                 int dev;
                 if (r < d) {
                     dev = r;
-                    atomicOr(&S.rdy[v], 1u << r);
+                    atomicOr(&rdy[v], 1u << r);
                     ++done_exec;
-                    uint32_t m = S.cons[v] & ~(1u << r);
+                    uint32_t m = cons[v] & ~(1u << r);
                     const int pos = rpos[v];
                     while (m) {
                         const int dst = __ffs(m) - 1;
                         m &= m - 1;
-                        sim_push(S, P, d + r * d + dst, pos);
+                        const int rr = d + r * d + dst;
+                        atomicOr(&bits[rr * W + (pos >> 5)], 1u << (pos & 31));
+                        atomicAdd(&cnt[rr], 1);
                     }
                 } else {
                     dev = (r - d) % d;
-                    atomicOr(&S.rdy[v], 1u << dev);
+                    atomicOr(&rdy[v], 1u << dev);
                 }
-                for (int j = P.succ_ptr[v]; j < P.succ_ptr[v + 1]; ++j) {
-                    const int w = P.succ_idx[j];
-                    if (S.assign[w] == dev && atomicSub(&S.missing[w], 1) == 1)
-                        sim_push(S, P, dev, rpos[w]);
+                for (int j = sp[v]; j < sp[v + 1]; ++j) {
+                    const int w = si[j];
+                    if (assign[w] == dev && atomicSub(&missing[w], 1) == 1) {
+                        const int pos = rpos[w];
+                        atomicOr(&bits[dev * W + (pos >> 5)], 1u << (pos & 31));
+                        atomicAdd(&cnt[dev], 1);
+                    }
                 }
             }
         }
-        remaining -= warp_sum(done_exec);
+        remaining -= __reduce_add_sync(FP_FULL_MASK, done_exec);
         __syncwarp();
         if (tracing) {
-            const int k = S.ctr[1];
+            const int k = ctr[1];
             for (int i = lane; i < k; i += 32) {
-                const int slot = S.elist[i];
-                const int sq = S.pseq[slot];
+                const int slot = elist[i];
+                const int sq = pseq[slot];
                 int rank = 0;
-                for (int j = 0; j < k; ++j) rank += S.pseq[S.elist[j]] < sq;
+                for (int j = 0; j < k; ++j) rank += pseq[elist[j]] < sq;
                 const int pos = out.n_events + rank;
                 if (pos < trace_cap) {
-                    int r = 0;
-                    while (P.pool_off[r + 1] <= slot) ++r;
+                    const int r = slot / SM;
                     fp_event e;
-                    e.time = tmin; e.etype = 1;
-                    e.v = S.sidx[i];
+                    e.time = tmin; e.etype = 1; e.v = sidx[i];
                     if (r < d) { e.kind = 0; e.a = (int8_t)r; e.b = -1; }
                     else { e.kind = 1; e.a = (int8_t)((r - d) / d); e.b = (int8_t)((r - d) % d); }
                     trace[pos] = e;
