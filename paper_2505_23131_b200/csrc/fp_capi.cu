@@ -165,6 +165,20 @@ int fp_problem_create(const fp_graph_desc *g, fp_problem **out) {
     }
     int nonentry = 0;
     for (int v = 0; v < n; ++v) nonentry += !g->is_entry[v];
+    // clean task durations, the reference's exact IEEE expressions
+    // (_simcore.pyx:183,189; cluster.py:108-124): computed once per problem
+    std::vector<double> edur((size_t)n * d), tdur((size_t)n * d * d, 0.0);
+    for (int v = 0; v < n; ++v)
+        for (int a = 0; a < d; ++a) {
+            volatile double e = g->flops[v] / g->rates[a];
+            edur[(size_t)v * d + a] = e;
+            for (int b = 0; b < d; ++b) {
+                if (a == b) continue;
+                volatile double num = g->obytes[v] * g->comm_factor;
+                volatile double t = num / g->bw[a * d + b];
+                tdur[((size_t)v * d + a) * d + b] = t;
+            }
+        }
 
     Arena A;
     const int nn = std::max(n, 1);
@@ -175,7 +189,8 @@ int fp_problem_create(const fp_graph_desc *g, fp_problem **out) {
            o_en = A.put(entry.data(), nn), o_fl = A.put(g->flops, n), o_ob = A.put(g->obytes, n),
            o_ra = A.put(g->rates, d), o_bw = A.put(g->bw, (size_t)d * d),
            o_tl = A.put(tl.data(), n), o_bl = A.put(bl.data(), n),
-           o_sl = A.put(slots.data(), R),
+           o_sl = A.put(slots.data(), R), o_ed = A.put(edur.data(), edur.size()),
+           o_td = A.put(tdur.data(), tdur.size()),
            o_rp = A.put(rpos.data(), 3 * n), o_rv = A.put(rvert.data(), 3 * n),
            o_kr = A.put(krank.data(), 3 * n);
     fp_problem *p = new fp_problem();
@@ -201,6 +216,8 @@ int fp_problem_create(const fp_graph_desc *g, fp_problem **out) {
     D.rates = (const double *)(base + o_ra); D.bw = (const double *)(base + o_bw);
     D.tlev = (const double *)(base + o_tl); D.blev = (const double *)(base + o_bl);
     D.slots = (const int *)(base + o_sl);
+    D.edur = (const double *)(base + o_ed);
+    D.tdur = (const double *)(base + o_td);
     D.rank_pos = (const int *)(base + o_rp); D.rank_vert = (const int *)(base + o_rv);
     D.krank = (const int *)(base + o_kr);
     p->sim_smem = make_layout(n, D.W, R, SM, false).bytes;

@@ -12,7 +12,7 @@ struct EpLayout {
     // SEL warp
     int cand, npl, clist, ce, cc, dsl, dse, order, flag;
     // PLC warp
-    int tstart, tend, xd, stats, xn;
+    int tstart, tend, xd, stats, xn, rsum;
     // simulator (PLC warp after the rollout; also the sim-only kernel)
     int rdy, missing, cons, assign, bits, cnt, pend, pv, pseq, skey, sidx, elist, ctr;
     int bytes;
@@ -22,7 +22,9 @@ __host__ __device__ inline int fp_align(int x, int a) { return (x + a - 1) / a *
 
 // n vertices, W words per bitset, R resources, SM slots per resource.
 // with_rollout = false gives the simulator-only layout.
-__host__ __device__ inline EpLayout make_layout(int n, int W, int R, int SM, bool with_rollout) {
+// rsum_doubles: per-device running REINFORCE sums kept in smem (2*d*h, grad mode)
+__host__ __device__ inline EpLayout make_layout(int n, int W, int R, int SM, bool with_rollout,
+                                               int rsum_doubles = 0) {
     EpLayout L;
     int o = 0;
     auto take = [&](int bytes, int align) {
@@ -42,13 +44,14 @@ __host__ __device__ inline EpLayout make_layout(int n, int W, int R, int SM, boo
         L.xd = take(8 * 32 * 5, 8);
         L.xn = take(8 * 32 * 5, 8);
         L.stats = take(8 * 16, 8);
+        L.rsum = take(8 * rsum_doubles, 8);
         L.cand = take(4 * W, 4);
         L.npl = take(4 * n, 4);
         L.clist = take(4 * n, 4);
         L.order = take(4 * n, 4);
         L.flag = take(16, 16);
     } else {
-        L.ce = L.cc = L.dsl = L.dse = L.tstart = L.tend = L.xd = L.xn = L.stats = 0;
+        L.ce = L.cc = L.dsl = L.dse = L.tstart = L.tend = L.xd = L.xn = L.stats = L.rsum = 0;
         L.cand = L.npl = L.clist = L.order = L.flag = 0;
     }
     L.pend = take(8 * P, 8);

@@ -27,6 +27,8 @@ struct DevProblem {
     const uint8_t *is_entry;
     const double *flops, *obytes, *rates, *bw;
     const double *tlev, *blev;
+    const double *edur;    // [n][d]    flops[v] / rates[a]              (simulate.py duration)
+    const double *tdur;    // [n][d][d] obytes[v] * cf / bw[a][b], 0 on the diagonal
     const int *slots;      // [R]
     const int *rank_pos;   // [3][n]  position of v in strategy order
     const int *rank_vert;  // [3][n]  vertex at position

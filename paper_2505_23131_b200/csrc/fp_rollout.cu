@@ -72,8 +72,7 @@ __device__ __forceinline__ void sel_chain(const DevProblem &PR, const DevPolicy 
     double *cc = (double *)(base + L.cc);
     double *dsl = (double *)(base + L.dsl);
     double *dse = (double *)(base + L.dse);
-    int *order = (int *)(base + L.order);
-    volatile int *flag = (volatile int *)(base + L.flag);
+    volatile int *order = (volatile int *)(base + L.order);
     const double eps = A.epsilon, ome = 1.0 - eps;
     const uint32_t k0 = (uint32_t)A.seed, k1 = (uint32_t)(A.seed >> 32);
     const uint32_t ctr_ep = A.episode_base + (uint32_t)ep;
@@ -100,7 +99,7 @@ __device__ __forceinline__ void sel_chain(const DevProblem &PR, const DevPolicy 
         const int incl = warp_inclusive_scan(pc);
         const int k = __shfl_sync(FP_FULL_MASK, incl, 31);
         if (k == 0) {  // cyclic graph: nothing is ever ready
-            if (lane == 0) { order[step] = -1; __threadfence_block(); *flag = step + 1; }
+            if (lane == 0) order[step] = -1;
             return;
         }
         {
@@ -201,16 +200,13 @@ __device__ __forceinline__ void sel_chain(const DevProblem &PR, const DevPolicy 
             if (mode == FP_MODE_GREEDY) idx = amax;
         }
         if (idx < 0) {  // forced vertex is not a candidate
-            if (lane == 0) { order[step] = -2; __threadfence_block(); *flag = step + 1; }
+            if (lane == 0) order[step] = -2;
             return;
         }
         const int v = clist[idx];
-        // publish early: the PLC warp only needs the vertex
-        if (lane == 0) {
-            order[step] = v;
-            __threadfence_block();
-            *flag = step + 1;
-        }
+        // publish early: the PLC warp only needs the vertex (a single 32-bit
+        // store replacing the -3 sentinel is the whole hand-off)
+        if (lane == 0) order[step] = v;
         if (want_lp) {
             const double ek = eps / (double)k;
             double entp = 0.0, lp = 0.0, pidx = 0.0, midx = 0.0, qp = 0.0;
@@ -281,8 +277,7 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
     double *xd = (double *)(base + L.xd);
     double *xn = (double *)(base + L.xn);
     double *stats = (double *)(base + L.stats);
-    const int *order = (const int *)(base + L.order);
-    volatile int *flag = (volatile int *)(base + L.flag);
+    const volatile int *order = (const volatile int *)(base + L.order);
     uint8_t *dev = base + L.assign;
     const double eps = A.epsilon, ome = 1.0 - eps, slope = PO.slope;
     const uint32_t k0 = (uint32_t)A.seed, k1 = (uint32_t)(A.seed >> 32);
@@ -295,16 +290,15 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
     const int *__restrict__ pi = PR.pred_idx;
     const uint8_t *__restrict__ ent = PR.is_entry;
     const double *__restrict__ flops = PR.flops;
-    const double *__restrict__ obytes = PR.obytes;
-    const double *__restrict__ bw = PR.bw;
-    const double cf = PR.comm_factor;
+    const double *__restrict__ tdur = PR.tdur;
+    const double *__restrict__ edur = PR.edur;
     const double b2p = PO.W(PR_PLC_H2_B)[0];
-    const double rate_l = lane < D ? PR.rates[lane] : 1.0;
+    double *rsl = (double *)(base + L.rsum);  // [D][h] running lp sums (grad)
+    double *rse = rsl + D * h;                // [D][h] running entropy sums
 
     for (int v = lane; v < n; v += 32) { tstart[v] = 0.0; tend[v] = 0.0; dev[v] = 0xFF; }
     double avail = 0.0, aflops = 0.0;  // lane d < D
     double Mr[5][HPL], cr[HPL], w2r[HPL], Sd[MAXD][HPL];
-    double Rl[GRAD ? MAXD : 1][HPL], Re[GRAD ? MAXD : 1][HPL];
     double dMl[GRAD ? 5 : 1][HPL], dMe[GRAD ? 5 : 1][HPL], dwl[HPL], dwe[HPL];
     double db2l = 0.0, db2e = 0.0;
     {
@@ -322,18 +316,17 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
             for (int d = 0; d < MAXD; ++d) Sd[d][t] = 0.0;
             if constexpr (GRAD) {
 #pragma unroll
-                for (int d = 0; d < MAXD; ++d) Rl[d][t] = Re[d][t] = 0.0;
-#pragma unroll
                 for (int c = 0; c < 5; ++c) dMl[c][t] = dMe[c][t] = 0.0;
             }
         }
+        if constexpr (GRAD)
+            for (int i = lane; i < 2 * D * h; i += 32) rsl[i] = 0.0;
     }
     __syncwarp();
     int status = FP_EP_OK;
     for (int step = 0; step < n; ++step) {
-        while (*flag <= step) { }
-        __threadfence_block();
-        const int v = order[step];
+        int v;
+        while ((v = order[step]) == -3) { }
         if (v < 0) { status = v == -1 ? FP_EP_DEADLOCK : FP_EP_BAD_ACTION; break; }
         double Av[HPL], Gv[HPL];
 #pragma unroll
@@ -351,12 +344,9 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
             for (int j = p0; j < p1; ++j) {
                 const int p = pi[j];
                 const int dp = dev[p];
-                double arr = 0.0;
-                if (!ent[p]) {
-                    arr = tend[p];
-                    if (dp != lane)
-                        arr = __dadd_rn(arr, __ddiv_rn(__dmul_rn(obytes[p], cf), bw[dp * D + lane]));
-                }
+                // arrival = end + transfer (0.0 on the same device), timeline.py:30-35
+                const double arr =
+                    ent[p] ? 0.0 : __dadd_rn(tend[p], tdur[(p * D + dp) * D + lane]);
                 f3 = j == p0 ? arr : fmax(f3, arr);
                 if (dp == lane) {
                     f1 = __dadd_rn(f1, flops[p]);
@@ -371,22 +361,33 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
         __syncwarp();
         // ---- column statistics: lane c < 5 sums over devices in order ----
         if (lane < 5) {
+            double col[MAXD];
+#pragma unroll
+            for (int d = 0; d < MAXD; ++d) col[d] = d < D ? xd[d * 5 + lane] : 0.0;
             double sum = 0.0;
-            for (int d = 0; d < D; ++d) sum = __dadd_rn(sum, xd[d * 5 + lane]);
+#pragma unroll
+            for (int d = 0; d < MAXD; ++d)
+                if (d < D) sum = __dadd_rn(sum, col[d]);
             const double mean = __ddiv_rn(sum, (double)D);
             double sq = 0.0;
-            for (int d = 0; d < D; ++d) {
-                const double df = __dsub_rn(xd[d * 5 + lane], mean);
-                sq = __dadd_rn(sq, __dmul_rn(df, df));
-            }
+#pragma unroll
+            for (int d = 0; d < MAXD; ++d)
+                if (d < D) {
+                    const double df = __dsub_rn(col[d], mean);
+                    sq = __dadd_rn(sq, __dmul_rn(df, df));
+                }
             const double sd = __dsqrt_rn(__ddiv_rn(sq, (double)D));
             stats[lane] = mean;
             stats[5 + lane] = sd < 1e-12 ? 1.0 : sd;
         }
         __syncwarp();
-        for (int i = lane; i < 5 * D; i += 32) {
-            const int c = i % 5;
-            xn[i] = __ddiv_rn(__dsub_rn(xd[i], stats[c]), stats[5 + c]);
+#pragma unroll
+        for (int t = 0; t < (5 * MAXD + 31) / 32; ++t) {
+            const int i = lane + 32 * t;
+            if (i < 5 * D) {
+                const int c = i % 5;
+                xn[i] = __ddiv_rn(__dsub_rn(xd[i], stats[c]), stats[5 + c]);
+            }
         }
         __syncwarp();
         // ---- pre-activations + head2 partial sums (lane = hidden column) ----
@@ -511,8 +512,8 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
                         dwe[t] = fma(ged, lv, dwe[t]);
                         arl[t] += dl;
                         are[t] += de;
-                        Rl[d][t] += dl;
-                        Re[d][t] += de;
+                        const int j = lane + 32 * t;
+                        if (j < h) { rsl[d * h + j] += dl; rse[d * h + j] += de; }
                         dMl[0][t] = fma(x0, dl, dMl[0][t]); dMe[0][t] = fma(x0, de, dMe[0][t]);
                         dMl[1][t] = fma(x1, dl, dMl[1][t]); dMe[1][t] = fma(x1, de, dMe[1][t]);
                         dMl[2][t] = fma(x2, dl, dMl[2][t]); dMe[2][t] = fma(x2, de, dMe[2][t]);
@@ -527,9 +528,8 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
                     if (j >= h) continue;
                     row[j] = arl[t];
                     row[h + j] = are[t];
-#pragma unroll
-                    for (int d = 0; d < MAXD; ++d)
-                        if (d == jdx) { row[2 * h + j] = Rl[d][t]; row[3 * h + j] = Re[d][t]; }
+                    row[2 * h + j] = rsl[jdx * h + j];
+                    row[3 * h + j] = rse[jdx * h + j];
                 }
             }
         }
@@ -537,7 +537,7 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
         if (lane == jdx) {
             aflops = __dadd_rn(aflops, flops[v]);
             if (!ent[v]) {
-                const double en = __dadd_rn(f4, __ddiv_rn(flops[v], rate_l));
+                const double en = __dadd_rn(f4, edur[v * D + jdx]);
                 tstart[v] = f4;
                 tend[v] = en;
                 avail = en;
@@ -563,12 +563,10 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
             for (int c = 0; c < 5; ++c) { q[c * h + j] = dMl[c][t]; q[5 * h + c * h + j] = dMe[c][t]; }
             q[10 * h + j] = dwl[t];
             q[11 * h + j] = dwe[t];
-#pragma unroll
-            for (int d = 0; d < MAXD; ++d)
-                if (d < D) {
-                    q[12 * h + 2 + d * h + j] = Rl[d][t];
-                    q[12 * h + 2 + D * h + d * h + j] = Re[d][t];
-                }
+            for (int d = 0; d < D; ++d) {
+                q[12 * h + 2 + d * h + j] = rsl[d * h + j];
+                q[12 * h + 2 + D * h + d * h + j] = rse[d * h + j];
+            }
         }
         if (lane == 0) { q[12 * h] = db2l; q[12 * h + 1] = db2e; }
     }
@@ -576,7 +574,7 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
 }
 
 template <int MAXD, int HPL, bool GRAD, int EPB>
-__global__ void __launch_bounds__(EPB * 64, 1)
+__global__ void __launch_bounds__(EPB * 64, 8 / EPB)
 rollout_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
     extern __shared__ __align__(16) uint8_t smem[];
     constexpr int RPL = (MAXD + MAXD * MAXD + 31) / 32;
@@ -590,7 +588,10 @@ rollout_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
     double *s_sm = (double *)smem;
     for (int v = threadIdx.x; v < n; v += blockDim.x) s_sm[v] = PO.s[v];
     uint8_t *base = smem + fp_align(8 * n, 16) + (size_t)slot * L.bytes;
-    if (!is_plc && lane == 0) *(volatile int *)(base + L.flag) = 0;
+    if (!is_plc) {
+        volatile int *order = (volatile int *)(base + L.order);
+        for (int t = lane; t < n; t += 32) order[t] = -3;  // hand-off sentinel
+    }
     __syncthreads();
     if (ep >= A.B) return;
     const bool want_lp = GRAD || A.step_lp != nullptr || A.step_ent != nullptr;
@@ -621,9 +622,10 @@ rollout_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
 template <int MAXD, int HPL, bool GRAD>
 static int launch_rollout(const fp_problem *p, const fp_policy *pol, const fp_rollout_args &a,
                           cudaStream_t st) {
-    constexpr int EPB = 2;
+    constexpr int EPB = 1;
     const DevProblem &PR = p->dev;
-    const EpLayout L = make_layout(PR.n, PR.W, PR.R, PR.SM, true);
+    const EpLayout L = make_layout(PR.n, PR.W, PR.R, PR.SM, true,
+                                   GRAD ? 2 * PR.d * pol->dev.h : 0);
     const int64_t smem = fp_align(8 * PR.n, 16) + (int64_t)L.bytes * EPB;
     if (smem > 227 * 1024) {
         set_error("episode state exceeds shared memory for this graph size");

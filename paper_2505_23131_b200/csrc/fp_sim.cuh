@@ -17,9 +17,9 @@
 //     (_simcore.pyx:147-159).
 //   * Completions: every in-flight record whose end == tmin exactly, in start
 //     order (_simcore.pyx:209-232); the loop stops when the last exec retires.
-//   * Durations are the reference's fp64 expressions with explicit _rn
-//     intrinsics (no FMA contraction): flops/rate, (bytes*cf)/bw (:183,:189),
-//     then * jitter factor when a table is given.
+//   * Durations are the reference's fp64 expressions flops/rate and
+//     (bytes*cf)/bw (:183,:189), evaluated once per problem on the host
+//     (P.edur / P.tdur), then * jitter factor when a table is given.
 // Lane l owns resources l, l+32, ... (RPL per lane): their free-slot counts
 // live in registers and their in-flight slots (r*SM + i) are only touched by
 // that lane; pending bitsets / counts are shared (atomic pushes).
@@ -73,6 +73,8 @@ __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *base
     const int *__restrict__ sp = P.succ_ptr;
     const int *__restrict__ si = P.succ_idx;
     const uint8_t *__restrict__ ent = P.is_entry;
+    const double *__restrict__ edur = P.edur;
+    const double *__restrict__ tdur = P.tdur;
 
     // ---- init (_simcore.pyx:71-105) ----
     for (int v = lane; v < n; v += 32) {
@@ -137,12 +139,12 @@ __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *base
                     int kind, tb;
                     if (r < d) {
                         kind = 0; tb = -1;
-                        dur = __ddiv_rn(P.flops[v], P.rates[r]);
+                        dur = edur[v * d + r];
                         if (jit) dur = __dmul_rn(dur, jit[v * d + r]);
                     } else {
                         const int ta = (r - d) / d;
                         kind = 1; tb = (r - d) - ta * d;
-                        dur = __ddiv_rn(__dmul_rn(P.obytes[v], P.comm_factor), P.bw[ta * d + tb]);
+                        dur = tdur[(v * d + ta) * d + tb];
                         if (jit) dur = __dmul_rn(dur, jit[n * d + (v * d + ta) * d + tb]);
                     }
                     while (pv[slot] >= 0) ++slot;
