@@ -198,6 +198,21 @@ int fp_rollout_batch(const fp_problem *p, const fp_policy *pol, const fp_rollout
                      void *stream);
 int fp_grad_ep_stride(const fp_policy *pol, int32_t d, int64_t *stride);
 
+/* ------------------------------------------------------------------------
+ * Stage-II update (flowplace/training.py:181-216, nn.py:184-277).
+ * fp_pg_reduce contracts the rollout's REINFORCE rows with per-episode
+ * coefficients alpha[e] (= -advantage_e / B_global for Stage II, -1/B for
+ * imitation) and beta (= -entropy_weight / B_global), deterministically;
+ * fp_policy_backward turns the reduced tables into the flat parameter
+ * gradient (same layout as the params); fp_sgd_step applies
+ * params -= lr * grad (nn.py:271-277).
+ * ------------------------------------------------------------------------ */
+int fp_pg_reduce(fp_policy *pol, const double *grad_rows, const double *grad_ep,
+                 const int32_t *assign, const double *alpha, double beta, int32_t B,
+                 void *stream);
+int fp_policy_backward(fp_policy *pol, double *grad, void *stream);
+int fp_sgd_step(double *params, const double *grad, int64_t count, double lr, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -115,6 +115,7 @@ encode_round_kernel(DevPolicy P, int k, int last) {
             u[t] += phb[j];
             hn[t] = leaky(u[t], s);
             P.U[e][k][(size_t)v * h + j] = u[t];
+            P.AG[e][k][(size_t)v * h + j] = agg[t];
             P.H[e][k + 1][(size_t)v * h + j] = hn[t];
         }
     }
@@ -351,7 +352,8 @@ int fp_policy_create(const fp_problem *p, const fp_policy_desc *desc, fp_policy 
            o_tp = take((size_t)(n + 1) * 4), o_ti = take((size_t)Lt * 4),
            o_ibp = take((size_t)(n + 1) * 4), o_ibi = take((size_t)Lb * 4),
            o_itp = take((size_t)(n + 1) * 4), o_iti = take((size_t)Lt * 4);
-    size_t o_H[2][kMaxRounds + 1], o_P[2][kMaxRounds], o_Q[2][kMaxRounds], o_U[2][kMaxRounds];
+    size_t o_H[2][kMaxRounds + 1], o_P[2][kMaxRounds], o_Q[2][kMaxRounds], o_U[2][kMaxRounds],
+        o_AG[2][kMaxRounds];
     for (int e = 0; e < n_enc; ++e) {
         o_H[e][0] = take((size_t)std::max(n, 1) * 7 * 8);
         for (int k = 0; k < K; ++k) {
@@ -359,6 +361,7 @@ int fp_policy_create(const fp_problem *p, const fp_policy_desc *desc, fp_policy 
             o_P[e][k] = take(nh);
             o_Q[e][k] = take(nh);
             o_U[e][k] = take(nh);
+            o_AG[e][k] = take(nh);
         }
     }
     size_t o_Zs = take(nh), o_emb = take(nh * 4), o_hp = take(nh), o_s = take((size_t)n * 8),
@@ -367,13 +370,15 @@ int fp_policy_create(const fp_problem *p, const fp_policy_desc *desc, fp_policy 
     size_t o_dH[2], o_dHn[2];
     for (int e = 0; e < 2; ++e) { o_dH[e] = take(nh); o_dHn[e] = take(nh); }
     size_t o_dU = take(nh), o_Ds = take(nh), o_Dd = take(nh), o_dagg = take(nh),
+           o_De = take(nh), o_dhid = take(nh), o_demb = take(nh * 4), o_dZ = take(nh * 2),
            o_ds = take((size_t)n * 8), o_dA = take(nh), o_dG = take(nh),
            o_dsm = take((size_t)(16 * h + 64) * 8);
-    const int prow = 1024;
-    size_t o_part = take((size_t)prow * 4 * kMaxHidden * 8);
+    const int prow = 16;  // episode chunks of the deterministic reduction
+    size_t o_part = take((size_t)prow * ((size_t)std::max(n, 1) * (2 * h + 1) + 16 * h + 64) * 8);
 
     fp_policy *pol = new fp_policy();
     pol->problem = p;
+    pol->n_params = desc->n_params;
     if (cudaMalloc(&pol->arena, size) != cudaSuccess) {
         delete pol;
         set_error("cudaMalloc failed for policy arena");
@@ -421,6 +426,7 @@ int fp_policy_create(const fp_problem *p, const fp_policy_desc *desc, fp_policy 
             P.Pm[e][k] = (double *)(b + o_P[e][k]);
             P.Qm[e][k] = (double *)(b + o_Q[e][k]);
             P.U[e][k] = (double *)(b + o_U[e][k]);
+            P.AG[e][k] = (double *)(b + o_AG[e][k]);
         }
     }
     P.Zs = (double *)(b + o_Zs); P.emb = (double *)(b + o_emb); P.hidpre = (double *)(b + o_hp);
@@ -428,7 +434,9 @@ int fp_policy_create(const fp_problem *p, const fp_policy_desc *desc, fp_policy 
     P.G = (double *)(b + o_G); P.M = (double *)(b + o_M); P.c = (double *)(b + o_c);
     for (int e = 0; e < 2; ++e) { P.dH[e] = (double *)(b + o_dH[e]); P.dHn[e] = (double *)(b + o_dHn[e]); }
     P.dU = (double *)(b + o_dU); P.Dsrc = (double *)(b + o_Ds); P.Ddst = (double *)(b + o_Dd);
-    P.dagg = (double *)(b + o_dagg); P.ds = (double *)(b + o_ds); P.dA = (double *)(b + o_dA);
+    P.dagg = (double *)(b + o_dagg); P.De = (double *)(b + o_De);
+    P.dhid = (double *)(b + o_dhid); P.demb = (double *)(b + o_demb); P.dZ = (double *)(b + o_dZ);
+    P.ds = (double *)(b + o_ds); P.dA = (double *)(b + o_dA);
     P.dG = (double *)(b + o_dG); P.dsmall = (double *)(b + o_dsm);
     P.partial = (double *)(b + o_part); P.partial_rows = prow;
     *out = pol;
@@ -437,6 +445,7 @@ int fp_policy_create(const fp_problem *p, const fp_policy_desc *desc, fp_policy 
 
 int fp_policy_destroy(fp_policy *pol) {
     if (!pol) return FP_OK;
+    if (pol->train) fp_train_state_free(pol->train);
     if (pol->arena) cudaFree(pol->arena);
     delete pol;
     return FP_OK;

@@ -58,12 +58,14 @@ struct DevPolicy {
     double *Pm[2][kMaxRounds];     // H[e][k] @ psi.w rows [0, d)
     double *Qm[2][kMaxRounds];     // H[e][k] @ psi.w rows [d, 2d)
     double *U[2][kMaxRounds];      // phi pre-activations
+    double *AG[2][kMaxRounds];     // aggregated messages (backward)
     double *Zs, *emb, *hidpre, *s; // SEL tables
     double *Zp, *A, *G, *M, *c;    // PLC tables
     // backward workspace
-    double *dH[2], *dHn[2], *dU, *Dsrc, *Ddst, *dagg;
+    double *dH[2], *dHn[2], *dU, *Dsrc, *Ddst, *dagg, *De;
+    double *dhid, *demb, *dZ;      // SEL head / z backward rows
     double *ds, *dA, *dG, *dsmall; // reduced gradient tables
-    double *partial;               // block partials for weight gradients
+    double *partial;               // episode-chunk partials of the reduction
     int partial_rows;
 
     __device__ __forceinline__ const double *W(int role) const { return params + off[role]; }
@@ -71,8 +73,13 @@ struct DevPolicy {
 
 }  // namespace fp
 
+struct fp_train_state;
+void fp_train_state_free(fp_train_state *);
+
 struct fp_policy {
     fp::DevPolicy dev;
     void *arena = nullptr;
     const fp_problem *problem = nullptr;
+    fp_train_state *train = nullptr;  // backward job lists (fp_train.cu)
+    int64_t n_params = 0;
 };

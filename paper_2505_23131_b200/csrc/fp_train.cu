@@ -1,0 +1,498 @@
+// Stage-II REINFORCE update on the GPU (flowplace/training.py:181-216 with the
+// autodiff of flowplace/nn.py:62-224, re-derived for the factorised policy).
+//
+//   loss = sum_e [ alpha_e * sum_t lp_e,t + beta * sum_t ent_e,t ]
+//   (alpha_e = -advantage_e / B_global, beta = -w_entropy / B_global; the
+//   reference's per-episode loss at B = 1; imitation: alpha = -1/B, beta = 0)
+//
+// 1. pg_reduce: the rollout kernel wrote, per episode, the gradients of
+//    sum lp and sum ent w.r.t. the per-vertex tables (SEL logit s[v]; PLC rows
+//    A[v], G[v] via running per-device sums; M, w2, b2).  This kernel contracts
+//    them with (alpha_e, beta) over the batch — a streaming, HBM-bound pass
+//    over B*n*4h doubles — in a fixed episode order (chunked partials, then an
+//    ordered chunk sum): bitwise deterministic, no atomics.
+// 2. head backward (SEL head + paths, PLC tables), 3. GNN backward (K rounds
+//    per encoder, gather-formulated message gradients), 4. weight gradients as
+//    row-contractions X^T Y over vertices (outer kernel, job list), 5. SGD.
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "fp_common.cuh"
+#include "fp_policy.cuh"
+
+namespace fp {
+
+__host__ __device__ inline int64_t grad_ep_stride_t(int n, int h, int d) {
+    return ((2LL * n + 12LL * h + 2 + 2LL * d * h) + 3) / 4 * 4;
+}
+
+__device__ __forceinline__ double lkd_t(double x, double s) { return x > 0.0 ? 1.0 : s; }
+__device__ __forceinline__ double lk_t(double x, double s) { return x > 0.0 ? x : s * x; }
+
+constexpr int kChunks = 16;
+
+// items: [0, n*h) (v, j) -> dA, dG; [n*h, n*h+n) -> ds[v];
+// then 5h dM, h dw2, 1 db2
+__global__ void pg_reduce_partial(DevPolicy P, int n, int h, int D, int B,
+                                  const double *__restrict__ rows, const double *__restrict__ gep,
+                                  const int32_t *__restrict__ assign,
+                                  const double *__restrict__ alpha, double beta) {
+    const int item = blockIdx.x * blockDim.x + threadIdx.x;
+    const int chunk = blockIdx.y;
+    const int nh = n * h;
+    const int items = nh + n + 6 * h + 1;
+    if (item >= items) return;
+    const int per = (B + kChunks - 1) / kChunks;
+    const int e0 = chunk * per, e1 = min(B, e0 + per);
+    const int64_t S = grad_ep_stride_t(n, h, D);
+    double *part = P.partial + (size_t)chunk * (2 * (size_t)nh + n + 6 * h + 1);
+    if (item < nh) {
+        const int v = item / h, j = item - v * h;
+        double a = 0.0, g = 0.0;
+        const size_t rstride = (size_t)n * 4 * h;
+        const double *r = rows + (size_t)v * 4 * h + j;
+        const double *tq = gep + 2 * n + 12 * h + 2 + j;
+#pragma unroll 4
+        for (int e = e0; e < e1; ++e) {
+            const double al = alpha[e];
+            const double *re = r + (size_t)e * rstride;
+            const double r0 = re[0], r1 = re[h], r2 = re[2 * h], r3 = re[3 * h];
+            const int dv = assign[(size_t)e * n + v];
+            const double *te = tq + (size_t)e * S + dv * h;
+            const double tl = te[0], tn = te[D * h];
+            a += al * r0 + beta * r1;
+            g += al * (tl - r2) + beta * (tn - r3);
+        }
+        part[item] = a;
+        part[nh + item] = g;
+        return;
+    }
+    int k = item - nh;
+    double acc = 0.0;
+    if (k < n) {  // ds[v]
+        for (int e = e0; e < e1; ++e)
+            acc += alpha[e] * gep[(size_t)e * S + k] + beta * gep[(size_t)e * S + n + k];
+    } else {
+        k -= n;  // small vectors: dM (5h), dw2 (h), db2 (1) -> lp part at 2n+off, ent at +5h/+h/+1
+        int lo, eo;
+        if (k < 5 * h) { lo = 2 * n + k; eo = 2 * n + 5 * h + k; }
+        else if (k < 6 * h) { lo = 2 * n + 10 * h + (k - 5 * h); eo = lo + h; }
+        else { lo = 2 * n + 12 * h; eo = lo + 1; }
+        for (int e = e0; e < e1; ++e)
+            acc += alpha[e] * gep[(size_t)e * S + lo] + beta * gep[(size_t)e * S + eo];
+    }
+    part[nh + item] = acc;
+}
+
+__global__ void pg_reduce_final(DevPolicy P, int n, int h) {
+    const int item = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nh = n * h;
+    const int total = 2 * nh + n + 6 * h + 1;
+    if (item >= total) return;
+    const size_t stride = 2 * (size_t)nh + n + 6 * h + 1;
+    double acc = 0.0;
+    for (int c = 0; c < kChunks; ++c) acc += P.partial[c * stride + item];
+    if (item < nh) P.dA[item] = acc;
+    else if (item < 2 * nh) P.dG[item - nh] = acc;
+    else if (item < 2 * nh + n) P.ds[item - 2 * nh] = acc;
+    else P.dsmall[h + (item - 2 * nh - n)] = acc;  // dsmall: [dc (h) | dM (5h) | dw2 (h) | db2]
+}
+
+// ---------------------------------------------------------------------------
+// head backward, warp per vertex, lane = hidden column
+// ---------------------------------------------------------------------------
+__global__ void head_bwd_kernel(DevPolicy P) {
+    const int lane = lane_id();
+    const int v = blockIdx.x * 4 + (threadIdx.x >> 5);
+    const int n = P.n, h = P.h;
+    if (v >= n) return;
+    const double s = P.slope;
+    // ---- SEL: s[v] = leaky(emb @ W1 + b1) @ w2 + b2 ----
+    const double *w1 = P.W(PR_SEL_H1_W), *w2 = P.W(PR_SEL_H2_W);
+    const double dsv = P.ds[v];
+    double dh[2] = {0.0, 0.0};
+    for (int t = 0; t < 2; ++t) {
+        const int j = lane + 32 * t;
+        if (j < h) {
+            dh[t] = dsv * w2[j] * lkd_t(P.hidpre[(size_t)v * h + j], s);
+            P.dhid[(size_t)v * h + j] = dh[t];
+        }
+    }
+    // demb_i = sum_j dhid_j W1[i][j], i < 4h
+    for (int i0 = 0; i0 < 4 * h; i0 += 32) {
+        const int i = i0 + lane;
+        double acc = 0.0;
+        for (int j = 0; j < h; ++j) {
+            const double dj = __shfl_sync(FP_FULL_MASK, dh[j >> 5], j & 31);
+            if (i < 4 * h) acc = fma(dj, w1[(size_t)i * h + j], acc);
+        }
+        if (i < 4 * h) P.demb[(size_t)v * 4 * h + i] = acc;
+    }
+    // ---- PLC: A = H@W1a + Z@W1d, G = H@W1b ----
+    const double *w1p = P.W(PR_PLC_H1_W);
+    double da[2] = {0.0, 0.0}, dg[2] = {0.0, 0.0};
+    for (int t = 0; t < 2; ++t) {
+        const int j = lane + 32 * t;
+        if (j < h) { da[t] = P.dA[(size_t)v * h + j]; dg[t] = P.dG[(size_t)v * h + j]; }
+    }
+    for (int t = 0; t < 2; ++t) {
+        const int j = lane + 32 * t;
+        double hp = 0.0, zp = 0.0;
+        for (int i = 0; i < h; ++i) {
+            const double ai = __shfl_sync(FP_FULL_MASK, da[i >> 5], i & 31);
+            const double gi = __shfl_sync(FP_FULL_MASK, dg[i >> 5], i & 31);
+            if (j < h) {
+                hp = fma(ai, w1p[(size_t)j * h + i], hp);
+                hp = fma(gi, w1p[(size_t)(h + j) * h + i], hp);
+                zp = fma(ai, w1p[(size_t)(3 * h + j) * h + i], zp);
+            }
+        }
+        if (j < h) {
+            P.dHn[1][(size_t)v * h + j] = hp;            // dH_plc (direct)
+            P.dZ[(size_t)n * h + (size_t)v * h + j] = zp;  // dZp
+        }
+    }
+}
+
+// dH of each encoder's output: SEL = direct + path scatters (inverse paths);
+// PLC = head part; shared encoder = both.
+__global__ void path_gather_kernel(DevPolicy P) {
+    const int lane = lane_id();
+    const int u = blockIdx.x * 4 + (threadIdx.x >> 5);
+    const int n = P.n, h = P.h;
+    if (u >= n) return;
+    for (int j = lane; j < h; j += 32) {
+        double acc = P.demb[(size_t)u * 4 * h + j];
+        for (int q = P.ibp_ptr[u]; q < P.ibp_ptr[u + 1]; ++q)
+            acc += P.demb[(size_t)P.ibp_idx[q] * 4 * h + h + j];
+        for (int q = P.itp_ptr[u]; q < P.itp_ptr[u + 1]; ++q)
+            acc += P.demb[(size_t)P.itp_idx[q] * 4 * h + 2 * h + j];
+        P.dZ[(size_t)u * h + j] = P.demb[(size_t)u * 4 * h + 3 * h + j];  // dZs
+        const double plc = P.dHn[1][(size_t)u * h + j];
+        if (P.n_enc == 1) {
+            P.dH[0][(size_t)u * h + j] = acc + plc;
+        } else {
+            P.dH[0][(size_t)u * h + j] = acc;
+            P.dH[1][(size_t)u * h + j] = plc;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// GNN backward for one (encoder, round)
+// ---------------------------------------------------------------------------
+// node part: dU = dH (.) leaky'(U); dH_k(direct) = dU @ phi[0:dk]^T;
+// dagg = dU @ phi[dk:dk+h]^T
+__global__ void gnn_bwd_node(DevPolicy P, int e, int k) {
+    const int lane = lane_id();
+    const int v = blockIdx.x * 4 + (threadIdx.x >> 5);
+    const int n = P.n, h = P.h;
+    if (v >= n) return;
+    const int dk = k == 0 ? 7 : h;
+    const double *phw = P.W(gnn_role(e, k, 2));
+    double du[2] = {0.0, 0.0};
+    for (int t = 0; t < 2; ++t) {
+        const int j = lane + 32 * t;
+        if (j < h) {
+            du[t] = P.dH[e][(size_t)v * h + j] * lkd_t(P.U[e][k][(size_t)v * h + j], P.slope);
+            P.dU[(size_t)v * h + j] = du[t];
+        }
+    }
+    for (int t = 0; t < 2; ++t) {
+        const int i = lane + 32 * t;  // output row i of phi
+        double hd = 0.0, ag = 0.0;
+        for (int j = 0; j < h; ++j) {
+            const double dj = __shfl_sync(FP_FULL_MASK, du[j >> 5], j & 31);
+            if (i < dk) hd = fma(dj, phw[(size_t)i * h + j], hd);
+            if (i < h) ag = fma(dj, phw[(size_t)(dk + i) * h + j], ag);
+        }
+        if (i < h) {
+            if (k > 0) P.dHn[0][(size_t)v * h + i] = hd;  // direct part of dH_k
+            P.dagg[(size_t)v * h + i] = ag;
+        }
+    }
+}
+
+// message part, gather-formulated over the in-message list of v (each in
+// message (w->v) has a mirror (v->w) with the same edge feature):
+//   Ddst[v] = sum_{w->v} dagg[v] (.) leaky'(P[w] + Q[v] + e we + b)
+//   Dsrc[v] = sum_{v->w} dagg[w] (.) leaky'(P[v] + Q[w] + e we + b)
+//   De[v]   = sum_{w->v} e * dagg[v] (.) leaky'(...)
+// then dH_k = dH_k(direct) + Dsrc @ Ws^T + Ddst @ Wd^T   (k > 0)
+__global__ void gnn_bwd_msg(DevPolicy P, int e, int k) {
+    const int lane = lane_id();
+    const int v = blockIdx.x * 4 + (threadIdx.x >> 5);
+    const int n = P.n, h = P.h;
+    if (v >= n) return;
+    const int dk = k == 0 ? 7 : h;
+    const double *Hk = P.H[e][k];
+    const double *psw = P.W(gnn_role(e, k, 0)), *psb = P.W(gnn_role(e, k, 1));
+    const double s = P.slope;
+    auto pq = [&](int x, int j, bool dst) {  // P[x][j] (dst=false) or Q[x][j]
+        if (k > 0) return dst ? P.Qm[e][k][(size_t)x * h + j] : P.Pm[e][k][(size_t)x * h + j];
+        double acc = 0.0;
+        const int off = dst ? dk : 0;
+        for (int i = 0; i < 7; ++i) acc = fma(Hk[x * 7 + i], psw[(off + i) * h + j], acc);
+        return acc;
+    };
+    double Dd[2] = {0, 0}, Ds[2] = {0, 0}, De[2] = {0, 0};
+    for (int t = 0; t < 2; ++t) {
+        const int j = lane + 32 * t;
+        if (j >= h) continue;
+        const double we = psw[(2 * dk) * h + j], b = psb[j];
+        const double pv = pq(v, j, false), qv = pq(v, j, true);
+        const double gv = P.dagg[(size_t)v * h + j];
+        for (int m = P.adj_ptr[v]; m < P.adj_ptr[v + 1]; ++m) {
+            const int w = P.adj_nbr[m];
+            const double ev = P.adj_e[m];
+            const double din = gv * lkd_t(pq(w, j, false) + qv + ev * we + b, s);
+            Dd[t] += din;
+            De[t] += ev * din;
+            Ds[t] += P.dagg[(size_t)w * h + j] * lkd_t(pv + pq(w, j, true) + ev * we + b, s);
+        }
+        P.Ddst[(size_t)v * h + j] = Dd[t];
+        P.Dsrc[(size_t)v * h + j] = Ds[t];
+        P.De[(size_t)v * h + j] = De[t];
+    }
+    if (k == 0) return;
+    for (int t = 0; t < 2; ++t) {
+        const int i = lane + 32 * t;
+        double acc = 0.0;
+        for (int j = 0; j < h; ++j) {
+            const double sj = __shfl_sync(FP_FULL_MASK, Ds[j >> 5], j & 31);
+            const double dj = __shfl_sync(FP_FULL_MASK, Dd[j >> 5], j & 31);
+            if (i < h) {
+                acc = fma(sj, psw[(size_t)i * h + j], acc);
+                acc = fma(dj, psw[(size_t)(h + i) * h + j], acc);
+            }
+        }
+        if (i < h) P.dHn[0][(size_t)v * h + i] += acc;
+    }
+}
+
+__global__ void copy_kernel(double *dst, const double *src, int count) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < count) dst[i] = src[i];
+}
+
+// ---------------------------------------------------------------------------
+// weight gradients: out[i][j] = sum_r X[r][xoff + i] * Y[r][j]  (X == nullptr:
+// ones -> bias), rows r < R.  Each job writes one row block of one tensor.
+// ---------------------------------------------------------------------------
+struct OuterJob {
+    const double *X;
+    const double *Y;
+    double *out;
+    int ldx, xoff, K, ldy, rows, h;
+};
+
+__global__ void outer_kernel(const OuterJob *jobs) {
+    const OuterJob J = jobs[blockIdx.y];
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= J.K * J.h) return;
+    const int i = idx / J.h, j = idx - i * J.h;
+    double acc = 0.0;
+    for (int r = 0; r < J.rows; ++r) {
+        const double x = J.X ? J.X[(size_t)r * J.ldx + J.xoff + i] : 1.0;
+        acc = fma(x, J.Y[(size_t)r * J.ldy + j], acc);
+    }
+    J.out[(size_t)i * J.h + j] = acc;
+}
+
+// PLC small terms + SEL head2 (single block): dWy = dM @ W1c^T, dby = dc @ W1c^T,
+// db1 = dc, dw2/db2 from the reduction, SEL w2 / b2.
+__global__ void small_bwd_kernel(DevPolicy P, double *grad) {
+    const int h = P.h, n = P.n;
+    const double *dc = P.dsmall, *dM = P.dsmall + h, *dw2 = P.dsmall + 6 * h;
+    const double db2 = P.dsmall[7 * h];
+    const double *w1p = P.W(PR_PLC_H1_W);
+    for (int idx = threadIdx.x; idx < 6 * h; idx += blockDim.x) {
+        const int r = idx / h, i = idx - r * h;  // r < 5: Wy row r; r == 5: by
+        const double *src = r < 5 ? dM + r * h : dc;
+        double acc = 0.0;
+        for (int j = 0; j < h; ++j) acc = fma(src[j], w1p[(size_t)(2 * h + i) * h + j], acc);
+        if (r < 5) grad[P.off[PR_PLC_Y_W] + r * h + i] = acc;
+        else grad[P.off[PR_PLC_Y_B] + i] = acc;
+    }
+    for (int j = threadIdx.x; j < h; j += blockDim.x) {
+        grad[P.off[PR_PLC_H1_B] + j] = dc[j];
+        grad[P.off[PR_PLC_H2_W] + j] = dw2[j];
+        // SEL head2: dw2[j] = sum_v ds_v * leaky(hidpre[v][j])
+        double acc = 0.0;
+        for (int v = 0; v < n; ++v) acc = fma(P.ds[v], lk_t(P.hidpre[(size_t)v * h + j], P.slope), acc);
+        grad[P.off[PR_SEL_H2_W] + j] = acc;
+    }
+    if (threadIdx.x == 0) {
+        grad[P.off[PR_PLC_H2_B]] = db2;
+        double acc = 0.0;
+        for (int v = 0; v < n; ++v) acc += P.ds[v];
+        grad[P.off[PR_SEL_H2_B]] = acc;
+    }
+}
+
+__global__ void sgd_kernel(double *params, const double *grad, int64_t count, double lr) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < count) params[i] = params[i] - lr * grad[i];
+}
+
+}  // namespace fp
+
+using namespace fp;
+
+struct fp_train_state {
+    fp::OuterJob *jobs_dev = nullptr;
+    std::vector<std::vector<fp::OuterJob>> batches;  // one launch per stage
+    std::vector<int> stage_offset;
+    double *bound_grad = nullptr;
+    const double *bound_params = nullptr;
+};
+
+void fp_train_state_free(fp_train_state *ts) {
+    if (!ts) return;
+    if (ts->jobs_dev) cudaFree(ts->jobs_dev);
+    delete ts;
+}
+
+namespace fp {
+
+static void add_job(std::vector<OuterJob> &v, const double *X, int ldx, int xoff, int K,
+                    const double *Y, int ldy, int rows, int h, double *out) {
+    v.push_back(OuterJob{X, Y, out, ldx, xoff, K, ldy, rows, h});
+}
+
+// Build the outer-product job lists for a given gradient buffer.
+static int build_jobs(fp_policy *pol, double *grad) {
+    DevPolicy &P = pol->dev;
+    const int n = P.n, h = P.h;
+    auto *ts = pol->train;
+    ts->batches.clear();
+    auto G = [&](int role) { return grad + P.off[role]; };
+    if (P.off[PR_PLC_Y_W] != P.off[PR_PLC_Y_B] + h) {
+        set_error("flat layout must store plc.y.b directly before plc.y.w");
+        return FP_ERR_INVALID;
+    }
+    // stage 0: dc = sum_v dA[v] (read by the small kernel and the W1c job)
+    std::vector<OuterJob> pre;
+    add_job(pre, nullptr, 0, 0, 1, P.dA, h, n, h, P.dsmall);
+    ts->batches.push_back(pre);
+    // stage 1: heads
+    std::vector<OuterJob> head;
+    const double *Hsel = P.H[0][P.K], *Hplc = P.H[P.n_enc - 1][P.K];
+    add_job(head, P.emb, 4 * h, 0, 4 * h, P.dhid, h, n, h, G(PR_SEL_H1_W));
+    add_job(head, nullptr, 0, 0, 1, P.dhid, h, n, h, G(PR_SEL_H1_B));
+    add_job(head, P.x, 5, 0, 5, P.dZ, h, n, h, G(PR_SEL_Z_W));
+    add_job(head, nullptr, 0, 0, 1, P.dZ, h, n, h, G(PR_SEL_Z_B));
+    add_job(head, Hplc, h, 0, h, P.dA, h, n, h, G(PR_PLC_H1_W));
+    add_job(head, Hplc, h, 0, h, P.dG, h, n, h, G(PR_PLC_H1_W) + (size_t)h * h);
+    // W1c rows = [by ; Wy]^T [dc ; dM]: X = rows of [by; Wy] (flat order b, w)
+    add_job(head, P.params + P.off[PR_PLC_Y_B], h, 0, h, P.dsmall, h, 6, h,
+            G(PR_PLC_H1_W) + (size_t)2 * h * h);
+    add_job(head, P.Zp, h, 0, h, P.dA, h, n, h, G(PR_PLC_H1_W) + (size_t)3 * h * h);
+    add_job(head, P.x, 5, 0, 5, P.dZ + (size_t)n * h, h, n, h, G(PR_PLC_Z_W));
+    add_job(head, nullptr, 0, 0, 1, P.dZ + (size_t)n * h, h, n, h, G(PR_PLC_Z_B));
+    ts->batches.push_back(head);
+    // GNN stages: (e, k) in backward order
+    for (int e = 0; e < P.n_enc; ++e)
+        for (int k = P.K - 1; k >= 0; --k) {
+            std::vector<OuterJob> js;
+            const int dk = k == 0 ? 7 : h;
+            add_job(js, P.H[e][k], dk, 0, dk, P.dU, h, n, h, G(gnn_role(e, k, 2)));
+            add_job(js, P.AG[e][k], h, 0, h, P.dU, h, n, h, G(gnn_role(e, k, 2)) + (size_t)dk * h);
+            add_job(js, nullptr, 0, 0, 1, P.dU, h, n, h, G(gnn_role(e, k, 3)));
+            add_job(js, P.H[e][k], dk, 0, dk, P.Dsrc, h, n, h, G(gnn_role(e, k, 0)));
+            add_job(js, P.H[e][k], dk, 0, dk, P.Ddst, h, n, h, G(gnn_role(e, k, 0)) + (size_t)dk * h);
+            add_job(js, nullptr, 0, 0, 1, P.De, h, n, h, G(gnn_role(e, k, 0)) + (size_t)2 * dk * h);
+            add_job(js, nullptr, 0, 0, 1, P.Ddst, h, n, h, G(gnn_role(e, k, 1)));
+            ts->batches.push_back(js);
+        }
+    size_t total = 0;
+    ts->stage_offset.clear();
+    for (auto &b : ts->batches) { ts->stage_offset.push_back((int)total); total += b.size(); }
+    if (ts->jobs_dev) cudaFree(ts->jobs_dev);
+    if (cudaMalloc(&ts->jobs_dev, total * sizeof(OuterJob)) != cudaSuccess) {
+        set_error("cudaMalloc failed for job list");
+        return FP_ERR_CUDA;
+    }
+    std::vector<OuterJob> flat;
+    for (auto &b : ts->batches) flat.insert(flat.end(), b.begin(), b.end());
+    cudaMemcpy(ts->jobs_dev, flat.data(), total * sizeof(OuterJob), cudaMemcpyHostToDevice);
+    ts->bound_grad = grad;
+    ts->bound_params = P.params;
+    return FP_OK;
+}
+
+static void launch_outer(fp_train_state *ts, int stage, cudaStream_t st) {
+    const auto &b = ts->batches[stage];
+    int maxk = 0;
+    for (auto &j : b) maxk = std::max(maxk, j.K * j.h);
+    dim3 grid((maxk + 127) / 128, (unsigned)b.size());
+    outer_kernel<<<grid, 128, 0, st>>>(ts->jobs_dev + ts->stage_offset[stage]);
+}
+
+}  // namespace fp
+
+extern "C" {
+
+int fp_pg_reduce(fp_policy *pol, const double *grad_rows, const double *grad_ep,
+                 const int32_t *assign, const double *alpha, double beta, int32_t B, void *stream) {
+    if (!pol || !grad_rows || !grad_ep || !assign || !alpha || B <= 0) {
+        set_error("bad pg_reduce arguments");
+        return FP_ERR_INVALID;
+    }
+    DevPolicy &P = pol->dev;
+    const int n = P.n, h = P.h, D = pol->problem->dev.d;
+    const int items = n * h + n + 6 * h + 1;
+    cudaStream_t st = (cudaStream_t)stream;
+    pg_reduce_partial<<<dim3((items + 127) / 128, kChunks), 128, 0, st>>>(
+        P, n, h, D, B, grad_rows, grad_ep, assign, alpha, beta);
+    const int total = 2 * n * h + n + 6 * h + 1;
+    pg_reduce_final<<<(total + 127) / 128, 128, 0, st>>>(P, n, h);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FP_ERR_CUDA; }
+    return FP_OK;
+}
+
+int fp_policy_backward(fp_policy *pol, double *grad, void *stream) {
+    if (!pol || !grad) { set_error("null argument"); return FP_ERR_INVALID; }
+    DevPolicy &P = pol->dev;
+    if (!P.params) { set_error("fp_policy_prepare must run before backward"); return FP_ERR_INVALID; }
+    if (!pol->train) pol->train = new fp_train_state();
+    auto *ts = pol->train;
+    if (ts->bound_grad != grad || ts->bound_params != P.params || ts->batches.empty()) {
+        int rc = build_jobs(pol, grad);
+        if (rc) return rc;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    const int n = P.n, h = P.h;
+    const int g4 = (n + 3) / 4;
+    cudaMemsetAsync(grad, 0, sizeof(double) * pol->n_params, st);
+    head_bwd_kernel<<<g4, 128, 0, st>>>(P);
+    path_gather_kernel<<<g4, 128, 0, st>>>(P);
+    launch_outer(ts, 0, st);  // dc
+    small_bwd_kernel<<<1, 128, 0, st>>>(P, grad);
+    launch_outer(ts, 1, st);  // head weight gradients
+    int stage = 2;
+    for (int e = 0; e < P.n_enc; ++e)
+        for (int k = P.K - 1; k >= 0; --k) {
+            gnn_bwd_node<<<g4, 128, 0, st>>>(P, e, k);
+            gnn_bwd_msg<<<g4, 128, 0, st>>>(P, e, k);
+            launch_outer(ts, stage++, st);
+            if (k > 0) copy_kernel<<<(n * h + 255) / 256, 256, 0, st>>>(P.dH[e], P.dHn[0], n * h);
+        }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FP_ERR_CUDA; }
+    return FP_OK;
+}
+
+int fp_sgd_step(double *params, const double *grad, int64_t count, double lr, void *stream) {
+    if (!params || !grad || count < 0) { set_error("bad sgd arguments"); return FP_ERR_INVALID; }
+    if (count == 0) return FP_OK;
+    sgd_kernel<<<(unsigned)((count + 255) / 256), 256, 0, (cudaStream_t)stream>>>(params, grad,
+                                                                                  count, lr);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FP_ERR_CUDA; }
+    return FP_OK;
+}
+
+}  // extern "C"

@@ -306,6 +306,22 @@ class PolicyContext:
         out._forced = ft
         return out
 
+    def policy_gradient(self, batch: RolloutBatch, alpha, beta: float, grad=None, stream=None):
+        """Flat parameter gradient of sum_e alpha_e * sum lp_e + beta * sum ent_e
+        for a rollout made with ``grad=True`` (fp_pg_reduce + fp_policy_backward)."""
+        import torch
+
+        B = batch.assign.shape[0]
+        alpha = torch.as_tensor(alpha, dtype=torch.float64, device="cuda").reshape(B).contiguous()
+        if grad is None:
+            grad = torch.empty(self.layout.size, dtype=torch.float64, device="cuda")
+        N.check(N.lib().fp_pg_reduce(self.handle, N.ptr(batch.grad_rows), N.ptr(batch.grad_ep),
+                                     N.ptr(batch.assign), N.ptr(alpha), ctypes.c_double(beta),
+                                     ctypes.c_int32(B), N.stream_ptr(stream)))
+        N.check(N.lib().fp_policy_backward(self.handle, N.ptr(grad), N.stream_ptr(stream)))
+        batch._alpha = alpha
+        return grad
+
     def grad_ep_stride(self) -> int:
         s = ctypes.c_int64()
         N.check(N.lib().fp_grad_ep_stride(self.handle, ctypes.c_int32(self.cluster.device_count),

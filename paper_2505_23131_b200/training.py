@@ -1,0 +1,319 @@
+"""Stage I/II training on the GPU — mirror of reference ``flowplace/training.py``.
+
+Reference semantics (``training.py:181-216``): per episode, reward = -makespan,
+advantage = reward - mean(all previous returns), loss = -(adv * sum lp +
+w * sum entropy), one SGD step with a linear lr schedule; epsilon linear
+0.2 -> 0.  The B200 trainer runs B episodes per update (B per GPU, episodes
+sharded over ranks):
+
+    encode -> rollout+sim (REINFORCE rows) -> alpha_e = (mk_e + baseline)/B_g
+    -> fp_pg_reduce -> fp_policy_backward -> NCCL allreduce([grad | sum r])
+    -> SGD (lr at the batch's first episode index) -> baseline update
+
+At B_global = 1 this is exactly the reference's per-episode update (the
+baseline is the mean of all previous returns, kept globally across ranks).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import itertools
+import json
+import math
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+
+from . import _native as N
+from .cluster import ClusterSpec
+from .graph import DataflowGraph
+from .heuristics import Assignment, CriticalPathRule
+from .params import (Params, init_policy_params, load_params, param_shapes, save_params)
+from .policy import PolicyConfig, PolicyContext
+from .simulate import exec_time_batch
+
+STAGES = ("imitation", "sim_rl", "system_rl")
+
+
+@dataclass
+class TrainConfig:
+    episodes: int = 500
+    lr0: float = 1e-4
+    lr1: float = 1e-7
+    epsilon0: float = 0.2
+    entropy_weight: float = 1e-2
+    seed: int = 0
+    strategy: str = "fifo"
+
+    def __post_init__(self):
+        if self.episodes < 1:
+            raise ValueError("episodes must be >= 1")
+        if self.entropy_weight < 0:
+            raise ValueError("entropy_weight must be >= 0")
+
+    def to_dict(self) -> dict:
+        return {"episodes": self.episodes, "lr0": self.lr0, "lr1": self.lr1,
+                "epsilon0": self.epsilon0, "entropy_weight": self.entropy_weight,
+                "seed": self.seed, "strategy": self.strategy}
+
+    @classmethod
+    def from_dict(cls, doc: dict) -> "TrainConfig":
+        keys = ("episodes", "lr0", "lr1", "epsilon0", "entropy_weight", "seed", "strategy")
+        return cls(**{k: doc[k] for k in keys if k in doc})
+
+
+@dataclass
+class LinearSchedule:
+    """v0 at step 0, v1 at step ``total``, linear between (nn.py:244-256)."""
+
+    v0: float
+    v1: float
+    total: int
+
+    def value(self, step: int) -> float:
+        if self.total <= 0:
+            return self.v1
+        frac = min(max(step, 0), self.total) / self.total
+        return self.v0 * (1.0 - frac) + self.v1 * frac
+
+
+class RewardTracker:
+    """Baseline = mean of all previously observed returns (training.py:65-78)."""
+
+    def __init__(self):
+        self.returns: list[float] = []
+
+    @property
+    def baseline(self) -> float:
+        return math.fsum(self.returns) / len(self.returns) if self.returns else 0.0
+
+    def observe(self, r: float) -> None:
+        self.returns.append(r)
+
+
+def _episode_seeds(config: TrainConfig, stage: str) -> list[int]:
+    root = np.random.SeedSequence([config.seed, STAGES.index(stage)])
+    return [int(s.generate_state(1)[0]) for s in root.spawn(config.episodes)]
+
+
+@dataclass
+class StageResult:
+    stage: str
+    params: Params
+    curve: list[dict]
+    best_makespan: float | None = None
+    best_assignment: Assignment | None = None
+    encoder_invocations: int = 0
+    final_loss: float | None = None
+
+
+class BatchedTrainer:
+    """B episodes per update on one GPU; ``world`` > 1 shards episodes over
+    ranks (torch.distributed NCCL group) with one allreduce per update."""
+
+    def __init__(self, ctx: PolicyContext, params, config: TrainConfig, batch_size: int = 1024,
+                 world: int = 1, rank: int = 0, group=None, stage: str = "sim_rl",
+                 executor=None):
+        import torch
+
+        self.ctx = ctx
+        self.config = config
+        self.B = int(batch_size)
+        self.world, self.rank, self.group = world, rank, group
+        self.stage = stage
+        self.executor = executor
+        self.Bg = self.B * world
+        self.flat = ctx.flat_params(params).clone()
+        n_params = ctx.layout.size
+        # [grad | sum of returns] -> one allreduce
+        self.gbuf = torch.zeros(n_params + 1, dtype=torch.float64, device="cuda")
+        self.grad = self.gbuf[:n_params]
+        self.alpha = torch.empty(self.B, dtype=torch.float64, device="cuda")
+        self.ret_sum = torch.zeros(1, dtype=torch.float64, device="cuda")  # global
+        self.count = 0                                                     # global episodes
+        self.updates = 0
+        self.lr_sched = LinearSchedule(config.lr0, config.lr1, config.episodes)
+        self.eps_sched = LinearSchedule(config.epsilon0, 0.0, config.episodes)
+        self.out = None
+
+    def load_flat(self, flat):
+        self.flat.copy_(flat)
+
+    def params(self) -> Params:
+        return self.ctx.layout.unflatten(self.flat.cpu().numpy())
+
+    def launches_per_step(self) -> int:
+        pc = self.ctx.config
+        n_enc = 1 if pc.shared_encoder else 2
+        # encode (K+1) + rollout + reduce (2) + alpha/baseline (torch ops: not ours)
+        # + backward (head 2 + outer 2 + small 1 + per (enc, round) 3 (+copy)) + sgd
+        per_round = n_enc * pc.k_rounds * 4 - n_enc
+        return (pc.k_rounds + 1) + 1 + 2 + 5 + per_round + 1
+
+    def step(self, seed: int, out=None, kernel_events=None, record=False):
+        """One update over B local episodes.  Returns host stats when
+        ``record`` (makespans, advantages, epsilon, lr) — that needs a sync."""
+        import torch
+        import torch.distributed as dist
+
+        ctx = self.ctx
+        ep0 = self.count  # global episodes before this batch
+        eps = 0.0 if self.stage == "imitation" else self.eps_sched.value(ep0)
+        lr = self.lr_sched.value(ep0)
+        if out is None:
+            out = self.out = self.out or ctx.alloc_batch(self.B, grad=True)
+        ctx.prepare(self.flat)
+        if kernel_events is not None:
+            kernel_events[0].record()
+        mode = "teacher" if self.stage == "imitation" else "sample"
+        ctx.rollout_batch(self.flat, self.B, eps, seed, mode=mode, grad=True, out=out,
+                          episode_base=self.rank * self.B, prepare=False,
+                          simulate=self.executor is None, strategy=self.config.strategy)
+        if kernel_events is not None:
+            kernel_events[1].record()
+        if self.executor is not None:
+            # Stage III: rewards from an external executor (host callable)
+            assign = out.assign.cpu().numpy()
+            mk = [float(self.executor(ctx.graph, Assignment(tuple(int(x) for x in a))))
+                  for a in assign]
+            out.makespan = torch.tensor(mk, dtype=torch.float64, device="cuda")
+        mk = out.makespan
+        # alpha_e = -adv_e / B_g, adv_e = -mk_e - baseline
+        if self.stage == "imitation":
+            self.alpha.fill_(-1.0 / self.Bg)
+            beta = 0.0
+        else:
+            base = self.ret_sum / self.count if self.count else torch.zeros_like(self.ret_sum)
+            torch.add(mk, base, out=self.alpha).mul_(1.0 / self.Bg)
+            beta = -self.config.entropy_weight / self.Bg
+        N.check(N.lib().fp_pg_reduce(ctx.handle, N.ptr(out.grad_rows), N.ptr(out.grad_ep),
+                                     N.ptr(out.assign), N.ptr(self.alpha), ctypes.c_double(beta),
+                                     ctypes.c_int32(self.B), N.stream_ptr()))
+        N.check(N.lib().fp_policy_backward(ctx.handle, N.ptr(self.grad), N.stream_ptr()))
+        torch.sum(mk, dim=0, keepdim=True, out=self.gbuf[-1:]).neg_()
+        if self.world > 1:
+            dist.all_reduce(self.gbuf, op=dist.ReduceOp.SUM, group=self.group)
+        N.check(N.lib().fp_sgd_step(N.ptr(self.flat), N.ptr(self.grad),
+                                    ctypes.c_int64(self.grad.numel()), ctypes.c_double(lr),
+                                    N.stream_ptr()))
+        if record:
+            base_host = float(self.ret_sum.item() / self.count) if self.count else 0.0
+        self.ret_sum += self.gbuf[-1:]
+        self.count += self.Bg
+        self.updates += 1
+        if record:
+            mkh = mk.cpu().numpy()
+            return {"makespan": mkh, "advantage": -mkh - base_host, "epsilon": eps, "lr": lr,
+                    "assign": out.assign.cpu().numpy()}
+        return None
+
+
+def _stage(stage: str, graph, cluster, config: TrainConfig, pconfig: PolicyConfig, params,
+           context=None, batch_size: int = 1, executor=None, world=1, rank=0, group=None):
+    ctx = context or PolicyContext(graph, cluster, pconfig)
+    start_enc = ctx.encode_count
+    tr = BatchedTrainer(ctx, params, config, batch_size, world, rank, group, stage, executor)
+    seeds = _episode_seeds(config, stage)
+    curve = []
+    best_mk, best_assign = None, None
+    n_updates = (config.episodes + tr.Bg - 1) // tr.Bg
+    for u in range(n_updates):
+        st = tr.step(seed=seeds[min(u * tr.Bg, len(seeds) - 1)], record=True)
+        for b in range(tr.B):
+            idx = u * tr.Bg + rank * tr.B + b
+            mk = float(st["makespan"][b])
+            row = {"index": idx, "makespan_ms": mk, "advantage": float(st["advantage"][b]),
+                   "epsilon": st["epsilon"], "lr": st["lr"]}
+            if stage == "imitation":
+                row["advantage"] = 0.0
+            curve.append(row)
+            if best_mk is None or mk < best_mk:
+                best_mk = mk
+                best_assign = Assignment(tuple(int(x) for x in st["assign"][b]), "doppler")
+    out_params = tr.params()
+    if isinstance(params, dict):  # keep the caller's dict in sync (reference mutates in place)
+        for k, v in out_params.items():
+            if k in params and hasattr(params[k], "data"):
+                params[k].data[...] = v.data
+    return StageResult(stage, params if isinstance(params, dict) else out_params, curve,
+                       best_makespan=None if stage == "imitation" else best_mk,
+                       best_assignment=None if stage == "imitation" else best_assign,
+                       encoder_invocations=ctx.encode_count - start_enc)
+
+
+def imitation_stage(graph, cluster, config, pconfig, params, teacher=None, context=None,
+                    batch_size: int = 1, **kw):
+    """Teacher-forced behavioural cloning of CriticalPathRule (training.py:129-155)."""
+    if teacher is not None and not isinstance(teacher, CriticalPathRule):
+        raise NotImplementedError("the CUDA trainer imitates CriticalPathRule")
+    return _stage("imitation", graph, cluster, config, pconfig, params, context, batch_size, **kw)
+
+
+def sim_rl_stage(graph, cluster, config, pconfig, params, context=None, batch_size: int = 1,
+                 **kw):
+    """Policy gradient with the clean GPU simulator as reward (training.py:219-232)."""
+    return _stage("sim_rl", graph, cluster, config, pconfig, params, context, batch_size, **kw)
+
+
+def system_rl_stage(graph, cluster, executor, config, pconfig, params, context=None,
+                    batch_size: int = 1, **kw):
+    """Policy gradient with rewards from an executor (training.py:235-248)."""
+
+    def safe(g, a):
+        try:
+            return float(executor(g, a))
+        except Exception as exc:  # noqa: BLE001 — reference wraps every failure
+            raise RuntimeError(f"executor failed: {exc}") from exc
+
+    return _stage("system_rl", graph, cluster, config, pconfig, params, context, batch_size,
+                  executor=safe, **kw)
+
+
+class SimulatorExecutor:
+    """Executor stand-in: the GPU simulator with per-call jitter seeds
+    (training.py:81-102; reference-exact host jitter tables)."""
+
+    def __init__(self, cluster: ClusterSpec, strategy: str = "fifo", jitter_sigma: float = 0.1,
+                 base_seed: int = 0):
+        if jitter_sigma > 0:
+            cluster = ClusterSpec.from_dict({**cluster.to_dict(), "jitter_sigma": jitter_sigma})
+        self.cluster = cluster
+        self.strategy = strategy
+        self.base_seed = base_seed
+        self._calls = itertools.count()
+
+    def __call__(self, graph: DataflowGraph, assignment) -> float:
+        seed = self.base_seed + next(self._calls)
+        mk = exec_time_batch(graph, [list(assignment)], self.cluster, self.strategy, seed=seed)
+        return float(mk[0])
+
+
+SIDECAR_SUFFIX = ".sidecar.json"
+
+
+def save_checkpoint(path, params, pconfig: PolicyConfig, config: TrainConfig,
+                    norm_stats: dict | None = None) -> None:
+    path = Path(path)
+    save_params(params, path)
+    sidecar = {"policy": pconfig.to_dict(), "train": config.to_dict(),
+               "feature_norm": norm_stats or {},
+               "epsilon": {"v0": config.epsilon0, "v1": 0.0, "total": config.episodes}}
+    Path(str(path) + SIDECAR_SUFFIX).write_text(json.dumps(sidecar, indent=2, sort_keys=True) + "\n")
+
+
+def load_checkpoint(path):
+    path = Path(path)
+    params = load_params(path)
+    sc = Path(str(path) + SIDECAR_SUFFIX)
+    sidecar = json.loads(sc.read_text()) if sc.exists() else {}
+    pconfig = PolicyConfig.from_dict(sidecar.get("policy", {}))
+    want = param_shapes(pconfig)
+    if set(want) != set(params):
+        raise ValueError(f"checkpoint does not match policy config: "
+                         f"{sorted(set(want) ^ set(params))}")
+    for name, shape in want.items():
+        if params[name].shape != shape:
+            raise ValueError(f"checkpoint tensor {name} has shape {params[name].shape}, "
+                             f"expected {shape}")
+    return params, pconfig, sidecar
