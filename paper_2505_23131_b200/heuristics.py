@@ -68,3 +68,38 @@ class ForcedActions:
 
     def __init__(self, actions):
         self.actions = np.asarray(actions, dtype=np.int32)
+
+
+class BruteForceCapError(ValueError):
+    pass
+
+
+def brute_force_optimal(graph, cluster, strategy: str = "fifo", cap: int = 1 << 20,
+                        features=None, batch: int = 65536):
+    """Exhaustive oracle (reference heuristics.py:183-212) as batched GPU
+    simulations: every assignment of the non-entry vertices (entries pinned to
+    device 0), argmin makespan, ties to the lexicographically smallest."""
+    import itertools
+
+    from .simulate import SimProblem
+
+    n, d = len(graph), cluster.device_count
+    if d ** n > cap:
+        raise BruteForceCapError(f"{d}**{n} assignments exceed the cap of {cap}")
+    import torch
+
+    prob = SimProblem(graph, cluster, features)
+    free = [v for v in range(n) if not graph.is_entry(v)]
+    combos = np.array(list(itertools.product(range(d), repeat=len(free))), dtype=np.int32)
+    combos = combos.reshape(-1, len(free))
+    best, best_mk = None, None
+    for s in range(0, len(combos), batch):
+        part = combos[s:s + batch]
+        a = np.zeros((len(part), n), dtype=np.int32)
+        a[:, free] = part
+        out = prob.simulate(torch.from_numpy(a).cuda(), strategy)
+        mk = out["makespan"].cpu().numpy()
+        i = int(np.argmin(mk))  # first minimum = lexicographically smallest
+        if best_mk is None or mk[i] < best_mk:
+            best_mk, best = float(mk[i]), tuple(int(x) for x in a[i])
+    return Assignment(best, "brute_force"), best_mk

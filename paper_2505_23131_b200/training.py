@@ -108,6 +108,46 @@ class StageResult:
     final_loss: float | None = None
 
 
+class GlobalUpdate:
+    """Device-agnostic part of one batched update shared by every rank:
+    the running-mean baseline over ALL previous returns of all ranks
+    (training.py:65-78, 196-198), alpha_e = (mk_e + baseline) / B_g, and the
+    single collective: allreduce(SUM) of [flat grad | sum of local returns]."""
+
+    def __init__(self, n_params: int, batch_size: int, world: int = 1, group=None,
+                 device="cuda"):
+        import torch
+
+        self.world, self.group = world, group
+        self.Bg = batch_size * world
+        self.gbuf = torch.zeros(n_params + 1, dtype=torch.float64, device=device)
+        self.grad = self.gbuf[:n_params]
+        self.ret_sum = torch.zeros(1, dtype=torch.float64, device=device)
+        self.count = 0
+
+    def baseline(self):
+        import torch
+
+        return self.ret_sum / self.count if self.count else torch.zeros_like(self.ret_sum)
+
+    def alpha(self, makespan, out):
+        """alpha_e = -advantage_e / B_g with advantage_e = -mk_e - baseline."""
+        import torch
+
+        return torch.add(makespan, self.baseline(), out=out).mul_(1.0 / self.Bg)
+
+    def finish(self, makespan):
+        """Append sum of local returns, allreduce, advance the baseline."""
+        import torch
+        import torch.distributed as dist
+
+        torch.sum(makespan, dim=0, keepdim=True, out=self.gbuf[-1:]).neg_()
+        if self.world > 1:
+            dist.all_reduce(self.gbuf, op=dist.ReduceOp.SUM, group=self.group)
+        self.ret_sum += self.gbuf[-1:]
+        self.count += self.Bg
+
+
 class BatchedTrainer:
     """B episodes per update on one GPU; ``world`` > 1 shards episodes over
     ranks (torch.distributed NCCL group) with one allreduce per update."""
@@ -125,13 +165,9 @@ class BatchedTrainer:
         self.executor = executor
         self.Bg = self.B * world
         self.flat = ctx.flat_params(params).clone()
-        n_params = ctx.layout.size
-        # [grad | sum of returns] -> one allreduce
-        self.gbuf = torch.zeros(n_params + 1, dtype=torch.float64, device="cuda")
-        self.grad = self.gbuf[:n_params]
+        self.upd = GlobalUpdate(ctx.layout.size, self.B, world, group)
+        self.grad = self.upd.grad
         self.alpha = torch.empty(self.B, dtype=torch.float64, device="cuda")
-        self.ret_sum = torch.zeros(1, dtype=torch.float64, device="cuda")  # global
-        self.count = 0                                                     # global episodes
         self.updates = 0
         self.lr_sched = LinearSchedule(config.lr0, config.lr1, config.episodes)
         self.eps_sched = LinearSchedule(config.epsilon0, 0.0, config.episodes)
@@ -155,10 +191,9 @@ class BatchedTrainer:
         """One update over B local episodes.  Returns host stats when
         ``record`` (makespans, advantages, epsilon, lr) — that needs a sync."""
         import torch
-        import torch.distributed as dist
 
         ctx = self.ctx
-        ep0 = self.count  # global episodes before this batch
+        ep0 = self.upd.count  # global episodes before this batch
         eps = 0.0 if self.stage == "imitation" else self.eps_sched.value(ep0)
         lr = self.lr_sched.value(ep0)
         if out is None:
@@ -180,27 +215,22 @@ class BatchedTrainer:
             out.makespan = torch.tensor(mk, dtype=torch.float64, device="cuda")
         mk = out.makespan
         # alpha_e = -adv_e / B_g, adv_e = -mk_e - baseline
+        if record:
+            base_host = float(self.upd.baseline().item())
         if self.stage == "imitation":
             self.alpha.fill_(-1.0 / self.Bg)
             beta = 0.0
         else:
-            base = self.ret_sum / self.count if self.count else torch.zeros_like(self.ret_sum)
-            torch.add(mk, base, out=self.alpha).mul_(1.0 / self.Bg)
+            self.upd.alpha(mk, self.alpha)
             beta = -self.config.entropy_weight / self.Bg
         N.check(N.lib().fp_pg_reduce(ctx.handle, N.ptr(out.grad_rows), N.ptr(out.grad_ep),
                                      N.ptr(out.assign), N.ptr(self.alpha), ctypes.c_double(beta),
                                      ctypes.c_int32(self.B), N.stream_ptr()))
         N.check(N.lib().fp_policy_backward(ctx.handle, N.ptr(self.grad), N.stream_ptr()))
-        torch.sum(mk, dim=0, keepdim=True, out=self.gbuf[-1:]).neg_()
-        if self.world > 1:
-            dist.all_reduce(self.gbuf, op=dist.ReduceOp.SUM, group=self.group)
+        self.upd.finish(mk)
         N.check(N.lib().fp_sgd_step(N.ptr(self.flat), N.ptr(self.grad),
                                     ctypes.c_int64(self.grad.numel()), ctypes.c_double(lr),
                                     N.stream_ptr()))
-        if record:
-            base_host = float(self.ret_sum.item() / self.count) if self.count else 0.0
-        self.ret_sum += self.gbuf[-1:]
-        self.count += self.Bg
         self.updates += 1
         if record:
             mkh = mk.cpu().numpy()
