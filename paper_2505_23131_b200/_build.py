@@ -16,6 +16,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 ROOT = PKG.parent
 LIB = PKG / "_flowplace_b200.so"
+PROF_LIB = PKG / "_flowplace_b200_prof.so"  # phase-profiling build (tools/ only)
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -34,23 +35,26 @@ def deps() -> list[Path]:
     return sources() + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "flowplace_b200.h"]
 
 
-def stale() -> bool:
-    if not LIB.exists():
+def stale(lib: Path = LIB) -> bool:
+    if not lib.exists():
         return True
-    t = LIB.stat().st_mtime
+    t = lib.stat().st_mtime
     return any(p.stat().st_mtime > t for p in deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not stale():
-        return LIB
-    objdir = PKG / "build"
+def build(force: bool = False, verbose: bool = False, profile: bool = False) -> Path:
+    lib = PROF_LIB if profile else LIB
+    if not force and not stale(lib):
+        return lib
+    objdir = PKG / ("build_prof" if profile else "build")
     objdir.mkdir(exist_ok=True)
     objs = []
     flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                     "--expt-relaxed-constexpr", "-I", str(ROOT / "include")]
     if verbose:
         flags += ["-Xptxas", "-v"]
+    if profile:
+        flags += ["-DFP_PHASE_PROFILE"]
     for src in sources():
         obj = objdir / (src.stem + ".o")
         cmd = [nvcc(), "-c", str(src), "-o", str(obj)] + flags
@@ -60,16 +64,16 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         if verbose and r.stderr:
             print(r.stderr, file=sys.stderr)
         objs.append(str(obj))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [nvcc(), "-shared", "-o", str(tmp)] + [str(o) for o in objs] + ARCH + [
         "-Xcompiler", "-fPIC"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc link failed:\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv,
+                profile="--profile" in sys.argv))

@@ -47,7 +47,9 @@ class FpGraphDesc(ctypes.Structure):
 def lib() -> ctypes.CDLL:
     global _lib
     if _lib is None:
-        path = Path(_LIB_PATH)
+        import os
+
+        path = Path(os.environ.get("FLOWPLACE_B200_LIB", str(_LIB_PATH)))
         if not path.exists():
             raise RuntimeError(
                 f"CUDA library {path} is not built; run `python -m paper_2505_23131_b200._build`"

@@ -6,6 +6,38 @@
 
 #define FP_FULL_MASK 0xffffffffu
 
+// Phase profiling (profiling build only: -DFP_PHASE_PROFILE).  Accumulates
+// clock64 deltas per phase into g_phase_cycles[phase] (one atomic per warp
+// per phase per step, lane 0) -- never compiled into the product library.
+#ifdef FP_PHASE_PROFILE
+static __device__ unsigned long long g_phase_cycles[64];
+static __device__ unsigned long long g_phase_count[64];
+// per-warp register accumulators (constant phase ids), flushed once per warp
+#define FP_PHASE_DECL unsigned long long fp_acc_[32] = {0}; unsigned fp_cnt_[32] = {0}
+#define FP_PHASE_BEGIN(var) long long var = clock64()
+#define FP_PHASE_END(var, id)                                     \
+    do {                                                          \
+        long long now_ = clock64();                               \
+        fp_acc_[(id) & 31] += (unsigned long long)(now_ - var);   \
+        fp_cnt_[(id) & 31] += 1;                                  \
+        var = now_;                                               \
+    } while (0)
+#define FP_PHASE_FLUSH(base)                                                    \
+    do {                                                                        \
+        if ((threadIdx.x & 31) == 0)                                            \
+            for (int i_ = 0; i_ < 32; ++i_)                                     \
+                if (fp_cnt_[i_]) {                                              \
+                    atomicAdd(&g_phase_cycles[(base) + i_], fp_acc_[i_]);        \
+                    atomicAdd(&g_phase_count[(base) + i_], (unsigned long long)fp_cnt_[i_]); \
+                }                                                               \
+    } while (0)
+#else
+#define FP_PHASE_DECL
+#define FP_PHASE_BEGIN(var)
+#define FP_PHASE_END(var, id)
+#define FP_PHASE_FLUSH(base)
+#endif
+
 namespace fp {
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }

@@ -92,6 +92,8 @@ __device__ __forceinline__ void sel_chain(const DevProblem &PR, const DevPolicy 
     }
     __syncwarp();
 
+    FP_PHASE_DECL;
+    FP_PHASE_BEGIN(ps);
     for (int step = 0; step < n; ++step) {
         // compact the candidate bitset into an ascending list
         const uint32_t cw = lane < W ? cand[lane] : 0u;
@@ -112,6 +114,7 @@ __device__ __forceinline__ void sel_chain(const DevProblem &PR, const DevPolicy 
             }
         }
         __syncwarp();
+        FP_PHASE_END(ps, 0);
         const bool fast = k <= 32;  // candidate i on lane i, values in registers
         int idx = -1;
         double e0 = 0.0, cum0 = 0.0, tot;
@@ -186,6 +189,7 @@ __device__ __forceinline__ void sel_chain(const DevProblem &PR, const DevPolicy 
                 }
             }
         }
+        FP_PHASE_END(ps, 1);
         int amax = -1;
         if (want_amax || mode == FP_MODE_GREEDY) {
             // first maximum of p = e / tot (policy.py:309, 396)
@@ -207,6 +211,7 @@ __device__ __forceinline__ void sel_chain(const DevProblem &PR, const DevPolicy 
         // publish early: the PLC warp only needs the vertex (a single 32-bit
         // store replacing the -3 sentinel is the whole hand-off)
         if (lane == 0) order[step] = v;
+        FP_PHASE_END(ps, 2);
         if (want_lp) {
             const double ek = eps / (double)k;
             double entp = 0.0, lp = 0.0, pidx = 0.0, midx = 0.0, qp = 0.0;
@@ -241,6 +246,7 @@ __device__ __forceinline__ void sel_chain(const DevProblem &PR, const DevPolicy 
                 if (A.step_ent) A.step_ent[2 * o] = ent;
             }
         }
+        FP_PHASE_END(ps, 3);
         if (lane == 0) {
             const size_t o = (size_t)ep * n + step;
             if (A.step_vd) A.step_vd[2 * o] = v;
@@ -254,7 +260,9 @@ __device__ __forceinline__ void sel_chain(const DevProblem &PR, const DevPolicy 
             if (atomicSub(&npl[w], 1) == 1) atomicOr(&cand[w >> 5], 1u << (w & 31));
         }
         __syncwarp();
+        FP_PHASE_END(ps, 4);
     }
+    FP_PHASE_FLUSH(0);
     if constexpr (GRAD) {
         double *g = A.grad_ep + (size_t)ep * grad_ep_stride(n, PO.h, PR.d);
         for (int v = lane; v < n; v += 32) { g[v] = dsl[v]; g[n + v] = dse[v]; }
@@ -324,10 +332,13 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
     }
     __syncwarp();
     int status = FP_EP_OK;
+    FP_PHASE_DECL;
+    FP_PHASE_BEGIN(pp_);
     for (int step = 0; step < n; ++step) {
         int v;
         while ((v = order[step]) == -3) { }
         if (v < 0) { status = v == -1 ? FP_EP_DEADLOCK : FP_EP_BAD_ACTION; break; }
+        FP_PHASE_END(pp_, 10);
         double Av[HPL], Gv[HPL];
 #pragma unroll
         for (int t = 0; t < HPL; ++t) {
@@ -359,6 +370,7 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
             xr[0] = aflops; xr[1] = f1; xr[2] = f2; xr[3] = f3; xr[4] = f4;
         }
         __syncwarp();
+        FP_PHASE_END(pp_, 11);
         // ---- column statistics: lane c < 5 sums over devices in order ----
         if (lane < 5) {
             double col[MAXD];
@@ -390,6 +402,7 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
             }
         }
         __syncwarp();
+        FP_PHASE_END(pp_, 12);
         // ---- pre-activations + head2 partial sums (lane = hidden column) ----
         double pre[MAXD][HPL];
         double part[MAXD];
@@ -436,6 +449,7 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
                 part[0] += __shfl_xor_sync(FP_FULL_MASK, part[0], o);
         }
         const double lgall = __shfl_sync(FP_FULL_MASK, part[0], (lane & (MAXD - 1)) << (5 - LOGD));
+        FP_PHASE_END(pp_, 13);
         const double lg = lane < D ? lgall + b2p : -INFINITY;
         const double lmx = warp_max_redux(lg);
         const double ed = lane < D ? exp(lg - lmx) : 0.0;
@@ -449,6 +463,7 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
             warp_argmax_first(am, ai);
             amax = ai;
         }
+        FP_PHASE_END(pp_, 14);
         int jdx;
         if (mode == FP_MODE_FORCED) {
             jdx = frow[2 * step + 1];
@@ -470,6 +485,7 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
                 jdx = hit ? __ffs(hit) - 1 : D - 1;
             }
         }
+        FP_PHASE_END(pp_, 15);
         if (want_lp) {
             const double ekd = eps / (double)D;
             double mixd = 0.0, lmd = 0.0;
@@ -533,6 +549,7 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
                 }
             }
         }
+        FP_PHASE_END(pp_, 16);
         // ---- commit (timeline.py:47-58) ----
         if (lane == jdx) {
             aflops = __dadd_rn(aflops, flops[v]);
@@ -552,7 +569,9 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
 #pragma unroll
                 for (int t = 0; t < HPL; ++t) Sd[d][t] += Gv[t];
         __syncwarp();
+        FP_PHASE_END(pp_, 17);
     }
+    FP_PHASE_FLUSH(0);
     if constexpr (GRAD) if (status == FP_EP_OK) {
         double *q = A.grad_ep + (size_t)ep * grad_ep_stride(n, h, D) + 2 * n;
 #pragma unroll
@@ -654,6 +673,19 @@ static int dispatch_grad(const fp_problem *p, const fp_policy *pol, const fp_rol
 using namespace fp;
 
 extern "C" {
+
+#ifdef FP_PHASE_PROFILE
+int fp_phase_read(unsigned long long *cycles, unsigned long long *counts, int reset) {
+    cudaMemcpyFromSymbol(cycles, g_phase_cycles, sizeof(unsigned long long) * 64);
+    cudaMemcpyFromSymbol(counts, g_phase_count, sizeof(unsigned long long) * 64);
+    if (reset) {
+        unsigned long long z[64] = {0};
+        cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
+        cudaMemcpyToSymbol(g_phase_count, z, sizeof(z));
+    }
+    return FP_OK;
+}
+#endif
 
 int fp_grad_ep_stride(const fp_policy *pol, int32_t d, int64_t *stride) {
     if (!pol || !stride) { set_error("null argument"); return FP_ERR_INVALID; }

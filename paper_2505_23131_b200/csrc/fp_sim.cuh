@@ -108,6 +108,8 @@ __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *base
     __syncwarp();
 
     SimOut out{0.0, FP_EP_OK, 0};
+    FP_PHASE_DECL;
+    FP_PHASE_BEGIN(pq_);
     int remaining = P.n_nonentry;
     double t = 0.0;
     int seq = 0;
@@ -168,6 +170,7 @@ __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *base
             }
         }
         __syncwarp();
+        FP_PHASE_END(pq_, 21);
         if (tracing) {
             const int k = ctr[0];
             for (int i = lane; i < k; i += 32) {
@@ -201,6 +204,7 @@ __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *base
             return out;
         }
         const double tmin = warp_min_redux(lmin);
+        FP_PHASE_END(pq_, 23);
         if (tracing && lane == 0) ctr[1] = 0;
         __syncwarp();
         int done_exec = 0;
@@ -249,6 +253,7 @@ __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *base
         }
         remaining -= __reduce_add_sync(FP_FULL_MASK, done_exec);
         __syncwarp();
+        FP_PHASE_END(pq_, 24);
         if (tracing) {
             const int k = ctr[1];
             for (int i = lane; i < k; i += 32) {
@@ -273,6 +278,7 @@ __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *base
     }
     out.makespan = t;
     if (tracing && out.n_events > trace_cap) out.status = FP_EP_TRACE_OVERFLOW;
+    FP_PHASE_FLUSH(0);
     return out;
 }
 
