@@ -38,6 +38,10 @@ extern "C" {
 #define FP_STRATEGY_DEPTH_FIRST 1
 #define FP_STRATEGY_BREADTH_FIRST 2
 
+/* launch flags (fp_sim_batch flags, fp_rollout_args.flags) */
+#define FP_FLAG_WIDE 1  /* force the HBM-resident (wide) episode path even when the
+                           compact shared-memory path would fit (tests / benchmarks) */
+
 /* per-episode status codes written by batched kernels */
 #define FP_EP_OK 0
 #define FP_EP_DEADLOCK 1        /* makespan slot holds the deadlock time   */
@@ -80,6 +84,13 @@ int fp_problem_destroy(fp_problem *p);
 /* Shared memory the simulator needs per in-flight episode (bytes). */
 int fp_problem_sim_smem(const fp_problem *p, int64_t *bytes_per_episode);
 
+/* Device workspace fp_sim_batch needs for B simulations (0 when every
+ * episode's state fits the compact shared-memory core).  Graphs whose state
+ * exceeds shared memory (n beyond ~2k at d = 8) run the wide path: a
+ * persistent grid with each resident episode's n-sized state in a slice of
+ * this caller-owned HBM workspace. */
+int fp_sim_workspace_size(const fp_problem *p, int32_t B, int32_t flags, int64_t *bytes);
+
 /* Work-conserving simulation of B assignments (device pointers).
  *   assign   [B][n] int32 device ids
  *   jitter   NULL, or per-task duration factors [n*d + n*d*d] per episode
@@ -87,11 +98,15 @@ int fp_problem_sim_smem(const fp_problem *p, int64_t *bytes_per_episode);
  *            episode b reads jitter + b*jitter_stride (stride 0 = shared)
  *   makespan [B] out; status [B] out (FP_EP_*)
  *   trace    NULL, or [B][trace_cap] events out; trace_len [B] out
- *   blocked  NULL, or [B][n] uint8 out: blocked frontier on deadlock */
+ *   blocked  NULL, or [B][n] uint8 out: blocked frontier on deadlock
+ *   workspace / workspace_bytes: device scratch of fp_sim_workspace_size bytes
+ *            (may be NULL / 0 when that size is 0)
+ *   flags    FP_FLAG_* */
 int fp_sim_batch(const fp_problem *p, const int32_t *assign, int32_t B, int32_t strategy,
                  const double *jitter, int64_t jitter_stride, double *makespan,
                  int32_t *status, fp_event *trace, int32_t trace_cap, int32_t *trace_len,
-                 uint8_t *blocked, void *stream);
+                 uint8_t *blocked, void *workspace, int64_t workspace_bytes, int32_t flags,
+                 void *stream);
 
 /* Drop-in for flowplace/_simcore.pyx:39-45 run_packed: host arrays in, host
  * events out (events[0..*n_events)).  Jitter factors are computed on the host
@@ -160,6 +175,12 @@ typedef struct fp_policy_desc {
     const int32_t *tpath_ptr, *tpath_idx; /* [n+1], SEL t-paths */
     const int64_t *param_offsets;         /* [FP_PARAM_ROLES] */
     int64_t n_params;
+    /* Forest form of the same paths: path(v) = (v, next[v], next[next[v]], ...),
+     * -1 ends a path.  Used when bpath_ptr == NULL (large graphs, where the
+     * explicit lists grow like n * depth); path sums are then computed on the
+     * GPU by pointer jumping.  Forward only: REINFORCE backward needs the
+     * explicit lists. */
+    const int32_t *bnext, *tnext;         /* [n] */
 } fp_policy_desc;
 
 typedef struct fp_policy fp_policy;
@@ -186,6 +207,9 @@ typedef struct fp_rollout_args {
     fp_event *trace;         /* optional simulator trace [B][trace_cap] */
     int32_t trace_cap;
     int32_t *trace_len;
+    int32_t flags;           /* FP_FLAG_* */
+    void *workspace;         /* device scratch, fp_rollout_workspace_size bytes */
+    int64_t workspace_bytes;
 } fp_rollout_args;
 
 int fp_policy_create(const fp_problem *p, const fp_policy_desc *desc, fp_policy **out);
@@ -193,6 +217,12 @@ int fp_policy_destroy(fp_policy *pol);
 /* GNN encode + head tables for one parameter snapshot (params: device flat). */
 int fp_policy_prepare(fp_policy *pol, const double *params, void *stream);
 int fp_policy_table(const fp_policy *pol, int32_t which, const double **ptr, int64_t *count);
+/* Device workspace fp_rollout_batch needs for B episodes (0 on the compact
+ * shared-memory path; graphs beyond it run the wide path, whose per-episode
+ * n-sized state lives in this caller-owned HBM scratch).  grad = 1 for a
+ * rollout that writes REINFORCE rows (compact path only). */
+int fp_rollout_workspace_size(const fp_problem *p, const fp_policy *pol, int32_t B,
+                              int32_t flags, int32_t grad, int64_t *bytes);
 /* Batched SEL/PLC episodes (+ fused WC simulation) — one warp per episode. */
 int fp_rollout_batch(const fp_problem *p, const fp_policy *pol, const fp_rollout_args *args,
                      void *stream);

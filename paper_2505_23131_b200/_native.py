@@ -16,6 +16,7 @@ from ._build import LIB as _LIB_PATH
 
 FP_OK, FP_ERR_INVALID, FP_ERR_CUDA, FP_ERR_UNSUPPORTED, FP_ERR_DEADLOCK, FP_ERR_OVERFLOW = range(6)
 EP_OK, EP_DEADLOCK, EP_TRACE_OVERFLOW, EP_BAD_ACTION = range(4)
+FLAG_WIDE = 1  # force the HBM-resident episode path
 
 _lib = None
 
@@ -85,7 +86,8 @@ def stream_ptr(stream=None) -> ctypes.c_void_p:
 
 EXPORTED = (
     "fp_last_error", "fp_version", "fp_problem_create", "fp_problem_destroy",
-    "fp_problem_sim_smem", "fp_sim_batch", "fp_run_packed", "fp_jitter_tables",
+    "fp_problem_sim_smem", "fp_sim_workspace_size", "fp_sim_batch", "fp_run_packed",
+    "fp_jitter_tables",
 )
 
 
@@ -108,7 +110,9 @@ class FpPolicyDesc(ctypes.Structure):
                 ("shared_encoder", ctypes.c_int32), ("leaky_slope", ctypes.c_double)] + [
         (name, ctypes.c_void_p) for name in (
             "x_static", "adj_ptr", "adj_src", "adj_edge", "bpath_ptr", "bpath_idx",
-            "tpath_ptr", "tpath_idx", "param_offsets")] + [("n_params", ctypes.c_int64)]
+            "tpath_ptr", "tpath_idx", "param_offsets")] + [("n_params", ctypes.c_int64),
+                                                           ("bnext", ctypes.c_void_p),
+                                                           ("tnext", ctypes.c_void_p)]
 
 
 class FpRolloutArgs(ctypes.Structure):
@@ -118,10 +122,12 @@ class FpRolloutArgs(ctypes.Structure):
         (name, ctypes.c_void_p) for name in (
             "forced", "assign", "step_vd", "step_lp", "step_ent", "step_argmax", "step_ncand",
             "makespan", "status", "grad_rows", "grad_ep", "trace")] + [
-        ("trace_cap", ctypes.c_int32), ("trace_len", ctypes.c_void_p)]
+        ("trace_cap", ctypes.c_int32), ("trace_len", ctypes.c_void_p),
+        ("flags", ctypes.c_int32), ("workspace", ctypes.c_void_p),
+        ("workspace_bytes", ctypes.c_int64)]
 
 
 EXPORTED = EXPORTED + (
     "fp_policy_create", "fp_policy_destroy", "fp_policy_prepare", "fp_policy_table",
-    "fp_rollout_batch", "fp_grad_ep_stride", "fp_pg_reduce", "fp_policy_backward", "fp_sgd_step",
+    "fp_rollout_workspace_size", "fp_rollout_batch", "fp_grad_ep_stride", "fp_pg_reduce", "fp_policy_backward", "fp_sgd_step",
 )

@@ -41,63 +41,109 @@ struct Arena {
     }
 };
 
-template <int RPL, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32, 1)
+// One warp per simulation.  Compact path: the whole episode state in the
+// warp's shared-memory slice, one wave.  Wide path (state beyond shared
+// memory): a persistent grid, each resident warp owning one HBM workspace
+// slice of L.gbytes and looping over episodes.
+template <int RPL, int WARPS, bool WIDE>
+__global__ void __launch_bounds__(WARPS * 32)
 sim_batch_kernel(DevProblem P, EpLayout L, const int32_t *__restrict__ assign, int B,
                  int strategy, const double *__restrict__ jit, long long jit_stride,
                  double *__restrict__ makespan, int32_t *__restrict__ status,
                  fp_event *__restrict__ trace, int trace_cap, int32_t *__restrict__ trace_len,
-                 uint8_t *__restrict__ blocked) {
+                 uint8_t *__restrict__ blocked, uint8_t *__restrict__ ws) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int warp = threadIdx.x >> 5;
-    const int ep = blockIdx.x * WARPS + warp;
-    if (ep >= B) return;
-    uint8_t *base = smem + (size_t)warp * L.bytes;
-    uint8_t *as = base + L.assign;
-    const int32_t *row = assign + (size_t)ep * P.n;
-    for (int v = lane_id(); v < P.n; v += 32) as[v] = (uint8_t)row[v];
-    __syncwarp();
-    SimOut o = sim_episode<RPL>(P, base, L, strategy,
-                                jit ? jit + (size_t)ep * jit_stride : nullptr,
-                                trace ? trace + (size_t)ep * trace_cap : nullptr, trace_cap,
-                                blocked ? blocked + (size_t)ep * P.n : nullptr);
-    if (lane_id() == 0) {
-        makespan[ep] = o.makespan;
-        status[ep] = o.status;
-        if (trace_len) trace_len[ep] = o.n_events;
+    const int gw = blockIdx.x * WARPS + warp;
+    uint8_t *sb = smem + (size_t)warp * L.bytes;
+    uint8_t *nb = WIDE ? ws + (size_t)gw * L.gbytes : sb;
+    for (int ep = gw; ep < B; ep += gridDim.x * WARPS) {
+        uint8_t *as = nb + L.assign;
+        const int32_t *row = assign + (size_t)ep * P.n;
+        for (int v = lane_id(); v < P.n; v += 32) as[v] = (uint8_t)row[v];
+        __syncwarp();
+        SimOut o = sim_episode<RPL, WIDE>(P, nb, sb, L, strategy,
+                                          jit ? jit + (size_t)ep * jit_stride : nullptr,
+                                          trace ? trace + (size_t)ep * trace_cap : nullptr,
+                                          trace_cap, blocked ? blocked + (size_t)ep * P.n : nullptr);
+        if (lane_id() == 0) {
+            makespan[ep] = o.makespan;
+            status[ep] = o.status;
+            if (trace_len) trace_len[ep] = o.n_events;
+        }
+        __syncwarp();
     }
+}
+
+constexpr int kSimWarps = 4;
+
+static bool sim_wide(const fp_problem *p, int flags) {
+    const EpLayout L = make_layout(p->dev.n, p->dev.W, p->dev.R, p->dev.SM, false);
+    return (flags & FP_FLAG_WIDE) || (int64_t)L.bytes * kSimWarps > 227 * 1024;
+}
+
+// Resident-episode count of a persistent launch: occupancy x SMs, capped by
+// the batch (one workspace slice per resident warp).
+int persistent_blocks(const void *kern, int threads, int64_t smem, int64_t blocks_needed) {
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, (size_t)smem) !=
+            cudaSuccess || per_sm < 1)
+        per_sm = 1;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(blocks_needed, (int64_t)sms * per_sm));
 }
 
 template <int RPL>
 static int launch_sim_t(const fp_problem *p, const int32_t *assign, int B, int strategy,
                         const double *jit, long long jstride, double *mk, int32_t *st,
                         fp_event *trace, int cap, int32_t *tlen, uint8_t *blocked,
+                        void *ws, int64_t ws_bytes, int flags, int64_t *ws_needed,
                         cudaStream_t stream) {
-    constexpr int WARPS = 4;
-    const EpLayout L = make_layout(p->dev.n, p->dev.W, p->dev.R, p->dev.SM, false);
+    constexpr int WARPS = kSimWarps;
+    const bool wide = sim_wide(p, flags);
+    const EpLayout L = make_layout(p->dev.n, p->dev.W, p->dev.R, p->dev.SM, false, 0, wide);
     const int64_t smem = (int64_t)L.bytes * WARPS;
     if (smem > 227 * 1024) {
-        set_error("simulator state exceeds shared memory (n/d too large for the smem core)");
+        set_error("simulator scratch exceeds shared memory (too many devices / slots)");
         return FP_ERR_UNSUPPORTED;
     }
-    auto kern = sim_batch_kernel<RPL, WARPS>;
+    const void *kern = wide ? (const void *)sim_batch_kernel<RPL, WARPS, true>
+                            : (const void *)sim_batch_kernel<RPL, WARPS, false>;
     FP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int grid = (B + WARPS - 1) / WARPS;
-    kern<<<grid, WARPS * 32, smem, stream>>>(p->dev, L, assign, B, strategy, jit, jstride, mk,
-                                             st, trace, cap, tlen, blocked);
+    const int64_t need_blocks = (B + WARPS - 1) / WARPS;
+    const int grid = wide ? persistent_blocks(kern, WARPS * 32, smem, need_blocks)
+                          : (int)need_blocks;
+    const int64_t need = wide ? (int64_t)grid * WARPS * L.gbytes : 0;
+    if (ws_needed) { *ws_needed = need; return FP_OK; }
+    if (need > 0 && (!ws || ws_bytes < need)) {
+        set_error("workspace too small for the HBM-resident simulator (see fp_sim_workspace_size)");
+        return FP_ERR_INVALID;
+    }
+    if (wide)
+        sim_batch_kernel<RPL, WARPS, true><<<grid, WARPS * 32, smem, stream>>>(
+            p->dev, L, assign, B, strategy, jit, jstride, mk, st, trace, cap, tlen, blocked,
+            (uint8_t *)ws);
+    else
+        sim_batch_kernel<RPL, WARPS, false><<<grid, WARPS * 32, smem, stream>>>(
+            p->dev, L, assign, B, strategy, jit, jstride, mk, st, trace, cap, tlen, blocked,
+            nullptr);
     FP_CUDA(cudaGetLastError());
     return FP_OK;
 }
 
 static int launch_sim(const fp_problem *p, const int32_t *assign, int B, int strategy,
                       const double *jit, long long jstride, double *mk, int32_t *st,
-                      fp_event *trace, int cap, int32_t *tlen, uint8_t *blocked,
-                      cudaStream_t stream) {
+                      fp_event *trace, int cap, int32_t *tlen, uint8_t *blocked, void *ws,
+                      int64_t ws_bytes, int flags, int64_t *ws_needed, cudaStream_t stream) {
     const int R = p->dev.R;
-    if (R <= 32) return launch_sim_t<1>(p, assign, B, strategy, jit, jstride, mk, st, trace, cap, tlen, blocked, stream);
-    if (R <= 96) return launch_sim_t<3>(p, assign, B, strategy, jit, jstride, mk, st, trace, cap, tlen, blocked, stream);
-    if (R <= 288) return launch_sim_t<9>(p, assign, B, strategy, jit, jstride, mk, st, trace, cap, tlen, blocked, stream);
-    return launch_sim_t<33>(p, assign, B, strategy, jit, jstride, mk, st, trace, cap, tlen, blocked, stream);
+#define FP_SIM_ARGS p, assign, B, strategy, jit, jstride, mk, st, trace, cap, tlen, blocked, ws, \
+                    ws_bytes, flags, ws_needed, stream
+    if (R <= 32) return launch_sim_t<1>(FP_SIM_ARGS);
+    if (R <= 96) return launch_sim_t<3>(FP_SIM_ARGS);
+    if (R <= 288) return launch_sim_t<9>(FP_SIM_ARGS);
+    return launch_sim_t<33>(FP_SIM_ARGS);
+#undef FP_SIM_ARGS
 }
 
 }  // namespace fp
@@ -238,15 +284,24 @@ int fp_problem_sim_smem(const fp_problem *p, int64_t *bytes) {
     return FP_OK;
 }
 
+int fp_sim_workspace_size(const fp_problem *p, int32_t B, int32_t flags, int64_t *bytes) {
+    if (!p || !bytes) { set_error("null argument"); return FP_ERR_INVALID; }
+    *bytes = 0;
+    if (B <= 0) return FP_OK;
+    return launch_sim(p, nullptr, B, 0, nullptr, 0, nullptr, nullptr, nullptr, 0, nullptr,
+                      nullptr, nullptr, 0, flags, bytes, 0);
+}
+
 int fp_sim_batch(const fp_problem *p, const int32_t *assign, int32_t B, int32_t strategy,
                  const double *jitter, int64_t jitter_stride, double *makespan, int32_t *status,
                  fp_event *trace, int32_t trace_cap, int32_t *trace_len, uint8_t *blocked,
-                 void *stream) {
+                 void *workspace, int64_t workspace_bytes, int32_t flags, void *stream) {
     if (!p || !assign || !makespan || !status) { set_error("null argument"); return FP_ERR_INVALID; }
     if (strategy < 0 || strategy > 2) { set_error("unknown strategy"); return FP_ERR_INVALID; }
     if (B <= 0) return FP_OK;
     return launch_sim(p, assign, B, strategy, jitter, jitter_stride, makespan, status, trace,
-                      trace_cap, trace_len, blocked, (cudaStream_t)stream);
+                      trace_cap, trace_len, blocked, workspace, workspace_bytes, flags, nullptr,
+                      (cudaStream_t)stream);
 }
 
 // ---- host libm jitter (the reference recipe, _simcore.pyx:15-36) ----------
@@ -324,28 +379,40 @@ int fp_run_packed(int32_t n, int32_t d, const int32_t *pred_indptr, const int32_
     }
     double *d_mk = (double *)(dmem + off_m);
     int32_t *d_st = (int32_t *)(dmem + off_m + 64), *d_len = (int32_t *)(dmem + off_m + 128);
+    int64_t ws_need = 0;
+    rc = launch_sim(p, nullptr, 1, strategy, nullptr, 0, nullptr, nullptr, nullptr, 0, nullptr,
+                    nullptr, nullptr, 0, 0, &ws_need, 0);
+    if (rc) return fail(rc);
+    void *ws = nullptr;
+    if (ws_need > 0 && cudaMalloc(&ws, ws_need) != cudaSuccess) {
+        set_error("cudaMalloc failed for the simulator workspace");
+        return fail(FP_ERR_CUDA);
+    }
     rc = launch_sim(p, (const int32_t *)dmem, 1, strategy, jn ? (const double *)(dmem + off_j) : nullptr,
                     0, d_mk, d_st, events ? (fp_event *)(dmem + off_t) : nullptr, cap, d_len,
-                    dmem + off_b, 0);
-    if (rc) return fail(rc);
+                    dmem + off_b, ws, ws_need, 0, nullptr, 0);
+    if (rc) { if (ws) cudaFree(ws); return fail(rc); }
     double mk = 0.0;
     int32_t st = 0, len = 0;
     if (cudaMemcpy(&mk, d_mk, 8, cudaMemcpyDeviceToHost) != cudaSuccess ||
         cudaMemcpy(&st, d_st, 4, cudaMemcpyDeviceToHost) != cudaSuccess ||
         cudaMemcpy(&len, d_len, 4, cudaMemcpyDeviceToHost) != cudaSuccess) {
         set_error(std::string("simulator kernel failed: ") + cudaGetErrorString(cudaGetLastError()));
+        if (ws) cudaFree(ws);
         return fail(FP_ERR_CUDA);
     }
     if (events && len > 0 &&
         cudaMemcpy(events, dmem + off_t, (size_t)std::min(len, cap) * sizeof(fp_event),
                    cudaMemcpyDeviceToHost) != cudaSuccess) {
         set_error("event download failed");
+        if (ws) cudaFree(ws);
         return fail(FP_ERR_CUDA);
     }
     if (blocked && st == FP_EP_DEADLOCK)
         cudaMemcpy(blocked, dmem + off_b, (size_t)n, cudaMemcpyDeviceToHost);
     *makespan = mk;
     if (n_events) *n_events = len;
+    if (ws) cudaFree(ws);
     cudaFree(dmem);
     fp_problem_destroy(p);
     if (st == FP_EP_DEADLOCK) { set_error("deadlock"); return FP_ERR_DEADLOCK; }

@@ -195,6 +195,28 @@ encode_round_kernel(DevPolicy P, int k, int last) {
     }
 }
 
+// Forest-form path sums (large graphs): S(v) = sum of H over path(v), by
+// pointer jumping -- after round r, S(v) covers the first 2^(r+1) vertices of
+// path(v) and J(v) points 2^(r+1) vertices down it (-1 past the end).
+// Round 0 reads H and the next arrays; round r >= 1 ping-pongs PS/PJ.
+// Pure gather-add over n x h doubles per round (HBM / L2 bound).
+__global__ void path_jump_kernel(DevPolicy P, int r) {
+    const int which = blockIdx.y;  // 0 = b-paths, 1 = t-paths
+    const int n = P.n, h = P.h;
+    const double *Sin = r == 0 ? P.H[0][P.K] : P.PS[which][(r - 1) & 1];
+    const int *Jin = r == 0 ? P.nxt[which] : P.PJ[which][(r - 1) & 1];
+    double *Sout = P.PS[which][r & 1];
+    int *Jout = P.PJ[which][r & 1];
+    const int64_t total = (int64_t)n * h;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int v = (int)(i / h), j = (int)(i - (int64_t)v * h);
+        const int w = Jin[v];
+        Sout[i] = w >= 0 ? Sin[i] + Sin[(size_t)w * h + j] : Sin[i];
+        if (j == 0) Jout[v] = w >= 0 ? Jin[w] : -1;
+    }
+}
+
 // SEL head over every vertex: s[v] = head(H[v] | sum_bpath H | sum_tpath H | Z[v]).
 template <int HPL>
 __global__ void __launch_bounds__(kEncWarps * 32) encode_sel_kernel(DevPolicy P) {
@@ -227,8 +249,16 @@ __global__ void __launch_bounds__(kEncWarps * 32) encode_sel_kernel(DevPolicy P)
         if (j >= h) continue;
         em[0][t] = Hs[(size_t)v * h + j];
         double hb = 0.0, ht = 0.0;
-        for (int p = P.bp_ptr[v]; p < P.bp_ptr[v + 1]; ++p) hb += Hs[(size_t)P.bp_idx[p] * h + j];
-        for (int p = P.tp_ptr[v]; p < P.tp_ptr[v + 1]; ++p) ht += Hs[(size_t)P.tp_idx[p] * h + j];
+        if (P.forest) {
+            const int rr = P.jump_rounds;
+            hb = rr == 0 ? em[0][t] : P.PS[0][(rr - 1) & 1][(size_t)v * h + j];
+            ht = rr == 0 ? em[0][t] : P.PS[1][(rr - 1) & 1][(size_t)v * h + j];
+        } else {
+            for (int p = P.bp_ptr[v]; p < P.bp_ptr[v + 1]; ++p)
+                hb += Hs[(size_t)P.bp_idx[p] * h + j];
+            for (int p = P.tp_ptr[v]; p < P.tp_ptr[v + 1]; ++p)
+                ht += Hs[(size_t)P.tp_idx[p] * h + j];
+        }
         em[1][t] = hb;
         em[2][t] = ht;
         em[3][t] = P.Zs[(size_t)v * h + j];
@@ -284,6 +314,13 @@ int policy_prepare(fp_policy *pol, const double *params, cudaStream_t st) {
             encode_round_kernel<2><<<grid, kEncWarps * 32, 0, st>>>(P, k, k == P.K - 1);
         FP_CUDA_RET(cudaGetLastError());
     }
+    if (P.forest)
+        for (int r = 0; r < P.jump_rounds; ++r) {
+            const int64_t total = (int64_t)P.n * P.h;
+            const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+            path_jump_kernel<<<dim3(blocks, 2), 256, 0, st>>>(P, r);
+            FP_CUDA_RET(cudaGetLastError());
+        }
     const int g2 = (P.n + kEncWarps - 1) / kEncWarps;
     if (P.h <= 32)
         encode_sel_kernel<1><<<g2, kEncWarps * 32, 0, st>>>(P);
@@ -320,7 +357,32 @@ int fp_policy_create(const fp_problem *p, const fp_policy_desc *desc, fp_policy 
         }
     }
     const int M = desc->adj_ptr[n];
-    const int Lb = desc->bpath_ptr[n], Lt = desc->tpath_ptr[n];
+    const bool forest = desc->bpath_ptr == nullptr;
+    if (forest && (!desc->bnext || !desc->tnext)) {
+        set_error("need either path lists or next arrays");
+        return FP_ERR_INVALID;
+    }
+    const int Lb = forest ? 0 : desc->bpath_ptr[n], Lt = forest ? 0 : desc->tpath_ptr[n];
+    int jump_rounds = 0;
+    if (forest) {
+        // longest path (vertices) over both forests -> ceil(log2) jumping rounds
+        int64_t longest = 1;
+        for (const int32_t *nx : {desc->bnext, desc->tnext}) {
+            std::vector<int> len(n, 0), stack;
+            for (int v = 0; v < n; ++v) {
+                int u = v;
+                while (u >= 0 && len[u] == 0) {
+                    stack.push_back(u);
+                    u = nx[u];
+                    if ((int)stack.size() > n) { set_error("next arrays contain a cycle"); return FP_ERR_INVALID; }
+                }
+                int base = u >= 0 ? len[u] : 0;
+                while (!stack.empty()) { len[stack.back()] = ++base; stack.pop_back(); }
+                longest = std::max<int64_t>(longest, len[v]);
+            }
+        }
+        while ((int64_t(1) << jump_rounds) < longest) ++jump_rounds;
+    }
     // inverse path lists: for u, the vertices v whose path contains u
     auto invert = [&](const int32_t *ptr, const int32_t *idx, std::vector<int> &iptr,
                       std::vector<int> &iidx) {
@@ -332,9 +394,11 @@ int fp_policy_create(const fp_problem *p, const fp_policy_desc *desc, fp_policy 
         for (int v = 0; v < n; ++v)
             for (int i = ptr[v]; i < ptr[v + 1]; ++i) iidx[fill[idx[i]]++] = v;
     };
-    std::vector<int> ibp, ibi, itp, iti;
-    invert(desc->bpath_ptr, desc->bpath_idx, ibp, ibi);
-    invert(desc->tpath_ptr, desc->tpath_idx, itp, iti);
+    std::vector<int> ibp(n + 1, 0), ibi, itp(n + 1, 0), iti;
+    if (!forest) {
+        invert(desc->bpath_ptr, desc->bpath_idx, ibp, ibi);
+        invert(desc->tpath_ptr, desc->tpath_idx, itp, iti);
+    }
 
     // arena layout
     std::vector<std::pair<size_t, size_t>> parts;  // (offset, bytes)
@@ -352,6 +416,12 @@ int fp_policy_create(const fp_problem *p, const fp_policy_desc *desc, fp_policy 
            o_tp = take((size_t)(n + 1) * 4), o_ti = take((size_t)Lt * 4),
            o_ibp = take((size_t)(n + 1) * 4), o_ibi = take((size_t)Lb * 4),
            o_itp = take((size_t)(n + 1) * 4), o_iti = take((size_t)Lt * 4);
+    size_t o_nx[2] = {0, 0}, o_PS[2][2] = {{0, 0}, {0, 0}}, o_PJ[2][2] = {{0, 0}, {0, 0}};
+    if (forest)
+        for (int w = 0; w < 2; ++w) {
+            o_nx[w] = take((size_t)n * 4);
+            for (int q = 0; q < 2; ++q) { o_PS[w][q] = take(nh); o_PJ[w][q] = take((size_t)n * 4); }
+        }
     size_t o_H[2][kMaxRounds + 1], o_P[2][kMaxRounds], o_Q[2][kMaxRounds], o_U[2][kMaxRounds],
         o_AG[2][kMaxRounds];
     for (int e = 0; e < n_enc; ++e) {
@@ -393,10 +463,15 @@ int fp_policy_create(const fp_problem *p, const fp_policy_desc *desc, fp_policy 
     up(o_ap, desc->adj_ptr, (size_t)(n + 1) * 4);
     up(o_an, desc->adj_src, (size_t)M * 4);
     up(o_ae, desc->adj_edge, (size_t)M * 8);
-    up(o_bp, desc->bpath_ptr, (size_t)(n + 1) * 4);
-    up(o_bi, desc->bpath_idx, (size_t)Lb * 4);
-    up(o_tp, desc->tpath_ptr, (size_t)(n + 1) * 4);
-    up(o_ti, desc->tpath_idx, (size_t)Lt * 4);
+    if (!forest) {
+        up(o_bp, desc->bpath_ptr, (size_t)(n + 1) * 4);
+        up(o_bi, desc->bpath_idx, (size_t)Lb * 4);
+        up(o_tp, desc->tpath_ptr, (size_t)(n + 1) * 4);
+        up(o_ti, desc->tpath_idx, (size_t)Lt * 4);
+    } else {
+        up(o_nx[0], desc->bnext, (size_t)n * 4);
+        up(o_nx[1], desc->tnext, (size_t)n * 4);
+    }
     up(o_ibp, ibp.data(), (size_t)(n + 1) * 4);
     up(o_ibi, ibi.data(), (size_t)Lb * 4);
     up(o_itp, itp.data(), (size_t)(n + 1) * 4);
@@ -419,6 +494,16 @@ int fp_policy_create(const fp_problem *p, const fp_policy_desc *desc, fp_policy 
     P.tp_ptr = (const int *)(b + o_tp); P.tp_idx = (const int *)(b + o_ti);
     P.ibp_ptr = (const int *)(b + o_ibp); P.ibp_idx = (const int *)(b + o_ibi);
     P.itp_ptr = (const int *)(b + o_itp); P.itp_idx = (const int *)(b + o_iti);
+    P.forest = forest ? 1 : 0;
+    P.jump_rounds = jump_rounds;
+    if (forest)
+        for (int w = 0; w < 2; ++w) {
+            P.nxt[w] = (const int *)(b + o_nx[w]);
+            for (int q = 0; q < 2; ++q) {
+                P.PS[w][q] = (double *)(b + o_PS[w][q]);
+                P.PJ[w][q] = (int *)(b + o_PJ[w][q]);
+            }
+        }
     for (int e = 0; e < n_enc; ++e) {
         P.H[e][0] = (double *)(b + o_H[e][0]);
         for (int k = 0; k < K; ++k) {

@@ -53,6 +53,11 @@ struct DevPolicy {
     const double *adj_e;           // standardized edge cost per message
     const int *bp_ptr, *bp_idx, *tp_ptr, *tp_idx;     // SEL b/t paths
     const int *ibp_ptr, *ibp_idx, *itp_ptr, *itp_idx; // inverse paths (u -> v with u in path(v))
+    // forest form (large graphs): next pointers + pointer-jumping buffers
+    int forest, jump_rounds;
+    const int *nxt[2];             // b_next, t_next
+    double *PS[2][2];              // [b/t][ping-pong] partial path sums, [n][h]
+    int *PJ[2][2];                 // [b/t][ping-pong] jump pointers
     // workspace (per snapshot)
     double *H[2][kMaxRounds + 1];  // layer inputs/outputs; H[e][0] is [n][7]
     double *Pm[2][kMaxRounds];     // H[e][k] @ psi.w rows [0, d)

@@ -36,6 +36,8 @@ struct DevProblem {
 };
 
 void set_error(const std::string &msg);
+// blocks of a persistent launch: occupancy x SMs, capped at blocks_needed
+int persistent_blocks(const void *kern, int threads, int64_t smem, int64_t blocks_needed);
 
 }  // namespace fp
 

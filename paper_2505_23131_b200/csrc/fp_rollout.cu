@@ -60,7 +60,7 @@ struct PlcLog {  // log2(MAXD)
 // ---------------------------------------------------------------------------
 template <bool GRAD>
 __device__ __forceinline__ void sel_chain(const DevProblem &PR, const DevPolicy &PO,
-                                          const fp_rollout_args &A, uint8_t *base,
+                                          const fp_rollout_args &A, uint8_t *base /* nb == sb */,
                                           const EpLayout &L, const double *s_sm, int ep,
                                           bool want_lp, bool want_amax) {
     const int lane = lane_id();
@@ -270,23 +270,277 @@ __device__ __forceinline__ void sel_chain(const DevProblem &PR, const DevPolicy 
 }
 
 // ---------------------------------------------------------------------------
+// SEL warp, wide path (graphs whose state lives in HBM)
+//
+// The compact chain re-compacts the candidate bitset every step (O(n/32)
+// words) -- quadratic at 10k-100k ops.  Here the candidate set is a 32-ary
+// tree over vertex ids whose node j at level l summarises leaves
+// [j*32^l, (j+1)*32^l): m = max SEL logit of its candidates, z = sum of
+// exp(s - m) over them, c = candidate count (t = max t-level for the
+// critical-path teacher).  A warp updates one node per level with one
+// coalesced 32-child load, a REDUX max and a butterfly sum, so insert /
+// remove / sample / argmax are O(log32 n) warp steps.  Sampling descends by
+// the cumulative weight in ascending-id order, i.e. the reference's
+// searchsorted(cumsum(p), u * sum(p), 'right') (policy.py:313-316), and the
+// uniform branch descends by count to the idx-th candidate in ascending
+// order; the entropy (only when requested) is one pass over the candidates.
+// ---------------------------------------------------------------------------
+struct TreeRef {
+    double *tm, *tz, *tt;
+    int *tc;
+    const uint32_t *cand;
+    const double *s, *tlev;
+    const EpLayout *L;
+    int n;
+    bool teacher;
+
+    // child `i` of node j at level l (l == 1: leaf = vertex)
+    __device__ __forceinline__ void child(int l, int j, double &m, double &z, double &t,
+                                          int &c) const {
+        const int ci = (j << 5) + lane_id();
+        if (l == 1) {
+            const bool ok = ci < n && ((cand[j] >> (ci & 31)) & 1u);
+            m = ok ? s[ci] : -INFINITY;
+            z = ok ? 1.0 : 0.0;
+            c = ok ? 1 : 0;
+            t = ok && teacher ? tlev[ci] : -INFINITY;
+        } else {
+            const bool ok = ci < L->tl_cnt[l - 1];
+            const int idx = L->tl_off[l - 1] + ci;
+            m = ok ? tm[idx] : -INFINITY;
+            z = ok ? tz[idx] : 0.0;
+            c = ok ? tc[idx] : 0;
+            t = ok && teacher ? tt[idx] : -INFINITY;
+        }
+    }
+
+    __device__ __forceinline__ void recompute(int l, int j) const {
+        double m, z, t;
+        int c;
+        child(l, j, m, z, t, c);
+        const double M = warp_max_redux(m);
+        const double zz = c > 0 ? z * exp(m - M) : 0.0;
+        const double Z = warp_sum(zz);
+        const int C = __reduce_add_sync(FP_FULL_MASK, c);
+        const double T = teacher ? warp_max_redux(t) : -INFINITY;
+        if (lane_id() == 0) {
+            const int idx = L->tl_off[l] + j;
+            tm[idx] = M; tz[idx] = Z; tc[idx] = C;
+            if (teacher) tt[idx] = T;
+        }
+        __syncwarp();
+    }
+
+    // leaf v changed: refresh its ancestors bottom-up
+    __device__ __forceinline__ void update(int v) const {
+        for (int l = 1; l <= L->tl_n; ++l) recompute(l, v >> (5 * l));
+    }
+
+    __device__ __forceinline__ int root() const { return L->tl_off[L->tl_n]; }
+
+    // first leaf whose inclusive cumulative weight exceeds target (root units)
+    __device__ __forceinline__ int descend_weight(double target) const {
+        int j = 0;
+        double Mn = tm[root()];
+        for (int l = L->tl_n; l >= 1; --l) {
+            double m, z, t;
+            int c;
+            child(l, j, m, z, t, c);
+            const double w = c > 0 ? z * exp(m - Mn) : 0.0;
+            const double cum = warp_inclusive_scan(w);
+            const unsigned nonempty = __ballot_sync(FP_FULL_MASK, c > 0);
+            const unsigned hit = __ballot_sync(FP_FULL_MASK, c > 0 && cum > target);
+            const int sel = hit ? __ffs(hit) - 1 : 31 - __clz(nonempty);
+            const double prev = __shfl_sync(FP_FULL_MASK, cum - w, sel);
+            const double ms = __shfl_sync(FP_FULL_MASK, m, sel);
+            target = (target - prev) * exp(Mn - ms);
+            Mn = ms;
+            j = (j << 5) + sel;
+        }
+        return j;
+    }
+
+    // the idx-th candidate (0-based) in ascending id order
+    __device__ __forceinline__ int descend_count(int idx) const {
+        int j = 0;
+        for (int l = L->tl_n; l >= 1; --l) {
+            double m, z, t;
+            int c;
+            child(l, j, m, z, t, c);
+            const int cum = warp_inclusive_scan(c);
+            const unsigned hit = __ballot_sync(FP_FULL_MASK, cum > idx);
+            const int sel = __ffs(hit) - 1;
+            idx -= __shfl_sync(FP_FULL_MASK, cum - c, sel);
+            j = (j << 5) + sel;
+        }
+        return j;
+    }
+
+    // first candidate attaining the maximum logit (key 0) or t-level (key 1)
+    __device__ __forceinline__ int descend_max(bool by_tlev) const {
+        int j = 0;
+        const double best = by_tlev ? tt[root()] : tm[root()];
+        for (int l = L->tl_n; l >= 1; --l) {
+            double m, z, t;
+            int c;
+            child(l, j, m, z, t, c);
+            const double key = by_tlev ? t : m;
+            const int sel = __ffs(__ballot_sync(FP_FULL_MASK, c > 0 && key == best)) - 1;
+            j = (j << 5) + sel;
+        }
+        return j;
+    }
+};
+
+__device__ __forceinline__ bool ring_publish(volatile int *ring, volatile int *dead, int step,
+                                             int v) {
+    int ok = 1;
+    if (lane_id() == 0) {
+        const int slot = step & (kRing - 1);
+        while (ring[slot] != -3) {
+            if (*dead) { ok = 0; break; }
+        }
+        if (ok) ring[slot] = v;
+    }
+    return __shfl_sync(FP_FULL_MASK, ok, 0) != 0;
+}
+
+__device__ __forceinline__ void sel_chain_wide(const DevProblem &PR, const DevPolicy &PO,
+                                               const fp_rollout_args &A, uint8_t *nb,
+                                               uint8_t *sb, const EpLayout &L, int ep,
+                                               bool want_lp, bool want_amax) {
+    const int lane = lane_id();
+    const int n = PR.n, W = PR.W;
+    uint32_t *cand = (uint32_t *)(nb + L.cand);
+    int *npl = (int *)(nb + L.npl);
+    volatile int *ring = (volatile int *)(sb + L.ring);
+    volatile int *dead = (volatile int *)(sb + L.flag);
+    const double eps = A.epsilon, ome = 1.0 - eps;
+    const uint32_t k0 = (uint32_t)A.seed, k1 = (uint32_t)(A.seed >> 32);
+    const uint32_t ctr_ep = A.episode_base + (uint32_t)ep;
+    const int mode = A.mode;
+    const int32_t *frow = mode == FP_MODE_FORCED ? A.forced + (size_t)ep * n * 2 : nullptr;
+    const int *__restrict__ pp = PR.pred_ptr;
+    const int *__restrict__ sp = PR.succ_ptr;
+    const int *__restrict__ si = PR.succ_idx;
+    const double *__restrict__ s = PO.s;
+    TreeRef T{(double *)(nb + L.tm), (double *)(nb + L.tz), (double *)(nb + L.tt),
+              (int *)(nb + L.tc), cand, s, PR.tlev, &L, n, mode == FP_MODE_TEACHER};
+
+    for (int w = lane; w < W; w += 32) cand[w] = 0u;
+    __syncwarp();
+    for (int v = lane; v < n; v += 32) {
+        const int np = pp[v + 1] - pp[v];
+        npl[v] = np;
+        if (np == 0) atomicOr(&cand[v >> 5], 1u << (v & 31));
+    }
+    __syncwarp();
+    for (int l = 1; l <= L.tl_n; ++l)
+        for (int j = 0; j < L.tl_cnt[l]; ++j) T.recompute(l, j);
+
+    const int rt = T.root();
+    for (int step = 0; step < n; ++step) {
+        const int k = T.tc[rt];
+        if (k == 0) {  // cyclic graph: nothing is ever ready
+            ring_publish(ring, dead, step, -1);
+            return;
+        }
+        const double Mr = T.tm[rt], Zr = T.tz[rt];
+        int v = -1;
+        if (mode == FP_MODE_FORCED) {
+            const int fv = frow[2 * step];
+            if (fv >= 0 && fv < n && ((cand[fv >> 5] >> (fv & 31)) & 1u)) v = fv;
+        } else if (mode == FP_MODE_TEACHER) {
+            v = T.descend_max(true);
+        } else if (mode == FP_MODE_SAMPLE) {
+            double u1, u2;
+            uniform2(philox4x32_10(U4{ctr_ep, (uint32_t)step, 0u, 0u}, k0, k1), u1, u2);
+            v = u1 < eps ? T.descend_count(min((int)(u2 * (double)k), k - 1))
+                         : T.descend_weight(u2 * Zr);
+        }
+        int amax = -1;
+        if (want_amax || mode == FP_MODE_GREEDY) {
+            amax = T.descend_max(false);
+            if (mode == FP_MODE_GREEDY) v = amax;
+        }
+        if (v < 0) {  // forced vertex is not a candidate
+            ring_publish(ring, dead, step, -2);
+            return;
+        }
+        if (!ring_publish(ring, dead, step, v)) return;
+        if (want_lp) {
+            const double ek = eps / (double)k;
+            const double p = exp(s[v] - Mr) / Zr;
+            const double mix = __dadd_rn(__dmul_rn(p, ome), ek);
+            const double lp = log(__dadd_rn(mix, 1e-30));
+            double entp = 0.0;
+            for (int w = lane; w < W; w += 32) {
+                uint32_t m = cand[w];
+                while (m) {
+                    const int u = (w << 5) + __ffs(m) - 1;
+                    m &= m - 1;
+                    const double pu = exp(s[u] - Mr) / Zr;
+                    const double mu = __dadd_rn(__dmul_rn(pu, ome), ek);
+                    entp += mu * log(__dadd_rn(mu, 1e-30));
+                }
+            }
+            const double ent = -warp_sum(entp);
+            if (lane == 0) {
+                const size_t o = (size_t)ep * n + step;
+                if (A.step_lp) A.step_lp[2 * o] = lp;
+                if (A.step_ent) A.step_ent[2 * o] = ent;
+            }
+        }
+        if (lane == 0) {
+            const size_t o = (size_t)ep * n + step;
+            if (A.step_vd) A.step_vd[2 * o] = v;
+            if (A.step_argmax) A.step_argmax[2 * o] = amax;
+            if (A.step_ncand) A.step_ncand[o] = k;
+            atomicAnd(&cand[v >> 5], ~(1u << (v & 31)));
+        }
+        __syncwarp();
+        T.update(v);
+        // successors whose last predecessor was just placed become candidates
+        for (int j0 = sp[v]; j0 < sp[v + 1]; j0 += 32) {
+            const int j = j0 + lane;
+            int w = -1;
+            if (j < sp[v + 1]) {
+                w = si[j];
+                if (--npl[w] == 0) atomicOr(&cand[w >> 5], 1u << (w & 31));
+                else w = -1;
+            }
+            __syncwarp();
+            unsigned ready = __ballot_sync(FP_FULL_MASK, w >= 0);
+            while (ready) {
+                const int src = __ffs(ready) - 1;
+                ready &= ready - 1;
+                T.update(__shfl_sync(FP_FULL_MASK, w, src));
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // PLC warp
 // ---------------------------------------------------------------------------
-template <int MAXD, int HPL, bool GRAD>
+template <int MAXD, int HPL, bool GRAD, bool WIDE = false>
 __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &PO,
-                                         const fp_rollout_args &A, uint8_t *base,
+                                         const fp_rollout_args &A, uint8_t *nb, uint8_t *sb,
                                          const EpLayout &L, int ep, bool want_lp,
                                          bool want_amax) {
+    static_assert(!(WIDE && GRAD), "REINFORCE rows are produced by the compact path only");
     const int lane = lane_id();
     const int n = PR.n, D = PR.d, h = PO.h;
     constexpr int LOGD = PlcLog<MAXD>::v;
-    double *tstart = (double *)(base + L.tstart);
-    double *tend = (double *)(base + L.tend);
-    double *xd = (double *)(base + L.xd);
-    double *xn = (double *)(base + L.xn);
-    double *stats = (double *)(base + L.stats);
-    const volatile int *order = (const volatile int *)(base + L.order);
-    uint8_t *dev = base + L.assign;
+    double *tstart = (double *)(nb + L.tstart);
+    double *tend = (double *)(nb + L.tend);
+    double *xd = (double *)(sb + L.xd);
+    double *xn = (double *)(sb + L.xn);
+    double *stats = (double *)(sb + L.stats);
+    const volatile int *order = (const volatile int *)(nb + L.order);
+    volatile int *ring = (volatile int *)(sb + L.ring);
+    volatile int *dead = (volatile int *)(sb + L.flag);
+    uint8_t *dev = nb + L.assign;
     const double eps = A.epsilon, ome = 1.0 - eps, slope = PO.slope;
     const uint32_t k0 = (uint32_t)A.seed, k1 = (uint32_t)(A.seed >> 32);
     const uint32_t ctr_ep = A.episode_base + (uint32_t)ep;
@@ -301,7 +555,7 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
     const double *__restrict__ tdur = PR.tdur;
     const double *__restrict__ edur = PR.edur;
     const double b2p = PO.W(PR_PLC_H2_B)[0];
-    double *rsl = (double *)(base + L.rsum);  // [D][h] running lp sums (grad)
+    double *rsl = (double *)(sb + L.rsum);    // [D][h] running lp sums (grad)
     double *rse = rsl + D * h;                // [D][h] running entropy sums
 
     for (int v = lane; v < n; v += 32) { tstart[v] = 0.0; tend[v] = 0.0; dev[v] = 0xFF; }
@@ -336,7 +590,16 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
     FP_PHASE_BEGIN(pp_);
     for (int step = 0; step < n; ++step) {
         int v;
-        while ((v = order[step]) == -3) { }
+        if constexpr (WIDE) {
+            // single-producer / single-consumer ring: the SEL warp refills a
+            // slot only after this warp hands it back (-3)
+            const int slot = step & (kRing - 1);
+            while ((v = ring[slot]) == -3) { }
+            __syncwarp();
+            if (lane == 0) ring[slot] = -3;
+        } else {
+            while ((v = order[step]) == -3) { }
+        }
         if (v < 0) { status = v == -1 ? FP_EP_DEADLOCK : FP_EP_BAD_ACTION; break; }
         FP_PHASE_END(pp_, 10);
         double Av[HPL], Gv[HPL];
@@ -467,7 +730,11 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
         int jdx;
         if (mode == FP_MODE_FORCED) {
             jdx = frow[2 * step + 1];
-            if (jdx < 0 || jdx >= D) { status = FP_EP_BAD_ACTION; break; }
+            if (jdx < 0 || jdx >= D) {
+                status = FP_EP_BAD_ACTION;
+                if (WIDE && lane == 0) *dead = 1;  // release a producer blocked on the ring
+                break;
+            }
         } else if (mode == FP_MODE_TEACHER) {
             // argmin earliest start, first device on ties (heuristics.py:85-91)
             const double tv = lane < D ? f4 : INFINITY;
@@ -619,13 +886,13 @@ rollout_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
         sel_chain<GRAD>(PR, PO, A, base, L, s_sm, ep, want_lp, want_amax);
         return;
     }
-    int status = plc_chain<MAXD, HPL, GRAD>(PR, PO, A, base, L, ep, want_lp, want_amax);
+    int status = plc_chain<MAXD, HPL, GRAD>(PR, PO, A, base, base, L, ep, want_lp, want_amax);
     const uint8_t *dev = base + L.assign;
     for (int v = lane; v < n; v += 32) A.assign[(size_t)ep * n + v] = dev[v] == 0xFF ? -1 : dev[v];
     double mk = 0.0;
     if (status == FP_EP_OK && A.simulate) {
         __syncwarp();
-        SimOut o = sim_episode<RPL>(PR, base, L, A.strategy, nullptr,
+        SimOut o = sim_episode<RPL>(PR, base, base, L, A.strategy, nullptr,
                                     A.trace ? A.trace + (size_t)ep * A.trace_cap : nullptr,
                                     A.trace_cap, nullptr);
         status = o.status;
@@ -661,11 +928,120 @@ static int launch_rollout(const fp_problem *p, const fp_policy *pol, const fp_ro
     return FP_OK;
 }
 
+// Wide path: persistent grid, one SEL + one PLC warp per resident episode,
+// n-sized state in the HBM workspace slice of this block, small scratch and
+// the hand-off ring in shared memory.  After the PLC chain the same warp
+// scores the assignment with the hierarchical-bitset simulator.
+template <int MAXD, int HPL>
+__global__ void __launch_bounds__(64, 8)
+rollout_wide_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    constexpr int RPL = (MAXD + MAXD * MAXD + 31) / 32;
+    const int lane = lane_id();
+    const bool is_plc = (threadIdx.x >> 5) & 1;
+    const int n = PR.n;
+    uint8_t *sb = smem;
+    uint8_t *nb = (uint8_t *)A.workspace + (size_t)blockIdx.x * L.gbytes;
+    const bool want_lp = A.step_lp != nullptr || A.step_ent != nullptr;
+    const bool want_amax = A.step_argmax != nullptr;
+    for (int ep = blockIdx.x; ep < A.B; ep += gridDim.x) {
+        if (!is_plc) {
+            volatile int *ring = (volatile int *)(sb + L.ring);
+            for (int t = lane; t < kRing; t += 32) ring[t] = -3;
+            if (lane == 0) *(volatile int *)(sb + L.flag) = 0;
+        }
+        __syncthreads();
+        if (!is_plc) {
+            sel_chain_wide(PR, PO, A, nb, sb, L, ep, want_lp, want_amax);
+        } else {
+            int status = plc_chain<MAXD, HPL, false, true>(PR, PO, A, nb, sb, L, ep, want_lp,
+                                                           want_amax);
+            const uint8_t *dev = nb + L.assign;
+            for (int v = lane; v < n; v += 32)
+                A.assign[(size_t)ep * n + v] = dev[v] == 0xFF ? -1 : dev[v];
+            double mk = 0.0;
+            if (status == FP_EP_OK && A.simulate) {
+                __syncwarp();
+                SimOut o = sim_episode<RPL, true>(
+                    PR, nb, sb, L, A.strategy, nullptr,
+                    A.trace ? A.trace + (size_t)ep * A.trace_cap : nullptr, A.trace_cap, nullptr);
+                status = o.status;
+                mk = o.makespan;
+                if (lane == 0 && A.trace_len) A.trace_len[ep] = o.n_events;
+            }
+            if (lane == 0) {
+                if (A.makespan) A.makespan[ep] = mk;
+                A.status[ep] = status;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+template <int MAXD, int HPL>
+static int launch_rollout_wide(const fp_problem *p, const fp_policy *pol,
+                               const fp_rollout_args &a, int64_t *ws_needed, cudaStream_t st) {
+    const DevProblem &PR = p->dev;
+    const EpLayout L = make_layout(PR.n, PR.W, PR.R, PR.SM, true, 0, true);
+    const int64_t smem = L.bytes;
+    if (smem > 227 * 1024) {
+        set_error("episode scratch exceeds shared memory (too many devices / slots)");
+        return FP_ERR_UNSUPPORTED;
+    }
+    auto kern = rollout_wide_kernel<MAXD, HPL>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FP_ERR_CUDA; }
+    const int grid = persistent_blocks((const void *)kern, 64, smem, a.B);
+    const int64_t need = (int64_t)grid * L.gbytes;
+    if (ws_needed) { *ws_needed = need; return FP_OK; }
+    if (!a.workspace || a.workspace_bytes < need) {
+        set_error("workspace too small for the wide rollout (see fp_rollout_workspace_size)");
+        return FP_ERR_INVALID;
+    }
+    kern<<<grid, 64, smem, st>>>(PR, pol->dev, a, L);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FP_ERR_CUDA; }
+    return FP_OK;
+}
+
+static bool rollout_compact_fits(const fp_problem *p, const fp_policy *pol, bool grad) {
+    const DevProblem &PR = p->dev;
+    const EpLayout L = make_layout(PR.n, PR.W, PR.R, PR.SM, true,
+                                   grad ? 2 * PR.d * pol->dev.h : 0);
+    // the compact SEL chain keeps the candidate bitset in one word per lane
+    return PR.n <= 1024 && fp_align(8 * PR.n, 16) + (int64_t)L.bytes <= 227 * 1024;
+}
+
 template <int MAXD, int HPL>
 static int dispatch_grad(const fp_problem *p, const fp_policy *pol, const fp_rollout_args &a,
-                         cudaStream_t st) {
-    return a.grad_rows ? launch_rollout<MAXD, HPL, true>(p, pol, a, st)
-                       : launch_rollout<MAXD, HPL, false>(p, pol, a, st);
+                         int64_t *ws_needed, cudaStream_t st) {
+    const bool grad = a.grad_rows != nullptr;
+    const bool wide = (a.flags & FP_FLAG_WIDE) || !rollout_compact_fits(p, pol, grad);
+    if (wide) {
+        if (grad) {
+            set_error("REINFORCE rows need the compact (shared-memory) rollout: graph too large");
+            return FP_ERR_UNSUPPORTED;
+        }
+        return launch_rollout_wide<MAXD, HPL>(p, pol, a, ws_needed, st);
+    }
+    if (ws_needed) { *ws_needed = 0; return FP_OK; }
+    return grad ? launch_rollout<MAXD, HPL, true>(p, pol, a, st)
+                : launch_rollout<MAXD, HPL, false>(p, pol, a, st);
+}
+
+static int dispatch(const fp_problem *p, const fp_policy *pol, const fp_rollout_args &a,
+                    int64_t *ws_needed, cudaStream_t st) {
+    const int D = p->dev.d, h = pol->dev.h;
+    if (h <= 32) {
+        if (D <= 4) return dispatch_grad<4, 1>(p, pol, a, ws_needed, st);
+        if (D <= 8) return dispatch_grad<8, 1>(p, pol, a, ws_needed, st);
+        if (D <= 16) return dispatch_grad<16, 1>(p, pol, a, ws_needed, st);
+        return dispatch_grad<32, 1>(p, pol, a, ws_needed, st);
+    }
+    if (D <= 8) return dispatch_grad<8, 2>(p, pol, a, ws_needed, st);
+    if (D <= 16) return dispatch_grad<16, 2>(p, pol, a, ws_needed, st);
+    return dispatch_grad<32, 2>(p, pol, a, ws_needed, st);
 }
 
 }  // namespace fp
@@ -693,6 +1069,18 @@ int fp_grad_ep_stride(const fp_policy *pol, int32_t d, int64_t *stride) {
     return FP_OK;
 }
 
+int fp_rollout_workspace_size(const fp_problem *p, const fp_policy *pol, int32_t B,
+                              int32_t flags, int32_t grad, int64_t *bytes) {
+    if (!p || !pol || !bytes) { set_error("null argument"); return FP_ERR_INVALID; }
+    *bytes = 0;
+    if (B <= 0) return FP_OK;
+    fp_rollout_args a{};
+    a.B = B;
+    a.flags = flags;
+    a.grad_rows = grad ? (double *)1 : nullptr;  // only tested for non-null
+    return dispatch(p, pol, a, bytes, 0);
+}
+
 int fp_rollout_batch(const fp_problem *p, const fp_policy *pol, const fp_rollout_args *args,
                      void *stream) {
     if (!p || !pol || !args || !args->assign || !args->status) {
@@ -701,22 +1089,11 @@ int fp_rollout_batch(const fp_problem *p, const fp_policy *pol, const fp_rollout
     }
     const fp_rollout_args &a = *args;
     if (a.B <= 0) return FP_OK;
-    if (p->dev.n > 1024) { set_error("rollout kernel supports n <= 1024"); return FP_ERR_UNSUPPORTED; }
     if (a.mode == FP_MODE_FORCED && !a.forced) { set_error("FORCED mode needs actions"); return FP_ERR_INVALID; }
     if (a.mode < 0 || a.mode > 3) { set_error("unknown mode"); return FP_ERR_INVALID; }
     if (a.grad_rows && !a.grad_ep) { set_error("grad_rows needs grad_ep"); return FP_ERR_INVALID; }
     if (a.simulate && !a.makespan) { set_error("simulate needs makespan"); return FP_ERR_INVALID; }
-    cudaStream_t st = (cudaStream_t)stream;
-    const int D = p->dev.d, h = pol->dev.h;
-    if (h <= 32) {
-        if (D <= 4) return dispatch_grad<4, 1>(p, pol, a, st);
-        if (D <= 8) return dispatch_grad<8, 1>(p, pol, a, st);
-        if (D <= 16) return dispatch_grad<16, 1>(p, pol, a, st);
-        return dispatch_grad<32, 1>(p, pol, a, st);
-    }
-    if (D <= 8) return dispatch_grad<8, 2>(p, pol, a, st);
-    if (D <= 16) return dispatch_grad<16, 2>(p, pol, a, st);
-    return dispatch_grad<32, 2>(p, pol, a, st);
+    return dispatch(p, pol, a, nullptr, (cudaStream_t)stream);
 }
 
 }  // extern "C"

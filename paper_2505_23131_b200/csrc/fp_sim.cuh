@@ -43,29 +43,68 @@ struct SimOut {
     int n_events;
 };
 
-// base: this episode's shared-memory slice; L.assign must hold the
-// assignment (made visible with __syncwarp).  All 32 lanes must call.
-template <int RPL>
-__device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *base,
+// Pending set of one resource: bit `pos` = the task whose vertex sits at
+// position pos of the strategy order.  Compact path: one flat bitset scanned
+// from word 0 (n <= ~1k).  Wide path (HIER): three levels -- L0 words, an L1
+// word per 32 L0 words, an L2 word per 32 L1 words -- so pushes and pops
+// are O(1) words plus an L2 scan of n/32768 words.  Pushes happen only in
+// the completion phase (any lane, atomicOr), pops only in the start phase by
+// the lane owning the resource, so the two never race.
+template <bool HIER>
+__device__ __forceinline__ void pend_push(uint32_t *b, const EpLayout &L, int pos) {
+    const int w = pos >> 5;
+    atomicOr(&b[w], 1u << (pos & 31));
+    if constexpr (HIER) {
+        atomicOr(&b[L.W + (w >> 5)], 1u << (w & 31));
+        atomicOr(&b[L.W + L.W1 + (w >> 10)], 1u << ((w >> 5) & 31));
+    }
+}
+
+template <bool HIER>
+__device__ __forceinline__ int pend_pop_hier(uint32_t *b, const EpLayout &L) {
+    uint32_t *b1 = b + L.W, *b2 = b1 + L.W1;
+    int w2 = 0;
+    uint32_t x2;
+    while ((x2 = b2[w2]) == 0u) ++w2;
+    const int w1 = (w2 << 5) + __ffs(x2) - 1;
+    uint32_t x1 = b1[w1];
+    const int w = (w1 << 5) + __ffs(x1) - 1;
+    uint32_t x = b[w];
+    const int bit = __ffs(x) - 1;
+    x &= ~(1u << bit);
+    b[w] = x;
+    if (x == 0u) {
+        x1 &= ~(1u << (w & 31));
+        b1[w1] = x1;
+        if (x1 == 0u) b2[w2] = x2 & ~(1u << (w1 & 31));
+    }
+    return (w << 5) + bit;
+}
+
+// nb: this episode's n-sized state (shared memory, or its HBM workspace slice
+// on the wide path); sb: its small shared-memory scratch.  nb + L.assign must
+// hold the assignment (made visible with __syncwarp).  All 32 lanes must call.
+template <int RPL, bool HIER = false>
+__device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *nb, uint8_t *sb,
                                               const EpLayout &L, int strategy,
                                               const double *__restrict__ jit,
                                               fp_event *__restrict__ trace, int trace_cap,
                                               uint8_t *__restrict__ blocked) {
     const int lane = lane_id();
-    const int n = P.n, d = P.d, W = P.W, R = P.R, SM = P.SM;
-    uint32_t *rdy = (uint32_t *)(base + L.rdy);
-    int *missing = (int *)(base + L.missing);
-    uint32_t *cons = (uint32_t *)(base + L.cons);
-    const uint8_t *assign = base + L.assign;
-    uint32_t *bits = (uint32_t *)(base + L.bits);
-    int *cnt = (int *)(base + L.cnt);
-    double *pend = (double *)(base + L.pend);
-    int *pv = (int *)(base + L.pv);
-    int *pseq = (int *)(base + L.pseq);
-    uint64_t *skey = (uint64_t *)(base + L.skey);
-    int *sidx = (int *)(base + L.sidx);
-    int *elist = (int *)(base + L.elist);
-    int *ctr = (int *)(base + L.ctr);
+    const int n = P.n, d = P.d, R = P.R, SM = P.SM, BW = L.BW;
+    uint32_t *rdy = (uint32_t *)(nb + L.rdy);
+    int *missing = (int *)(nb + L.missing);
+    uint32_t *cons = (uint32_t *)(nb + L.cons);
+    const uint8_t *assign = nb + L.assign;
+    uint32_t *bits = (uint32_t *)(nb + L.bits);
+    int *cnt = (int *)(sb + L.cnt);
+    double *pend = (double *)(sb + L.pend);
+    int *pv = (int *)(sb + L.pv);
+    int *pseq = (int *)(sb + L.pseq);
+    uint64_t *skey = (uint64_t *)(sb + L.skey);
+    int *sidx = (int *)(sb + L.sidx);
+    int *elist = (int *)(sb + L.elist);
+    int *ctr = (int *)(sb + L.ctr);
     const uint32_t dmask = d >= 32 ? 0xffffffffu : ((1u << d) - 1u);
     const int *__restrict__ rpos = P.rank_pos + strategy * n;
     const int *__restrict__ rvert = P.rank_vert + strategy * n;
@@ -87,7 +126,7 @@ __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *base
         for (int j = P.pred_ptr[v]; j < P.pred_ptr[v + 1]; ++j) miss += !ent[P.pred_idx[j]];
         missing[v] = miss;
     }
-    for (int i = lane; i < R * W; i += 32) bits[i] = 0u;
+    for (int i = lane; i < R * BW; i += 32) bits[i] = 0u;
     int fr[RPL];
 #pragma unroll
     for (int q = 0; q < RPL; ++q) {
@@ -101,8 +140,7 @@ __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *base
     __syncwarp();
     for (int v = lane; v < n; v += 32)
         if (!ent[v] && missing[v] == 0) {
-            const int pos = rpos[v];
-            atomicOr(&bits[assign[v] * W + (pos >> 5)], 1u << (pos & 31));
+            pend_push<HIER>(bits + assign[v] * BW, L, rpos[v]);
             atomicAdd(&cnt[assign[v]], 1);
         }
     __syncwarp();
@@ -127,16 +165,22 @@ __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *base
             if (r >= R) continue;
             int c = cnt[r];
             if (fr[q] > 0 && c > 0) {
-                uint32_t *wb = bits + r * W;
+                uint32_t *wb = bits + r * BW;
                 int w = 0;
                 int slot = r * SM;
                 int f = fr[q];
                 while (f > 0 && c > 0) {
-                    uint32_t word = wb[w];
-                    while (word == 0u) word = wb[++w];
-                    const int b = __ffs(word) - 1;
-                    wb[w] = word & ~(1u << b);
-                    const int v = rvert[(w << 5) + b];
+                    int pos;
+                    if constexpr (HIER) {
+                        pos = pend_pop_hier<HIER>(wb, L);
+                    } else {
+                        uint32_t word = wb[w];
+                        while (word == 0u) word = wb[++w];
+                        const int b = __ffs(word) - 1;
+                        wb[w] = word & ~(1u << b);
+                        pos = (w << 5) + b;
+                    }
+                    const int v = rvert[pos];
                     double dur;
                     int kind, tb;
                     if (r < d) {
@@ -234,7 +278,7 @@ __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *base
                         const int dst = __ffs(m) - 1;
                         m &= m - 1;
                         const int rr = d + r * d + dst;
-                        atomicOr(&bits[rr * W + (pos >> 5)], 1u << (pos & 31));
+                        pend_push<HIER>(bits + rr * BW, L, pos);
                         atomicAdd(&cnt[rr], 1);
                     }
                 } else {
@@ -244,8 +288,7 @@ __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *base
                 for (int j = sp[v]; j < sp[v + 1]; ++j) {
                     const int w = si[j];
                     if (assign[w] == dev && atomicSub(&missing[w], 1) == 1) {
-                        const int pos = rpos[w];
-                        atomicOr(&bits[dev * W + (pos >> 5)], 1u << (pos & 31));
+                        pend_push<HIER>(bits + dev * BW, L, rpos[w]);
                         atomicAdd(&cnt[dev], 1);
                     }
                 }

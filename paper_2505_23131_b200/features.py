@@ -23,9 +23,16 @@ COMPUTE_COST, IN_COMM_SUM, OUT_COMM_SUM, T_LEVEL, B_LEVEL = range(5)
 
 @dataclass
 class StaticGraphFeatures:
+    """``b_next[v]`` / ``t_next[v]`` are the argmax neighbours of the two
+    longest-path sweeps (-1 at a path's end): the paths form two forests, and
+    ``b_paths[v]`` = (v, b_next[v], b_next[b_next[v]], ...).  The explicit
+    path tuples (reference ``features.py:88-95``) are materialised on first
+    use only -- their total length grows like n * depth (2.7e8 entries at
+    100k ops), so large graphs are handed to the GPU as the next arrays."""
+
     matrix: np.ndarray
-    b_paths: tuple[tuple[int, ...], ...]
-    t_paths: tuple[tuple[int, ...], ...]
+    b_next: np.ndarray
+    t_next: np.ndarray
     comm_factor: float
 
     @property
@@ -35,6 +42,33 @@ class StaticGraphFeatures:
     @property
     def b_level(self) -> np.ndarray:
         return self.matrix[:, B_LEVEL]
+
+    @property
+    def b_paths(self) -> tuple[tuple[int, ...], ...]:
+        if getattr(self, "_b_paths", None) is None:
+            nxt = self.b_next.tolist()
+            self._b_paths = tuple(_walk(v, nxt) for v in range(len(nxt)))
+        return self._b_paths
+
+    @property
+    def t_paths(self) -> tuple[tuple[int, ...], ...]:
+        if getattr(self, "_t_paths", None) is None:
+            nxt = self.t_next.tolist()
+            self._t_paths = tuple(_walk(v, nxt) for v in range(len(nxt)))
+        return self._t_paths
+
+    def path_lengths(self, which: str) -> np.ndarray:
+        """Length of every b- or t-path, from the next forest (O(n))."""
+        nxt = self.b_next if which == "b" else self.t_next
+        n = len(nxt)
+        out = np.zeros(n, dtype=np.int64)
+        # a path's successor is a predecessor (b) / successor (t) in the DAG,
+        # so one sweep in the order the levels were computed fills it
+        order = self._order_b if which == "b" else self._order_t
+        for v in order:
+            w = nxt[v]
+            out[v] = 1 + (out[w] if w >= 0 else 0)
+        return out
 
 
 def edge_comm_cost(graph: DataflowGraph, u: int, comm_factor: float) -> float:
@@ -75,5 +109,8 @@ def static_features(graph: DataflowGraph,
         mat[v, OUT_COMM_SUM] = cc[v] * len(graph.succs(v))
     t_next = _longest(graph, reversed(order), graph.succs, lambda v, w: cc[v], mat, T_LEVEL)
     b_next = _longest(graph, order, graph.preds, lambda v, u: cc[u], mat, B_LEVEL)
-    return StaticGraphFeatures(mat, tuple(_walk(v, b_next) for v in range(n)),
-                               tuple(_walk(v, t_next) for v in range(n)), comm_factor)
+    f = StaticGraphFeatures(mat, np.asarray(b_next, dtype=np.int32),
+                            np.asarray(t_next, dtype=np.int32), comm_factor)
+    f._order_b = list(order)
+    f._order_t = list(reversed(order))
+    return f

@@ -188,11 +188,18 @@ def _candidate_sets(graph: DataflowGraph, order) -> list[tuple[int, ...]]:
     return out
 
 
+# Graphs above this size hand the SEL paths to the GPU as next-pointer
+# forests (path sums by pointer jumping) instead of explicit lists, whose
+# total length grows like n * depth.  Matches the compact rollout's limit:
+# REINFORCE rows (and so the backward, which needs the lists) stop there.
+FOREST_MIN_N = 1024
+
+
 class PolicyContext:
     """Per-graph rollout machinery on the GPU (reference policy.py:281-402)."""
 
     def __init__(self, graph: DataflowGraph, cluster: ClusterSpec, config: PolicyConfig,
-                 features: StaticGraphFeatures | None = None):
+                 features: StaticGraphFeatures | None = None, forest: bool | None = None):
         if config.mp_mode != "per_episode":
             raise NotImplementedError("mp_mode='per_step' is not implemented by the CUDA rollout")
         self.graph = graph
@@ -204,6 +211,7 @@ class PolicyContext:
         self.encode_count = 0
         self.sim = SimProblem(graph, cluster, self.features)
         self.layout = FlatLayout.for_config(config)
+        self.forest = len(graph) > FOREST_MIN_N if forest is None else bool(forest)
         self._make_native()
         self._flat = None          # device flat params of the current snapshot
         self._prepared_key = None
@@ -219,13 +227,19 @@ class PolicyContext:
         for name, role in N.ROLE_BY_HEAD.items():
             offs[role] = self.layout.offset(name)
         ptr, src, edge = self.enc.csr_into()
-        bp, bi, tp, ti = self.enc.paths_csr()
+        # explicit path lists for graphs the compact kernels (and the REINFORCE
+        # backward) handle; the next-pointer forests beyond that
+        bnext = np.ascontiguousarray(self.features.b_next, dtype=np.int32)
+        tnext = np.ascontiguousarray(self.features.t_next, dtype=np.int32)
+        bp = bi = tp = ti = None
+        if not self.forest:
+            bp, bi, tp, ti = self.enc.paths_csr()
         x = np.ascontiguousarray(self.enc.x_static, dtype=np.float64)
-        self._host_keep = (offs, ptr, src, edge, bp, bi, tp, ti, x)
+        self._host_keep = (offs, ptr, src, edge, bp, bi, tp, ti, x, bnext, tnext)
         desc = N.FpPolicyDesc(self.config.hidden, self.config.k_rounds,
                               int(self.config.shared_encoder), float(self.config.leaky_slope),
                               *[N.ptr(a).value for a in (x, ptr, src, edge, bp, bi, tp, ti, offs)],
-                              self.layout.size)
+                              self.layout.size, N.ptr(bnext).value, N.ptr(tnext).value)
         h = ctypes.c_void_p()
         N.check(N.lib().fp_policy_create(self.sim.handle, ctypes.byref(desc), ctypes.byref(h)))
         self.handle = h
@@ -274,7 +288,8 @@ class PolicyContext:
                       mode: str = "sample", forced=None, simulate: bool = True,
                       strategy: str = "fifo", trace_steps: bool = False, grad: bool = False,
                       sim_trace: bool = False, episode_base: int = 0, prepare: bool = True,
-                      stream=None, out: RolloutBatch | None = None) -> RolloutBatch:
+                      stream=None, out: RolloutBatch | None = None,
+                      wide: bool = False) -> RolloutBatch:
         import torch
 
         if mode not in N.MODE:
@@ -300,11 +315,32 @@ class PolicyContext:
                                        out.step_argmax, out.step_ncand, out.makespan,
                                        out.status, out.grad_rows, out.grad_ep, out.trace)],
             out.trace.shape[1] // 16 if out.trace is not None else 0,
-            N.ptr(out.trace_len).value)
+            N.ptr(out.trace_len).value, N.FLAG_WIDE if wide else 0)
+        ws = self.workspace(B, wide=wide, grad=out.grad_rows is not None)
+        args.workspace = N.ptr(ws).value
+        args.workspace_bytes = 0 if ws is None else ws.numel()
         N.check(N.lib().fp_rollout_batch(self.sim.handle, self.handle, ctypes.byref(args),
                                          N.stream_ptr(stream)))
         out._forced = ft
         return out
+
+    def workspace(self, B: int, *, wide: bool = False, grad: bool = False):
+        """Device scratch of the wide (HBM-resident) rollout for ``B`` episodes;
+        None when the compact shared-memory kernel applies.  Cached, grown on
+        demand."""
+        import torch
+
+        need = ctypes.c_int64()
+        N.check(N.lib().fp_rollout_workspace_size(
+            self.sim.handle, self.handle, ctypes.c_int32(B),
+            ctypes.c_int32(N.FLAG_WIDE if wide else 0), ctypes.c_int32(int(grad)),
+            ctypes.byref(need)))
+        if need.value == 0:
+            return None
+        ws = getattr(self, "_ws", None)
+        if ws is None or ws.numel() < need.value:
+            self._ws = ws = torch.empty(need.value, dtype=torch.uint8, device="cuda")
+        return ws
 
     def policy_gradient(self, batch: RolloutBatch, alpha, beta: float, grad=None, stream=None):
         """Flat parameter gradient of sum_e alpha_e * sum lp_e + beta * sum ent_e

@@ -201,8 +201,24 @@ class SimProblem:
                                          ctypes.c_int64(seed), N.ptr(out)))
         return out
 
+    def workspace(self, B: int, wide: bool = False):
+        """Device scratch for ``B`` simulations (None on the compact shared-memory
+        path); cached and grown on demand."""
+        import torch
+
+        need = ctypes.c_int64()
+        N.check(N.lib().fp_sim_workspace_size(self.handle, ctypes.c_int32(B),
+                                              ctypes.c_int32(N.FLAG_WIDE if wide else 0),
+                                              ctypes.byref(need)))
+        if need.value == 0:
+            return None
+        ws = getattr(self, "_ws", None)
+        if ws is None or ws.numel() < need.value:
+            self._ws = ws = torch.empty(need.value, dtype=torch.uint8, device="cuda")
+        return ws
+
     def simulate(self, assign, strategy: str = "fifo", *, jitter=None, trace: bool = False,
-                 stream=None):
+                 stream=None, wide: bool = False):
         """Batched simulation of device-resident int32 assignments [B, n].
 
         Returns a dict of device tensors: makespan [B] f64, status [B] i32 and,
@@ -227,11 +243,13 @@ class SimProblem:
         if jitter is not None:
             jitter = jitter.contiguous()
             jstride = jitter.shape[-1] if jitter.dim() == 2 else 0
+        ws = self.workspace(B, wide)
         N.check(N.lib().fp_sim_batch(
             self.handle, N.ptr(assign), ctypes.c_int32(B), ctypes.c_int32(code), N.ptr(jitter),
             ctypes.c_int64(jstride), N.ptr(out["makespan"]), N.ptr(out["status"]),
             N.ptr(out.get("events")), ctypes.c_int32(cap), N.ptr(out.get("trace_len")),
-            N.ptr(out.get("blocked")), N.stream_ptr(stream)))
+            N.ptr(out.get("blocked")), N.ptr(ws), ctypes.c_int64(0 if ws is None else ws.numel()),
+            ctypes.c_int32(N.FLAG_WIDE if wide else 0), N.stream_ptr(stream)))
         return out
 
 

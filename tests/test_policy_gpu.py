@@ -178,3 +178,98 @@ def test_epsilon_one_is_uniform(torch_cuda):
     assert np.all(np.abs(counts - B / 4) <= 4 * sigma)
     lp = rb.step_lp.cpu().numpy()
     assert np.allclose(lp[:, :, 1], np.log(0.5), atol=1e-12)
+
+
+# ---- wide (HBM-resident) rollout path --------------------------------------
+def _rollout_np(rb):
+    return {k: getattr(rb, k).cpu().numpy() for k in (
+        "assign", "status", "makespan", "step_vd", "step_lp", "step_ent", "step_argmax",
+        "step_ncand")}
+
+
+@pytest.mark.parametrize("which", ["ffnn", "llama"])
+def test_wide_rollout_matches_compact(which, torch_cuda):
+    """The candidate-tree / HBM-state kernel forced onto graphs the compact
+    kernel also runs: identical actions, assignments and makespans under the
+    same Philox draws; log-probs and entropies within 1e-12 (the tree sums
+    candidates in a different order)."""
+    if which == "ffnn":
+        g, cl = builders.build_ffnn(8, 4, 16, 4, 2), ClusterSpec.uniform(8, 1e6, 1e5)
+    else:
+        g, cl = builders.build_llama_block(), ClusterSpec.uniform(8, 1e9, 1e7)
+    pc = PolicyConfig()
+    params = init_policy_params(pc, seed=5)
+    ctx = PolicyContext(g, cl, pc)
+    for mode, eps in (("sample", 0.2), ("sample", 0.9), ("teacher", 0.0), ("greedy", 0.0)):
+        a = _rollout_np(ctx.rollout_batch(params, 48, eps, 77, mode=mode, trace_steps=True))
+        b = _rollout_np(ctx.rollout_batch(params, 48, eps, 77, mode=mode, trace_steps=True,
+                                          wide=True))
+        assert (a["status"] == 0).all() and (b["status"] == 0).all()
+        for k in ("assign", "step_vd", "step_ncand", "makespan"):
+            assert np.array_equal(a[k], b[k]), (which, mode, k)
+        np.testing.assert_allclose(b["step_lp"], a["step_lp"], rtol=1e-12, atol=1e-14)
+        np.testing.assert_allclose(b["step_ent"], a["step_ent"], rtol=1e-12, atol=1e-14)
+        assert np.array_equal(a["step_argmax"], b["step_argmax"]), (which, mode)
+        # forced replay of the same actions through the wide kernel
+        f = _rollout_np(ctx.rollout_batch(params, 48, eps, 0, mode="forced",
+                                          forced=a["step_vd"], trace_steps=True, wide=True))
+        assert np.array_equal(f["assign"], a["assign"]) and np.array_equal(f["makespan"],
+                                                                           a["makespan"])
+        np.testing.assert_allclose(f["step_lp"], a["step_lp"], rtol=1e-12, atol=1e-14)
+
+
+def test_wide_bad_actions_terminate(torch_cuda):
+    """A bad forced device far beyond the hand-off ring depth must release the
+    producer warp (no hang) and report FP_EP_BAD_ACTION."""
+    g, cl = builders.build_llama_block(), ClusterSpec.uniform(8, 1e9, 1e7)
+    pc = PolicyConfig()
+    params = init_policy_params(pc, seed=0)
+    ctx = PolicyContext(g, cl, pc)
+    ref = ctx.rollout_batch(params, 2, 0.0, 0, mode="teacher", trace_steps=True)
+    acts = ref.step_vd.cpu().numpy().copy()
+    acts[0, 3, 1] = 99        # bad device early: SEL warp is blocked on a full ring
+    acts[1, 150, 0] = 10 ** 6  # bad vertex late
+    rb = ctx.rollout_batch(params, 2, 0.0, 0, mode="forced", forced=acts, wide=True)
+    assert rb.status.cpu().numpy().tolist() == [3, 3]
+
+
+def test_wide_large_dag_matches_oracle_draws(torch_cuda):
+    """A 2k-op sparse DAG (beyond the compact kernel): sampled episodes equal
+    the numpy oracle's under the same Philox draws; makespans bit-exact."""
+    g, cl = builders.sparse_dag(2000, seed=3), ClusterSpec.uniform(8, 1e9, 1e7)
+    pc = PolicyConfig()
+    params = init_policy_params(pc, seed=1)
+    ctx = PolicyContext(g, cl, pc)
+    assert ctx.workspace(4) is not None
+    B, seed = 4, 31
+    rb = ctx.rollout_batch(params, B, 0.2, seed, trace_steps=True)
+    r = _rollout_np(rb)
+    assert (r["status"] == 0).all()
+    octx = _oracle_ctx(ctx)
+    P = OP.leaves(params, need=False)
+    for b in (0, 3):
+        ro = OP.rollout(P, octx, 0.2, mode="uniform", seed=seed, episode=b)
+        got = [(int(r["step_vd"][b, t, 0]), int(r["step_vd"][b, t, 1])) for t in range(len(g))]
+        assert got == [(s["vertex"], s["device"]) for s in ro["steps"]], b
+        for t in range(0, len(g), 97):
+            s = ro["steps"][t]
+            assert _close(r["step_lp"][b, t, 0], s["sel_logprob"])
+            assert _close(r["step_ent"][b, t, 0], s["sel_entropy"])
+            assert _close(r["step_lp"][b, t, 1], s["plc_logprob"])
+        omk, _ = osim.exec_time(g, r["assign"][b], cl)
+        assert r["makespan"][b] == omk
+
+
+def test_forest_path_sums_match_path_lists(torch_cuda):
+    """SEL logits from pointer-jumped path sums (large-graph form) equal the
+    explicit path-list sums to rounding."""
+    for g, cl in ((builders.build_llama_block(), ClusterSpec.uniform(8, 1e9, 1e7)),
+                  (builders.sparse_dag(900, seed=4), ClusterSpec.uniform(8, 1e9, 1e7))):
+        pc = PolicyConfig()
+        params = init_policy_params(pc, seed=2)
+        a = PolicyContext(g, cl, pc)
+        b = PolicyContext(g, cl, pc, forest=True)
+        a.prepare(params)
+        b.prepare(params)
+        np.testing.assert_allclose(b.read_table("sel_logit"), a.read_table("sel_logit"),
+                                   rtol=1e-11, atol=1e-12)
