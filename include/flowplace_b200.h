@@ -214,6 +214,11 @@ typedef struct fp_rollout_args {
 
 int fp_policy_create(const fp_problem *p, const fp_policy_desc *desc, fp_policy **out);
 int fp_policy_destroy(fp_policy *pol);
+/* Encoder implementation: 0 (default) = aggregation kernels + fp64 tensor-core
+ * (DMMA) node-MLP kernels when hidden is a multiple of 8 (<= 64); 1 = one
+ * fused CUDA-core kernel per round with the reference's per-column FMA order.
+ * Both agree with the reference to rounding (1e-11). */
+int fp_policy_set_encoder(fp_policy *pol, int32_t fused);
 /* GNN encode + head tables for one parameter snapshot (params: device flat). */
 int fp_policy_prepare(fp_policy *pol, const double *params, void *stream);
 int fp_policy_table(const fp_policy *pol, int32_t which, const double **ptr, int64_t *count);

@@ -15,14 +15,16 @@
 #include <algorithm>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "fp_common.cuh"
 #include "fp_policy.cuh"
+#include "fp_gnn.cuh"
 
 namespace fp {
 
-constexpr int kEncWarps = 4;
+constexpr int kEncWarps = 8;
 
 __device__ __forceinline__ double leaky(double x, double s) { return x > 0.0 ? x : s * x; }
 
@@ -38,158 +40,266 @@ __device__ __forceinline__ double bcast(const double (&v)[HPL], int i) {
     return r;
 }
 
-template <int HPL>
-__global__ void __launch_bounds__(kEncWarps * 32)
+// Weight staging: every block of an encoder reads the same small matrices,
+// so they are copied to shared memory once per block (h <= 32) and the
+// per-vertex MLPs read them with conflict-free LDS (lane = column).
+struct RoundW {
+    const double *psw, *psb, *phw, *phb, *nw;  // psi (k==0: 15 rows; else the edge row only)
+    const double *szw, *szb, *pzw, *pzb, *w1a, *w1b, *w1d;  // last-round head weights
+};
+
+__device__ __forceinline__ void stage(double *dst, const double *src, int count) {
+    for (int i = threadIdx.x; i < count; i += blockDim.x) dst[i] = src[i];
+}
+
+// doubles of shared memory the staged weights of round k need
+__host__ __device__ inline int round_smem_doubles(int h, int k, bool last, bool sel, bool plc) {
+    const int dk = k == 0 ? 7 : h;
+    int c = (k == 0 ? (2 * dk + 1) * h : h) + h + (dk + h) * h + h;
+    if (!last) c += 2 * h * h;
+    else {
+        if (sel) c += 6 * h;
+        if (plc) c += 6 * h + 3 * h * h;
+    }
+    return c;
+}
+
+// One GNN round for every vertex of one encoder (blockIdx.y): gather +
+// segment-reduce of the messages into v (CSR by destination, message order
+// kept), the phi update, and either the next round's P/Q projections or the
+// last round's head rows.  Warps stride over destinations; a warp loads up
+// to 32 message (source, edge) pairs with one coalesced access, then gathers
+// the P[src] rows four at a time (independent 256-byte loads in flight) and
+// accumulates them in message order (bit-identical to the sequential sum).
+// BWD: also store U / AG / Zp for the REINFORCE backward (compact graphs).
+// HC: hidden width as a compile-time constant (0 = runtime P.h) so the
+// per-vertex MLP loops fully unroll -- the loads and shuffles of later
+// columns then overlap the dependent fp64 FMA chain.
+template <int HPL, int HC, bool STAGE, bool BWD>
+__global__ void __launch_bounds__(kEncWarps * 32, 3)
 encode_round_kernel(DevPolicy P, int k, int last) {
+    extern __shared__ __align__(16) double wsm[];
     const int lane = lane_id();
-    const int gw = blockIdx.x * kEncWarps + (threadIdx.x >> 5);
-    const int n = P.n, h = P.h;
-    const int e = gw / max(n, 1), v = gw - e * n;
-    if (e >= P.n_enc || n == 0) return;
+    const int warp = threadIdx.x >> 5;
+    const int e = blockIdx.y;
+    const int n = P.n, h = HC ? HC : P.h;
     const int dk = k == 0 ? 7 : h;
     const double *Hk = P.H[e][k];
-    const double *psw = P.W(gnn_role(e, k, 0)), *psb = P.W(gnn_role(e, k, 1));
-    const double *phw = P.W(gnn_role(e, k, 2)), *phb = P.W(gnn_role(e, k, 3));
     const double s = P.slope;
+    const bool feeds_sel = e == 0;
+    const bool feeds_plc = P.n_enc == 1 || e == 1;
 
-    double q[HPL], we[HPL], bb[HPL], agg[HPL];
-#pragma unroll
-    for (int t = 0; t < HPL; ++t) {
-        const int j = lane + 32 * t;
-        q[t] = we[t] = bb[t] = agg[t] = 0.0;
-        if (j < h) {
-            if (k == 0) {
-                double acc = 0.0;
-                for (int i = 0; i < 7; ++i) acc = fma(Hk[v * 7 + i], psw[(dk + i) * h + j], acc);
-                q[t] = acc;
-            } else {
-                q[t] = P.Qm[e][k][(size_t)v * h + j];
+    RoundW W;
+    {
+        const double *psw = P.W(gnn_role(e, k, 0)), *psb = P.W(gnn_role(e, k, 1));
+        const double *phw = P.W(gnn_role(e, k, 2)), *phb = P.W(gnn_role(e, k, 3));
+        const double *nw = last ? nullptr : P.W(gnn_role(e, k + 1, 0));
+        if constexpr (STAGE) {
+            double *o = wsm;
+            auto put = [&](const double *src, int count) {
+                stage(o, src, count);
+                const double *at = o;
+                o += count;
+                return at;
+            };
+            W.psw = k == 0 ? put(psw, (2 * dk + 1) * h) : put(psw + (size_t)2 * dk * h, h) - (size_t)2 * dk * h;
+            W.psb = put(psb, h);
+            W.phw = put(phw, (dk + h) * h);
+            W.phb = put(phb, h);
+            W.nw = last ? nullptr : put(nw, 2 * h * h);
+            W.szw = W.szb = W.pzw = W.pzb = W.w1a = W.w1b = W.w1d = nullptr;
+            if (last && feeds_sel) { W.szw = put(P.W(PR_SEL_Z_W), 5 * h); W.szb = put(P.W(PR_SEL_Z_B), h); }
+            if (last && feeds_plc) {
+                const double *w1 = P.W(PR_PLC_H1_W);
+                W.pzw = put(P.W(PR_PLC_Z_W), 5 * h);
+                W.pzb = put(P.W(PR_PLC_Z_B), h);
+                W.w1a = put(w1, h * h);
+                W.w1b = put(w1 + (size_t)h * h, h * h);
+                W.w1d = put(w1 + (size_t)3 * h * h, h * h);
             }
-            we[t] = psw[(2 * dk) * h + j];
-            bb[t] = psb[j];
+            __syncthreads();
+        } else {
+            W.psw = psw; W.psb = psb; W.phw = phw; W.phb = phb; W.nw = nw;
+            W.szw = P.W(PR_SEL_Z_W); W.szb = P.W(PR_SEL_Z_B);
+            W.pzw = P.W(PR_PLC_Z_W); W.pzb = P.W(PR_PLC_Z_B);
+            const double *w1 = P.W(PR_PLC_H1_W);
+            W.w1a = w1; W.w1b = w1 + (size_t)h * h; W.w1d = w1 + (size_t)3 * h * h;
         }
     }
-    for (int m = P.adj_ptr[v]; m < P.adj_ptr[v + 1]; ++m) {
-        const int w = P.adj_nbr[m];
-        const double ev = P.adj_e[m];
+
+    for (int v = blockIdx.x * kEncWarps + warp; v < n; v += gridDim.x * kEncWarps) {
+        double q[HPL], we[HPL], bb[HPL], agg[HPL];
+        // this vertex's own input row, one element per lane (broadcast by shfl)
+        const double hrow0 = lane < dk ? Hk[(size_t)v * dk + lane] : 0.0;
+        const double hrow1 = (HPL > 1 && lane + 32 < dk) ? Hk[(size_t)v * dk + lane + 32] : 0.0;
 #pragma unroll
         for (int t = 0; t < HPL; ++t) {
             const int j = lane + 32 * t;
-            if (j >= h) continue;
-            double p;
-            if (k == 0) {
-                p = 0.0;
-                for (int i = 0; i < 7; ++i) p = fma(Hk[w * 7 + i], psw[i * h + j], p);
-            } else {
-                p = P.Pm[e][k][(size_t)w * h + j];
+            q[t] = we[t] = bb[t] = agg[t] = 0.0;
+            if (j < h) {
+                if (k == 0) {
+                    double acc = 0.0;
+                    for (int i = 0; i < 7; ++i)
+                        acc = fma(__shfl_sync(FP_FULL_MASK, hrow0, i), W.psw[(dk + i) * h + j], acc);
+                    q[t] = acc;
+                } else {
+                    q[t] = P.Qm[e][k][(size_t)v * h + j];
+                }
+                we[t] = W.psw[(2 * dk) * h + j];
+                bb[t] = W.psb[j];
             }
-            agg[t] += leaky(p + q[t] + ev * we[t] + bb[t], s);
         }
-    }
-    // update: U = [H | agg] @ phi.w + phi.b
-    double u[HPL];
+        const int m0 = P.adj_ptr[v], m1 = P.adj_ptr[v + 1];
+        for (int c0 = m0; c0 < m1; c0 += 32) {
+            const int cnt = min(32, m1 - c0);
+            const int my_w = lane < cnt ? P.adj_nbr[c0 + lane] : 0;
+            const double my_e = lane < cnt ? P.adj_e[c0 + lane] : 0.0;
+            for (int i0 = 0; i0 < cnt; i0 += 4) {
+                int wv[4];
+                double ev[4];
 #pragma unroll
-    for (int t = 0; t < HPL; ++t) u[t] = 0.0;
-    for (int i = 0; i < dk; ++i) {
-        const double hv = Hk[(size_t)v * dk + i];
+                for (int u = 0; u < 4; ++u) {
+                    wv[u] = __shfl_sync(FP_FULL_MASK, my_w, (i0 + u) & 31);
+                    ev[u] = __shfl_sync(FP_FULL_MASK, my_e, (i0 + u) & 31);
+                }
 #pragma unroll
-        for (int t = 0; t < HPL; ++t) {
-            const int j = lane + 32 * t;
-            if (j < h) u[t] = fma(hv, phw[i * h + j], u[t]);
+                for (int t = 0; t < HPL; ++t) {
+                    const int j = lane + 32 * t;
+                    if (j >= h) continue;
+                    double pv[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        pv[u] = 0.0;
+                        if (i0 + u < cnt) {
+                            if (k == 0) {
+                                const double *hw = Hk + (size_t)wv[u] * 7;
+                                double p = 0.0;
+                                for (int i = 0; i < 7; ++i) p = fma(hw[i], W.psw[i * h + j], p);
+                                pv[u] = p;
+                            } else {
+                                pv[u] = P.Pm[e][k][(size_t)wv[u] * h + j];
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (i0 + u < cnt) agg[t] += leaky(pv[u] + q[t] + ev[u] * we[t] + bb[t], s);
+                }
+            }
         }
-    }
-    for (int i = 0; i < h; ++i) {
-        const double a = bcast<HPL>(agg, i);
+        // update: U = [H | agg] @ phi.w + phi.b
+        double u[HPL];
 #pragma unroll
-        for (int t = 0; t < HPL; ++t) {
-            const int j = lane + 32 * t;
-            if (j < h) u[t] = fma(a, phw[(dk + i) * h + j], u[t]);
-        }
-    }
-    double hn[HPL];
+        for (int t = 0; t < HPL; ++t) u[t] = 0.0;
+        auto self_term = [&](auto DK) {
+            constexpr int dkc = decltype(DK)::value;
+            const int dkr = dkc ? dkc : dk;
+#pragma unroll 8
+            for (int i = 0; i < dkr; ++i) {
+                const double hv = __shfl_sync(FP_FULL_MASK, i < 32 ? hrow0 : hrow1, i & 31);
 #pragma unroll
-    for (int t = 0; t < HPL; ++t) {
-        const int j = lane + 32 * t;
-        hn[t] = 0.0;
-        if (j < h) {
-            u[t] += phb[j];
-            hn[t] = leaky(u[t], s);
-            P.U[e][k][(size_t)v * h + j] = u[t];
-            P.AG[e][k][(size_t)v * h + j] = agg[t];
-            P.H[e][k + 1][(size_t)v * h + j] = hn[t];
-        }
-    }
-    if (!last) {
-        const double *nw = P.W(gnn_role(e, k + 1, 0));
-        double pp[HPL], qq[HPL];
-#pragma unroll
-        for (int t = 0; t < HPL; ++t) pp[t] = qq[t] = 0.0;
+                for (int t = 0; t < HPL; ++t) {
+                    const int j = lane + 32 * t;
+                    if (j < h) u[t] = fma(hv, W.phw[i * h + j], u[t]);
+                }
+            }
+        };
+        if (k == 0) self_term(std::integral_constant<int, 7>{});
+        else self_term(std::integral_constant<int, HC>{});
+#pragma unroll 8
         for (int i = 0; i < h; ++i) {
-            const double a = bcast<HPL>(hn, i);
+            const double a = bcast<HPL>(agg, i);
+#pragma unroll
+            for (int t = 0; t < HPL; ++t) {
+                const int j = lane + 32 * t;
+                if (j < h) u[t] = fma(a, W.phw[(dk + i) * h + j], u[t]);
+            }
+        }
+        double hn[HPL];
+#pragma unroll
+        for (int t = 0; t < HPL; ++t) {
+            const int j = lane + 32 * t;
+            hn[t] = 0.0;
+            if (j < h) {
+                u[t] += W.phb[j];
+                hn[t] = leaky(u[t], s);
+                if constexpr (BWD) {
+                    P.U[e][k][(size_t)v * h + j] = u[t];
+                    P.AG[e][k][(size_t)v * h + j] = agg[t];
+                }
+                P.H[e][k + 1][(size_t)v * h + j] = hn[t];
+            }
+        }
+        if (!last) {
+            double pp[HPL], qq[HPL];
+#pragma unroll
+            for (int t = 0; t < HPL; ++t) pp[t] = qq[t] = 0.0;
+#pragma unroll 8
+            for (int i = 0; i < h; ++i) {
+                const double a = bcast<HPL>(hn, i);
+#pragma unroll
+                for (int t = 0; t < HPL; ++t) {
+                    const int j = lane + 32 * t;
+                    if (j < h) {
+                        pp[t] = fma(a, W.nw[i * h + j], pp[t]);
+                        qq[t] = fma(a, W.nw[(h + i) * h + j], qq[t]);
+                    }
+                }
+            }
 #pragma unroll
             for (int t = 0; t < HPL; ++t) {
                 const int j = lane + 32 * t;
                 if (j < h) {
-                    pp[t] = fma(a, nw[i * h + j], pp[t]);
-                    qq[t] = fma(a, nw[(h + i) * h + j], qq[t]);
+                    P.Pm[e][k + 1][(size_t)v * h + j] = pp[t];
+                    P.Qm[e][k + 1][(size_t)v * h + j] = qq[t];
                 }
             }
+            continue;
         }
-#pragma unroll
-        for (int t = 0; t < HPL; ++t) {
-            const int j = lane + 32 * t;
-            if (j < h) {
-                P.Pm[e][k + 1][(size_t)v * h + j] = pp[t];
-                P.Qm[e][k + 1][(size_t)v * h + j] = qq[t];
-            }
-        }
-        return;
-    }
-    // ---- last round: per-vertex head rows ----
-    const bool feeds_sel = e == 0;
-    const bool feeds_plc = P.n_enc == 1 || e == 1;
-    const double *x = P.x + (size_t)v * 5;
-    if (feeds_sel) {
-        const double *zw = P.W(PR_SEL_Z_W), *zb = P.W(PR_SEL_Z_B);
-#pragma unroll
-        for (int t = 0; t < HPL; ++t) {
-            const int j = lane + 32 * t;
-            if (j >= h) continue;
-            double z = 0.0;
-            for (int i = 0; i < 5; ++i) z = fma(x[i], zw[i * h + j], z);
-            P.Zs[(size_t)v * h + j] = z + zb[j];
-        }
-    }
-    if (feeds_plc) {
-        const double *zw = P.W(PR_PLC_Z_W), *zb = P.W(PR_PLC_Z_B), *w1 = P.W(PR_PLC_H1_W);
-        double z[HPL], a[HPL], g[HPL];
-#pragma unroll
-        for (int t = 0; t < HPL; ++t) {
-            const int j = lane + 32 * t;
-            z[t] = a[t] = g[t] = 0.0;
-            if (j >= h) continue;
-            double acc = 0.0;
-            for (int i = 0; i < 5; ++i) acc = fma(x[i], zw[i * h + j], acc);
-            z[t] = acc + zb[j];
-            P.Zp[(size_t)v * h + j] = z[t];
-        }
-        for (int i = 0; i < h; ++i) {
-            const double hv = bcast<HPL>(hn, i), zv = bcast<HPL>(z, i);
+        // ---- last round: per-vertex head rows ----
+        const double xr = lane < 5 ? P.x[(size_t)v * 5 + lane] : 0.0;
+        if (feeds_sel) {
 #pragma unroll
             for (int t = 0; t < HPL; ++t) {
                 const int j = lane + 32 * t;
-                if (j >= h) continue;
-                a[t] = fma(hv, w1[i * h + j], a[t]);
-                a[t] = fma(zv, w1[(3 * h + i) * h + j], a[t]);
-                g[t] = fma(hv, w1[(h + i) * h + j], g[t]);
+                double z = 0.0;
+                for (int i = 0; i < 5; ++i)
+                    z = fma(__shfl_sync(FP_FULL_MASK, xr, i), W.szw[i * h + j < 5 * h ? i * h + j : 0], z);
+                if (j < h) P.Zs[(size_t)v * h + j] = z + W.szb[j];
             }
         }
+        if (feeds_plc) {
+            double z[HPL], a[HPL], g[HPL];
 #pragma unroll
-        for (int t = 0; t < HPL; ++t) {
-            const int j = lane + 32 * t;
-            if (j < h) {
-                P.A[(size_t)v * h + j] = a[t];
-                P.G[(size_t)v * h + j] = g[t];
+            for (int t = 0; t < HPL; ++t) {
+                const int j = lane + 32 * t;
+                z[t] = a[t] = g[t] = 0.0;
+                double acc = 0.0;
+                for (int i = 0; i < 5; ++i)
+                    acc = fma(__shfl_sync(FP_FULL_MASK, xr, i), W.pzw[i * h + j < 5 * h ? i * h + j : 0], acc);
+                if (j >= h) continue;
+                z[t] = acc + W.pzb[j];
+                if constexpr (BWD) P.Zp[(size_t)v * h + j] = z[t];
+            }
+#pragma unroll 8
+            for (int i = 0; i < h; ++i) {
+                const double hv = bcast<HPL>(hn, i), zv = bcast<HPL>(z, i);
+#pragma unroll
+                for (int t = 0; t < HPL; ++t) {
+                    const int j = lane + 32 * t;
+                    if (j >= h) continue;
+                    a[t] = fma(hv, W.w1a[i * h + j], a[t]);
+                    a[t] = fma(zv, W.w1d[i * h + j], a[t]);
+                    g[t] = fma(hv, W.w1b[i * h + j], g[t]);
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < HPL; ++t) {
+                const int j = lane + 32 * t;
+                if (j < h) {
+                    P.A[(size_t)v * h + j] = a[t];
+                    P.G[(size_t)v * h + j] = g[t];
+                }
             }
         }
     }
@@ -200,6 +310,7 @@ encode_round_kernel(DevPolicy P, int k, int last) {
 // path(v) and J(v) points 2^(r+1) vertices down it (-1 past the end).
 // Round 0 reads H and the next arrays; round r >= 1 ping-pongs PS/PJ.
 // Pure gather-add over n x h doubles per round (HBM / L2 bound).
+template <bool VEC2>
 __global__ void path_jump_kernel(DevPolicy P, int r) {
     const int which = blockIdx.y;  // 0 = b-paths, 1 = t-paths
     const int n = P.n, h = P.h;
@@ -207,22 +318,44 @@ __global__ void path_jump_kernel(DevPolicy P, int r) {
     const int *Jin = r == 0 ? P.nxt[which] : P.PJ[which][(r - 1) & 1];
     double *Sout = P.PS[which][r & 1];
     int *Jout = P.PJ[which][r & 1];
-    const int64_t total = (int64_t)n * h;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int v = (int)(i / h), j = (int)(i - (int64_t)v * h);
-        const int w = Jin[v];
-        Sout[i] = w >= 0 ? Sin[i] + Sin[(size_t)w * h + j] : Sin[i];
-        if (j == 0) Jout[v] = w >= 0 ? Jin[w] : -1;
+    if constexpr (VEC2) {  // h even: 16-byte accesses, two columns per thread
+        const int h2 = h >> 1;
+        const int64_t total = (int64_t)n * h2;
+        const double2 *S2 = (const double2 *)Sin;
+        double2 *O2 = (double2 *)Sout;
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+             i += (int64_t)gridDim.x * blockDim.x) {
+            const int v = (int)(i / h2), j = (int)(i - (int64_t)v * h2);
+            const int w = Jin[v];
+            double2 a = S2[i];
+            if (w >= 0) {
+                const double2 b = S2[(size_t)w * h2 + j];
+                a.x += b.x;
+                a.y += b.y;
+            }
+            O2[i] = a;
+            if (j == 0) Jout[v] = w >= 0 ? Jin[w] : -1;
+        }
+    } else {
+        const int64_t total = (int64_t)n * h;
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+             i += (int64_t)gridDim.x * blockDim.x) {
+            const int v = (int)(i / h), j = (int)(i - (int64_t)v * h);
+            const int w = Jin[v];
+            Sout[i] = w >= 0 ? Sin[i] + Sin[(size_t)w * h + j] : Sin[i];
+            if (j == 0) Jout[v] = w >= 0 ? Jin[w] : -1;
+        }
     }
 }
 
 // SEL head over every vertex: s[v] = head(H[v] | sum_bpath H | sum_tpath H | Z[v]).
-template <int HPL>
-__global__ void __launch_bounds__(kEncWarps * 32) encode_sel_kernel(DevPolicy P) {
+// head1.w (4h x h) staged in shared memory; BWD also stores the embedding and
+// pre-activation rows the backward reads.
+template <int HPL, int HC, bool STAGE, bool BWD>
+__global__ void __launch_bounds__(kEncWarps * 32, 3) encode_sel_kernel(DevPolicy P) {
+    extern __shared__ __align__(16) double wsm[];
     const int lane = lane_id();
-    const int v = blockIdx.x * kEncWarps + (threadIdx.x >> 5);
-    const int n = P.n, h = P.h;
+    const int n = P.n, h = HC ? HC : P.h;
     const double s = P.slope;
     const double *Hs = P.H[0][P.K];
     if (blockIdx.x == 0 && (threadIdx.x >> 5) == 0) {
@@ -240,56 +373,66 @@ __global__ void __launch_bounds__(kEncWarps * 32) encode_sel_kernel(DevPolicy P)
             P.c[j] = acc + b1[j];
         }
     }
-    if (v >= n) return;
-    double em[4][HPL];
-#pragma unroll
-    for (int t = 0; t < HPL; ++t) {
-        const int j = lane + 32 * t;
-        em[0][t] = em[1][t] = em[2][t] = em[3][t] = 0.0;
-        if (j >= h) continue;
-        em[0][t] = Hs[(size_t)v * h + j];
-        double hb = 0.0, ht = 0.0;
-        if (P.forest) {
-            const int rr = P.jump_rounds;
-            hb = rr == 0 ? em[0][t] : P.PS[0][(rr - 1) & 1][(size_t)v * h + j];
-            ht = rr == 0 ? em[0][t] : P.PS[1][(rr - 1) & 1][(size_t)v * h + j];
-        } else {
-            for (int p = P.bp_ptr[v]; p < P.bp_ptr[v + 1]; ++p)
-                hb += Hs[(size_t)P.bp_idx[p] * h + j];
-            for (int p = P.tp_ptr[v]; p < P.tp_ptr[v + 1]; ++p)
-                ht += Hs[(size_t)P.tp_idx[p] * h + j];
-        }
-        em[1][t] = hb;
-        em[2][t] = ht;
-        em[3][t] = P.Zs[(size_t)v * h + j];
-        for (int b = 0; b < 4; ++b) P.emb[(size_t)v * 4 * h + b * h + j] = em[b][t];
-    }
     const double *w1 = P.W(PR_SEL_H1_W), *b1 = P.W(PR_SEL_H1_B), *w2 = P.W(PR_SEL_H2_W),
                  *b2 = P.W(PR_SEL_H2_B);
-    double acc[HPL];
+    if constexpr (STAGE) {
+        stage(wsm, w1, 4 * h * h);
+        __syncthreads();
+        w1 = wsm;
+    }
+    for (int v = blockIdx.x * kEncWarps + (threadIdx.x >> 5); v < n;
+         v += gridDim.x * kEncWarps) {
+        double em[4][HPL];
 #pragma unroll
-    for (int t = 0; t < HPL; ++t) acc[t] = 0.0;
-    for (int b = 0; b < 4; ++b)
-        for (int i = 0; i < h; ++i) {
-            const double ev = bcast<HPL>(em[b], i);
+        for (int t = 0; t < HPL; ++t) {
+            const int j = lane + 32 * t;
+            em[0][t] = em[1][t] = em[2][t] = em[3][t] = 0.0;
+            if (j >= h) continue;
+            em[0][t] = Hs[(size_t)v * h + j];
+            double hb = 0.0, ht = 0.0;
+            if (P.forest) {
+                const int rr = P.jump_rounds;
+                hb = rr == 0 ? em[0][t] : P.PS[0][(rr - 1) & 1][(size_t)v * h + j];
+                ht = rr == 0 ? em[0][t] : P.PS[1][(rr - 1) & 1][(size_t)v * h + j];
+            } else {
+                for (int p = P.bp_ptr[v]; p < P.bp_ptr[v + 1]; ++p)
+                    hb += Hs[(size_t)P.bp_idx[p] * h + j];
+                for (int p = P.tp_ptr[v]; p < P.tp_ptr[v + 1]; ++p)
+                    ht += Hs[(size_t)P.tp_idx[p] * h + j];
+            }
+            em[1][t] = hb;
+            em[2][t] = ht;
+            em[3][t] = P.Zs[(size_t)v * h + j];
+            if constexpr (BWD)
+                for (int b = 0; b < 4; ++b) P.emb[(size_t)v * 4 * h + b * h + j] = em[b][t];
+        }
+        double acc[HPL];
 #pragma unroll
-            for (int t = 0; t < HPL; ++t) {
-                const int j = lane + 32 * t;
-                if (j < h) acc[t] = fma(ev, w1[(b * h + i) * h + j], acc[t]);
+        for (int t = 0; t < HPL; ++t) acc[t] = 0.0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+#pragma unroll 8
+            for (int i = 0; i < h; ++i) {
+                const double ev = bcast<HPL>(em[b], i);
+#pragma unroll
+                for (int t = 0; t < HPL; ++t) {
+                    const int j = lane + 32 * t;
+                    if (j < h) acc[t] = fma(ev, w1[(b * h + i) * h + j], acc[t]);
+                }
+            }
+        double part = 0.0;
+#pragma unroll
+        for (int t = 0; t < HPL; ++t) {
+            const int j = lane + 32 * t;
+            if (j < h) {
+                const double pre = acc[t] + b1[j];
+                if constexpr (BWD) P.hidpre[(size_t)v * h + j] = pre;
+                part = fma(leaky(pre, s), w2[j], part);
             }
         }
-    double part = 0.0;
-#pragma unroll
-    for (int t = 0; t < HPL; ++t) {
-        const int j = lane + 32 * t;
-        if (j < h) {
-            const double pre = acc[t] + b1[j];
-            P.hidpre[(size_t)v * h + j] = pre;
-            part = fma(leaky(pre, s), w2[j], part);
-        }
+        part = warp_sum(part);
+        if (lane == 0) P.s[v] = part + b2[0];
     }
-    part = warp_sum(part);
-    if (lane == 0) P.s[v] = part + b2[0];
 }
 
 #define FP_CUDA_RET(call)                                                             \
@@ -301,33 +444,143 @@ __global__ void __launch_bounds__(kEncWarps * 32) encode_sel_kernel(DevPolicy P)
         }                                                                             \
     } while (0)
 
-int policy_prepare(fp_policy *pol, const double *params, cudaStream_t st) {
-    DevPolicy &P = pol->dev;
-    P.params = params;
-    if (P.n == 0) return FP_OK;
-    const int rows = P.n_enc * P.n;
-    const int grid = (rows + kEncWarps - 1) / kEncWarps;
+template <int HPL, int HC, bool STAGE, bool BWD>
+static int launch_encode(DevPolicy &P, cudaStream_t st) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int vblocks = (P.n + kEncWarps - 1) / kEncWarps;
     for (int k = 0; k < P.K; ++k) {
-        if (P.h <= 32)
-            encode_round_kernel<1><<<grid, kEncWarps * 32, 0, st>>>(P, k, k == P.K - 1);
-        else
-            encode_round_kernel<2><<<grid, kEncWarps * 32, 0, st>>>(P, k, k == P.K - 1);
+        const bool last = k == P.K - 1;
+        const int64_t smem = STAGE ? 8LL * round_smem_doubles(P.h, k, last, true, true) : 0;
+        auto kern = encode_round_kernel<HPL, HC, STAGE, BWD>;
+        if (smem > 48 * 1024)
+            FP_CUDA_RET(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem));
+        // staged weights amortise over many vertices per block: one resident wave
+        int occ = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kEncWarps * 32, (size_t)smem);
+        const int bx = STAGE ? std::min(vblocks, std::max(1, sms * std::max(occ, 1) / P.n_enc))
+                             : vblocks;
+        kern<<<dim3(std::max(bx, 1), P.n_enc), kEncWarps * 32, smem, st>>>(P, k, last);
         FP_CUDA_RET(cudaGetLastError());
     }
     if (P.forest)
         for (int r = 0; r < P.jump_rounds; ++r) {
             const int64_t total = (int64_t)P.n * P.h;
-            const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-            path_jump_kernel<<<dim3(blocks, 2), 256, 0, st>>>(P, r);
+            const int blocks = (int)std::min<int64_t>((total / 2 + 255) / 256, (int64_t)sms * 16);
+            if (P.h % 2 == 0)
+                path_jump_kernel<true><<<dim3(blocks, 2), 256, 0, st>>>(P, r);
+            else
+                path_jump_kernel<false><<<dim3(blocks, 2), 256, 0, st>>>(P, r);
             FP_CUDA_RET(cudaGetLastError());
         }
-    const int g2 = (P.n + kEncWarps - 1) / kEncWarps;
-    if (P.h <= 32)
-        encode_sel_kernel<1><<<g2, kEncWarps * 32, 0, st>>>(P);
-    else
-        encode_sel_kernel<2><<<g2, kEncWarps * 32, 0, st>>>(P);
+    const int64_t smem2 = STAGE ? 8LL * 4 * P.h * P.h : 0;
+    auto kern2 = encode_sel_kernel<HPL, HC, STAGE, BWD>;
+    if (smem2 > 48 * 1024)
+        FP_CUDA_RET(cudaFuncSetAttribute(kern2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem2));
+    int occ2 = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, kern2, kEncWarps * 32, (size_t)smem2);
+    const int bx2 = STAGE ? std::min(vblocks, sms * std::max(occ2, 1)) : vblocks;
+    kern2<<<std::max(bx2, 1), kEncWarps * 32, smem2, st>>>(P);
     FP_CUDA_RET(cudaGetLastError());
     return FP_OK;
+}
+
+// Split encoder: aggregation kernels (HBM) + DMMA node-MLP kernels, for
+// hidden widths that tile by 8 (every PolicyConfig the reference ships).
+template <int H, bool BWD>
+static int launch_gnn_tc(DevPolicy &P, cudaStream_t st) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int warps = H <= 32 ? 8 : 4, threads = warps * 32;
+    const int tiles = (P.n + 7) / 8;
+    const int tile_blocks = (tiles + warps - 1) / warps;
+    auto grid_for = [&](const void *kern, int64_t smem, int want) {
+        int occ = 1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, (size_t)smem) !=
+                cudaSuccess || occ < 1)
+            occ = 1;
+        return std::max(1, std::min(want, std::max(1, sms * occ / P.n_enc)));
+    };
+    auto set_smem = [&](const void *kern, int64_t smem) {
+        if (smem > 48 * 1024)
+            return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        return cudaSuccess;
+    };
+    {
+        const int64_t smem = 8LL * (2 * (2 * H / 8) * 32 + warps * 8 * tile_stride(8));
+        const void *kern = (const void *)gnn_proj0_kernel<H>;
+        FP_CUDA_RET(set_smem(kern, smem));
+        gnn_proj0_kernel<H><<<dim3(grid_for(kern, smem, tile_blocks), P.n_enc), threads, smem, st>>>(P);
+        FP_CUDA_RET(cudaGetLastError());
+    }
+    constexpr int VPW = H / 2 >= 32 ? 1 : 32 / (H / 2);
+    const int agg_blocks = (P.n + 8 * VPW - 1) / (8 * VPW);
+    for (int k = 0; k < P.K; ++k) {
+        const bool last = k == P.K - 1;
+        {
+            const void *kern = (const void *)gnn_agg_kernel<H>;
+            gnn_agg_kernel<H><<<dim3(grid_for(kern, 0, agg_blocks), P.n_enc), 256, 0, st>>>(P, k);
+            FP_CUDA_RET(cudaGetLastError());
+        }
+        const int64_t smem = 8LL * node_smem_doubles(H, k, last, warps);
+        const void *kern = (const void *)gnn_node_kernel<H, BWD>;
+        FP_CUDA_RET(set_smem(kern, smem));
+        gnn_node_kernel<H, BWD><<<dim3(grid_for(kern, smem, tile_blocks), P.n_enc), threads, smem,
+                                  st>>>(P, k, last);
+        FP_CUDA_RET(cudaGetLastError());
+    }
+    if (P.forest)
+        for (int r = 0; r < P.jump_rounds; ++r) {
+            const int64_t total = (int64_t)P.n * H;
+            const int blocks = (int)std::min<int64_t>((total / 2 + 255) / 256, (int64_t)sms * 16);
+            path_jump_kernel<true><<<dim3(blocks, 2), 256, 0, st>>>(P, r);
+            FP_CUDA_RET(cudaGetLastError());
+        }
+    {
+        const int64_t smem = 8LL * sel_smem_doubles(H, warps);
+        const void *kern = (const void *)gnn_sel_kernel<H, BWD>;
+        FP_CUDA_RET(set_smem(kern, smem));
+        int occ = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, (size_t)smem);
+        const int gx = std::max(1, std::min(tile_blocks, sms * std::max(occ, 1)));
+        gnn_sel_kernel<H, BWD><<<gx, threads, smem, st>>>(P);
+        FP_CUDA_RET(cudaGetLastError());
+    }
+    return FP_OK;
+}
+
+template <int H>
+static int launch_gnn_tc_any(DevPolicy &P, cudaStream_t st) {
+    return P.forest ? launch_gnn_tc<H, false>(P, st) : launch_gnn_tc<H, true>(P, st);
+}
+
+int policy_prepare(fp_policy *pol, const double *params, cudaStream_t st) {
+    {
+        DevPolicy &P = pol->dev;
+        P.params = params;
+        if (P.n == 0) return FP_OK;
+        if (!pol->fused_encoder) switch (P.h) {
+            case 8: return launch_gnn_tc_any<8>(P, st);
+            case 16: return launch_gnn_tc_any<16>(P, st);
+            case 32: return launch_gnn_tc_any<32>(P, st);
+            case 64: return launch_gnn_tc_any<64>(P, st);
+            default: break;
+        }
+    }
+    DevPolicy &P = pol->dev;
+    P.params = params;
+    if (P.n == 0) return FP_OK;
+    // forest-form policies (large graphs) are forward-only: no backward rows
+    const bool bwd = !P.forest;
+    if (P.h == 32)
+        return bwd ? launch_encode<1, 32, true, true>(P, st) : launch_encode<1, 32, true, false>(P, st);
+    if (P.h < 32)
+        return bwd ? launch_encode<1, 0, true, true>(P, st) : launch_encode<1, 0, true, false>(P, st);
+    return bwd ? launch_encode<2, 0, false, true>(P, st) : launch_encode<2, 0, false, false>(P, st);
 }
 
 }  // namespace fp
@@ -533,6 +786,12 @@ int fp_policy_destroy(fp_policy *pol) {
     if (pol->train) fp_train_state_free(pol->train);
     if (pol->arena) cudaFree(pol->arena);
     delete pol;
+    return FP_OK;
+}
+
+int fp_policy_set_encoder(fp_policy *pol, int32_t fused) {
+    if (!pol) { set_error("null argument"); return FP_ERR_INVALID; }
+    pol->fused_encoder = fused ? 1 : 0;
     return FP_OK;
 }
 

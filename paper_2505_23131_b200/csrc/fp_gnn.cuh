@@ -1,0 +1,418 @@
+// GNN encoder split into its two rooflines (flowplace/policy.py:149-223):
+//
+//   gnn_agg_kernel   message passing: for every destination v,
+//                    agg[v] = sum_{m into v} leaky(P[src_m] + Q[v] + e_m*we + b)
+//                    (policy.py:159-166 with psi split by input block).  A
+//                    pure gather / segment-reduce over the CSR-by-destination
+//                    message list: H/2 lanes per destination, one 16-byte
+//                    load of P[src] per lane per message, four messages in
+//                    flight, summed in message order.  HBM-bound.
+//   gnn_node_kernel  the per-vertex MLPs as dense [rows x K] @ [K x N] tiles
+//                    on the fp64 tensor cores (DMMA, mma.sync m8n8k4 f64 --
+//                    the only tensor-core path that keeps the reference's
+//                    float64; tcgen05 has no f64 kind): phi update
+//                    U = [H | agg] @ phi.w + b, H' = leaky(U), then the next
+//                    round's P/Q projections or the head tables (Zs, Zp,
+//                    A = [H|Zp] @ [W1a; W1d], G = H @ W1b).
+//   gnn_proj0_kernel round-0 P/Q = H0 @ psi rows (7-column input).
+//   gnn_sel_kernel   SEL head over every vertex: [H | sum_b H | sum_t H | Zs]
+//                    @ head1.w (4h x h) -> leaky -> . head2.w  (DMMA).
+//
+// Weight matrices are staged once per block into shared memory in MMA
+// fragment order (each lane's B element contiguous: conflict-free), A tiles
+// are 8 vertex rows with a row stride == 4 (mod 16) doubles so the
+// half-warp fragment loads hit 16 distinct 8-byte banks.
+#pragma once
+
+#include "fp_common.cuh"
+#include "fp_policy.cuh"
+
+namespace fp {
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c[0]), "+d"(c[1])
+                 : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ double gleaky(double x, double s) { return x > 0.0 ? x : s * x; }
+
+// row stride (doubles) of an 8-row A tile with K columns
+__host__ __device__ constexpr int tile_stride(int K) { return ((K + 11) / 16) * 16 + 4; }
+
+// Stage a K x N matrix B(k, n) into fragment order [KT][NT][32]:
+// lane l of (kt, nt) holds B(kt*4 + l%4, nt*8 + l/4); rows >= K are zero.
+template <typename F>
+__device__ __forceinline__ void stage_frag(double *dst, int K, int KT, int NT, F B) {
+    for (int i = threadIdx.x; i < KT * NT * 32; i += blockDim.x) {
+        const int l = i & 31, nt = (i >> 5) % NT, kt = (i >> 5) / NT;
+        const int k = kt * 4 + (l & 3), nn = nt * 8 + (l >> 2);
+        dst[i] = k < K ? B(k, nn) : 0.0;
+    }
+}
+
+// acc[nt] += A(8 x KT*4, smem, stride sa) @ Bf(fragment order, KT x NT)
+// D fragment: acc[nt][i] = D[lane >> 2][nt*8 + (lane & 3)*2 + i]
+template <int NT>
+__device__ __forceinline__ void tile_mma(const double *As, int sa, int KT, const double *Bf,
+                                         double (&acc)[NT][2]) {
+    const int lane = lane_id();
+    const double *ap = As + (lane >> 2) * sa + (lane & 3);
+    const double *bp = Bf + lane;
+#pragma unroll 4
+    for (int kt = 0; kt < KT; ++kt) {
+        const double a = ap[kt * 4];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma(acc[nt], a, bp[(kt * NT + nt) * 32]);
+    }
+}
+
+template <int NT>
+__device__ __forceinline__ void zero_acc(double (&acc)[NT][2]) {
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+}
+
+// ---------------------------------------------------------------------------
+// Aggregation (HBM-bound gather / segment reduce)
+// ---------------------------------------------------------------------------
+template <int H>
+__global__ void __launch_bounds__(256) gnn_agg_kernel(DevPolicy P, int k) {
+    constexpr int HL = H / 2;                   // lanes per destination (double2 each)
+    constexpr int VPW = HL >= 32 ? 1 : 32 / HL; // destinations per warp
+    static_assert(H % 2 == 0 && H <= 64, "H must be even and <= 64");
+    const int e = blockIdx.y;
+    const int lane = lane_id();
+    const int sub = HL >= 32 ? 0 : lane / HL;
+    const int l = HL >= 32 ? lane : lane % HL;
+    const int n = P.n;
+    const int dk = k == 0 ? 7 : H;
+    const double *psw = P.W(gnn_role(e, k, 0)), *psb = P.W(gnn_role(e, k, 1));
+    // parameter rows sit at arbitrary offsets of the flat vector: scalar loads
+    const double2 we = make_double2(psw[(size_t)(2 * dk) * H + 2 * l], psw[(size_t)(2 * dk) * H + 2 * l + 1]);
+    const double2 bb = make_double2(psb[2 * l], psb[2 * l + 1]);
+    const double2 *Pm = (const double2 *)P.Pm[e][k];
+    const double2 *Qm = (const double2 *)P.Qm[e][k];
+    double2 *agg = (double2 *)P.AG[e][k];
+    const double s = P.slope;
+    const int warps = blockDim.x >> 5;
+    const int gw = blockIdx.x * warps + (threadIdx.x >> 5);
+    for (int vb = gw * VPW; vb < n; vb += gridDim.x * warps * VPW) {
+        const int v = vb + sub;
+        if (v >= n || (HL < 32 && lane >= VPW * HL)) continue;
+        const double2 q = Qm[(size_t)v * HL + l];
+        double ax = 0.0, ay = 0.0;
+        const int m1 = P.adj_ptr[v + 1];
+        for (int m = P.adj_ptr[v]; m < m1; m += 4) {
+            int w[4];
+            double ev[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const bool ok = m + u < m1;
+                w[u] = ok ? P.adj_nbr[m + u] : 0;
+                ev[u] = ok ? P.adj_e[m + u] : 0.0;
+            }
+            double2 p[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                p[u] = m + u < m1 ? Pm[(size_t)w[u] * HL + l] : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (m + u < m1) {
+                    // the reference message: leaky(P[src] + Q[dst] + e*we + b), summed in order
+                    ax += gleaky(p[u].x + q.x + ev[u] * we.x + bb.x, s);
+                    ay += gleaky(p[u].y + q.y + ev[u] * we.y + bb.y, s);
+                }
+        }
+        agg[(size_t)v * HL + l] = make_double2(ax, ay);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Round-0 projections: [P0 | Q0] = H0 (n x 7) @ [psi.w rows 0..6 | rows 7..13]
+// ---------------------------------------------------------------------------
+template <int H>
+__global__ void __launch_bounds__(256) gnn_proj0_kernel(DevPolicy P) {
+    constexpr int NT2 = 2 * H / 8;
+    constexpr int S = tile_stride(8);
+    extern __shared__ __align__(16) double gsm[];
+    const int e = blockIdx.y, lane = lane_id(), warp = threadIdx.x >> 5;
+    const int warps = blockDim.x >> 5, n = P.n;
+    const double *psw = P.W(gnn_role(e, 0, 0));
+    double *Bf = gsm;
+    double *Xs = gsm + 2 * NT2 * 32 + warp * 8 * S;
+    stage_frag(Bf, 7, 2, NT2, [&](int kk, int j) {
+        return j < H ? psw[kk * H + j] : psw[(7 + kk) * H + (j - H)];
+    });
+    __syncthreads();
+    const double *H0 = P.H[e][0];
+    for (int tile = blockIdx.x * warps + warp; tile * 8 < n; tile += gridDim.x * warps) {
+        const int v0 = tile * 8;
+        for (int i = lane; i < 64; i += 32) {
+            const int r = i >> 3, c = i & 7, v = v0 + r;
+            Xs[r * S + c] = v < n && c < 7 ? H0[(size_t)v * 7 + c] : 0.0;
+        }
+        __syncwarp();
+        double acc[NT2][2];
+        zero_acc(acc);
+        tile_mma<NT2>(Xs, S, 2, Bf, acc);
+        const int v = v0 + (lane >> 2);
+        if (v < n) {
+#pragma unroll
+            for (int nt = 0; nt < NT2; ++nt) {
+                const int col = nt * 8 + (lane & 3) * 2;
+                double *dst = col < H ? P.Pm[e][0] + (size_t)v * H + col
+                                      : P.Qm[e][0] + (size_t)v * H + (col - H);
+                *(double2 *)dst = make_double2(acc[nt][0], acc[nt][1]);
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// shared-memory doubles of gnn_node_kernel for (H, k, last), warps per block
+__host__ __device__ inline int node_smem_doubles(int H, int k, bool last, int warps) {
+    const int NT = H / 8, dk = k == 0 ? 7 : H, KT1 = (dk + H + 3) / 4;
+    int c = KT1 * NT * 32;                      // phi
+    if (!last) c += (H / 4) * 2 * NT * 32;      // next psi [Ws | Wd]
+    else c += 2 * 2 * NT * 32 + (2 * H / 4) * NT * 32 + (H / 4) * NT * 32;  // zs, zp, w1ad, w1b
+    return c + warps * 8 * tile_stride(2 * H);
+}
+
+// ---------------------------------------------------------------------------
+// Node MLPs of round k (DMMA): phi update + next projections or head tables
+// ---------------------------------------------------------------------------
+template <int H, bool BWD>
+__global__ void __launch_bounds__(256, 2) gnn_node_kernel(DevPolicy P, int k, int last) {
+    constexpr int NT = H / 8;
+    constexpr int S = tile_stride(2 * H);
+    extern __shared__ __align__(16) double gsm[];
+    const int e = blockIdx.y, lane = lane_id(), warp = threadIdx.x >> 5;
+    const int warps = blockDim.x >> 5, n = P.n;
+    const int dk = k == 0 ? 7 : H, K1 = dk + H, KT1 = (K1 + 3) / 4;
+    const double s = P.slope;
+    const bool feeds_sel = e == 0;
+    const bool feeds_plc = P.n_enc == 1 || e == 1;
+    const double *phw = P.W(gnn_role(e, k, 2)), *phb = P.W(gnn_role(e, k, 3));
+
+    double *o = gsm;
+    double *Fphi = o;
+    stage_frag(Fphi, K1, KT1, NT, [&](int kk, int j) { return phw[kk * H + j]; });
+    o += KT1 * NT * 32;
+    double *Fnext = nullptr, *Fzs = nullptr, *Fzp = nullptr, *Fw1ad = nullptr, *Fw1b = nullptr;
+    if (!last) {
+        const double *nw = P.W(gnn_role(e, k + 1, 0));
+        Fnext = o;
+        stage_frag(Fnext, H, H / 4, 2 * NT, [&](int kk, int j) {
+            return j < H ? nw[kk * H + j] : nw[(H + kk) * H + (j - H)];
+        });
+        o += (H / 4) * 2 * NT * 32;
+    } else {
+        if (feeds_sel) {
+            const double *zw = P.W(PR_SEL_Z_W);
+            Fzs = o;
+            stage_frag(Fzs, 5, 2, NT, [&](int kk, int j) { return zw[kk * H + j]; });
+        }
+        o += 2 * NT * 32;
+        if (feeds_plc) {
+            const double *zw = P.W(PR_PLC_Z_W), *w1 = P.W(PR_PLC_H1_W);
+            Fzp = o;
+            stage_frag(Fzp, 5, 2, NT, [&](int kk, int j) { return zw[kk * H + j]; });
+            Fw1ad = o + 2 * NT * 32;
+            stage_frag(Fw1ad, 2 * H, 2 * H / 4, NT, [&](int kk, int j) {
+                return kk < H ? w1[kk * H + j] : w1[(3 * H + kk - H) * H + j];
+            });
+            Fw1b = Fw1ad + (2 * H / 4) * NT * 32;
+            stage_frag(Fw1b, H, H / 4, NT, [&](int kk, int j) { return w1[(H + kk) * H + j]; });
+        }
+        o += 2 * NT * 32 + (2 * H / 4) * NT * 32 + (H / 4) * NT * 32;
+    }
+    double *Xs = o + warp * 8 * S;
+    __syncthreads();
+
+    const double *Hk = P.H[e][k];
+    const double *agg = P.AG[e][k];
+    const int r = lane >> 2, c2 = (lane & 3) * 2;
+    for (int tile = blockIdx.x * warps + warp; tile * 8 < n; tile += gridDim.x * warps) {
+        const int v0 = tile * 8;
+        const int v = v0 + r;
+        const bool vok = v < n;
+        // A tile [H_k | agg], zero-padded to KT1*4 columns
+        for (int i = lane; i < 8 * KT1 * 4; i += 32) {
+            const int rr = i / (KT1 * 4), cc = i - rr * (KT1 * 4), vv = v0 + rr;
+            double x = 0.0;
+            if (vv < n) x = cc < dk ? Hk[(size_t)vv * dk + cc] : cc < K1 ? agg[(size_t)vv * H + cc - dk] : 0.0;
+            Xs[rr * S + cc] = x;
+        }
+        __syncwarp();
+        double acc[NT][2];
+        zero_acc(acc);
+        tile_mma<NT>(Xs, S, KT1, Fphi, acc);
+        __syncwarp();
+        // U + b -> H' = leaky(U); H' becomes the next GEMM's A tile (cols 0..H-1)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            const int col = nt * 8 + c2;
+            const double u0 = acc[nt][0] + phb[col], u1 = acc[nt][1] + phb[col + 1];
+            const double h0 = gleaky(u0, s), h1 = gleaky(u1, s);
+            if (vok) {
+                *(double2 *)(P.H[e][k + 1] + (size_t)v * H + col) = make_double2(h0, h1);
+                if constexpr (BWD) *(double2 *)(P.U[e][k] + (size_t)v * H + col) = make_double2(u0, u1);
+            }
+            Xs[r * S + col] = h0;
+            Xs[r * S + col + 1] = h1;
+        }
+        __syncwarp();
+        if (!last) {
+            double pq[2 * NT][2];
+            zero_acc(pq);
+            tile_mma<2 * NT>(Xs, S, H / 4, Fnext, pq);
+            if (vok) {
+#pragma unroll
+                for (int nt = 0; nt < 2 * NT; ++nt) {
+                    const int col = nt * 8 + c2;
+                    double *dst = col < H ? P.Pm[e][k + 1] + (size_t)v * H + col
+                                          : P.Qm[e][k + 1] + (size_t)v * H + (col - H);
+                    *(double2 *)dst = make_double2(pq[nt][0], pq[nt][1]);
+                }
+            }
+            __syncwarp();
+            continue;
+        }
+        // ---- last round: head tables.  x (5 static features) at cols H..H+7 ----
+        {
+            const int rr = lane >> 2, cc = (lane & 3) * 2, vv = v0 + rr;
+            Xs[rr * S + H + cc] = vv < n && cc < 5 ? P.x[(size_t)vv * 5 + cc] : 0.0;
+            Xs[rr * S + H + cc + 1] = vv < n && cc + 1 < 5 ? P.x[(size_t)vv * 5 + cc + 1] : 0.0;
+        }
+        __syncwarp();
+        if (feeds_sel) {
+            const double *zb = P.W(PR_SEL_Z_B);
+            double z[NT][2];
+            zero_acc(z);
+            tile_mma<NT>(Xs + H, S, 2, Fzs, z);
+            if (vok)
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) {
+                    const int col = nt * 8 + c2;
+                    *(double2 *)(P.Zs + (size_t)v * H + col) =
+                        make_double2(z[nt][0] + zb[col], z[nt][1] + zb[col + 1]);
+                }
+        }
+        if (feeds_plc) {
+            const double *zb = P.W(PR_PLC_Z_B);
+            double z[NT][2];
+            zero_acc(z);
+            tile_mma<NT>(Xs + H, S, 2, Fzp, z);
+            __syncwarp();  // x consumed before z overwrites cols H..2H-1
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+                const int col = nt * 8 + c2;
+                const double z0 = z[nt][0] + zb[col], z1 = z[nt][1] + zb[col + 1];
+                if constexpr (BWD)
+                    if (vok) *(double2 *)(P.Zp + (size_t)v * H + col) = make_double2(z0, z1);
+                Xs[r * S + H + col] = z0;
+                Xs[r * S + H + col + 1] = z1;
+            }
+            __syncwarp();
+            double a[NT][2], g[NT][2];
+            zero_acc(a);
+            zero_acc(g);
+            tile_mma<NT>(Xs, S, 2 * H / 4, Fw1ad, a);
+            tile_mma<NT>(Xs, S, H / 4, Fw1b, g);
+            if (vok)
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) {
+                    const int col = nt * 8 + c2;
+                    *(double2 *)(P.A + (size_t)v * H + col) = make_double2(a[nt][0], a[nt][1]);
+                    *(double2 *)(P.G + (size_t)v * H + col) = make_double2(g[nt][0], g[nt][1]);
+                }
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// SEL head (DMMA): s[v] = leaky([H | Sb | St | Zs] @ head1.w + b1) . head2.w + b2
+// ---------------------------------------------------------------------------
+__host__ __device__ inline int sel_smem_doubles(int H, int warps) {
+    return (4 * H / 4) * (H / 8) * 32 + warps * 8 * tile_stride(4 * H);
+}
+
+template <int H, bool BWD>
+__global__ void __launch_bounds__(256, 2) gnn_sel_kernel(DevPolicy P) {
+    constexpr int NT = H / 8;
+    constexpr int S = tile_stride(4 * H);
+    extern __shared__ __align__(16) double gsm[];
+    const int lane = lane_id(), warp = threadIdx.x >> 5;
+    const int warps = blockDim.x >> 5, n = P.n;
+    const double s = P.slope;
+    if (blockIdx.x == 0 && warp == 0) {
+        // M = Wy @ W1c (5 x h), c = by @ W1c + b1  (PLC, policy.py:218-222)
+        const double *yw = P.W(PR_PLC_Y_W), *yb = P.W(PR_PLC_Y_B), *w1 = P.W(PR_PLC_H1_W),
+                     *b1 = P.W(PR_PLC_H1_B);
+        for (int j = lane; j < H; j += 32) {
+            for (int rr = 0; rr < 5; ++rr) {
+                double acc = 0.0;
+                for (int i = 0; i < H; ++i) acc = fma(yw[rr * H + i], w1[(2 * H + i) * H + j], acc);
+                P.M[rr * H + j] = acc;
+            }
+            double acc = 0.0;
+            for (int i = 0; i < H; ++i) acc = fma(yb[i], w1[(2 * H + i) * H + j], acc);
+            P.c[j] = acc + b1[j];
+        }
+    }
+    const double *w1 = P.W(PR_SEL_H1_W), *b1 = P.W(PR_SEL_H1_B), *w2 = P.W(PR_SEL_H2_W),
+                 *b2 = P.W(PR_SEL_H2_B);
+    double *Fw = gsm;
+    stage_frag(Fw, 4 * H, H, NT, [&](int kk, int j) { return w1[kk * H + j]; });
+    double *Xs = gsm + H * NT * 32 + warp * 8 * S;
+    __syncthreads();
+    const double *Hs = P.H[0][P.K];
+    const int rb = P.jump_rounds;
+    const double *Sb = P.forest && rb > 0 ? P.PS[0][(rb - 1) & 1] : Hs;
+    const double *St = P.forest && rb > 0 ? P.PS[1][(rb - 1) & 1] : Hs;
+    const int r = lane >> 2, c2 = (lane & 3) * 2;
+    for (int tile = blockIdx.x * warps + warp; tile * 8 < n; tile += gridDim.x * warps) {
+        const int v0 = tile * 8;
+        for (int i = lane; i < 8 * 4 * H; i += 32) {
+            const int rr = i / (4 * H), cc = i - rr * 4 * H, vv = v0 + rr;
+            const int b = cc / H, j = cc - b * H;
+            double x = 0.0;
+            if (vv < n) {
+                if (b == 0) x = Hs[(size_t)vv * H + j];
+                else if (b == 3) x = P.Zs[(size_t)vv * H + j];
+                else if (P.forest) x = (b == 1 ? Sb : St)[(size_t)vv * H + j];
+                else {
+                    const int *pp = b == 1 ? P.bp_ptr : P.tp_ptr;
+                    const int *pi = b == 1 ? P.bp_idx : P.tp_idx;
+                    for (int q = pp[vv]; q < pp[vv + 1]; ++q) x += Hs[(size_t)pi[q] * H + j];
+                }
+                if constexpr (BWD) P.emb[(size_t)vv * 4 * H + cc] = x;
+            }
+            Xs[rr * S + cc] = x;
+        }
+        __syncwarp();
+        double acc[NT][2];
+        zero_acc(acc);
+        tile_mma<NT>(Xs, S, H, Fw, acc);
+        const int v = v0 + r;
+        double part = 0.0;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int col = nt * 8 + c2 + i;
+                const double pre = acc[nt][i] + b1[col];
+                if constexpr (BWD)
+                    if (v < n) P.hidpre[(size_t)v * H + col] = pre;
+                part = fma(gleaky(pre, s), w2[col], part);
+            }
+        part += __shfl_xor_sync(FP_FULL_MASK, part, 1);
+        part += __shfl_xor_sync(FP_FULL_MASK, part, 2);
+        if ((lane & 3) == 0 && v < n) P.s[v] = part + b2[0];
+        __syncwarp();
+    }
+}
+
+}  // namespace fp

@@ -86,5 +86,6 @@ struct fp_policy {
     void *arena = nullptr;
     const fp_problem *problem = nullptr;
     fp_train_state *train = nullptr;  // backward job lists (fp_train.cu)
+    int fused_encoder = 0;            // 1: single fused per-vertex kernel (reference order)
     int64_t n_params = 0;
 };

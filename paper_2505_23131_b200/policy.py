@@ -251,6 +251,12 @@ class PolicyContext:
             self._lib.fp_policy_destroy(h)
             self.handle = None
 
+    def set_encoder(self, fused: bool):
+        """Select the fused per-vertex encoder (reference FMA order) instead of
+        the default aggregation + DMMA node-MLP kernels."""
+        N.check(N.lib().fp_policy_set_encoder(self.handle, ctypes.c_int32(int(fused))))
+        self._prepared_key = None
+
     def flat_params(self, params) -> "object":
         """Upload a params dict (or pass through a flat CUDA tensor)."""
         import torch

@@ -273,3 +273,29 @@ def test_forest_path_sums_match_path_lists(torch_cuda):
         b.prepare(params)
         np.testing.assert_allclose(b.read_table("sel_logit"), a.read_table("sel_logit"),
                                    rtol=1e-11, atol=1e-12)
+
+
+@pytest.mark.parametrize("which", ["ffnn", "chainmm_h16", "fixture_h8"])
+def test_dmma_encoder_matches_fused_encoder(which, torch_cuda):
+    """The split encoder (aggregation + fp64 tensor-core node MLPs) against the
+    fused CUDA-core encoder that keeps the reference's FMA order: every
+    head table within 1e-12 relative."""
+    from helpers import fixture6
+    if which == "ffnn":
+        g, cl, pc = builders.build_ffnn(8, 4, 16, 4, 2), ClusterSpec.uniform(8, 1e6, 1e5), \
+            PolicyConfig()
+    elif which == "chainmm_h16":
+        g, cl, pc = builders.build_chainmm(64, 2), ClusterSpec.uniform(4, 1e6, 1e5), \
+            PolicyConfig(hidden=16, k_rounds=3, shared_encoder=True)
+    else:
+        g, cl, pc = fixture6(), ClusterSpec.uniform(2, 1000.0, 256.0), PolicyConfig(hidden=8)
+    params = init_policy_params(pc, seed=9)
+    a = PolicyContext(g, cl, pc)
+    b = PolicyContext(g, cl, pc)
+    b.set_encoder(fused=True)
+    a.prepare(params)
+    b.prepare(params)
+    for name in ("H_sel", "H_plc", "sel_logit", "A", "G", "M", "c"):
+        x, y = a.read_table(name), b.read_table(name)
+        np.testing.assert_allclose(x, y, rtol=1e-12, atol=1e-13 * max(1.0, np.abs(y).max()),
+                                   err_msg=f"{which}:{name}")
