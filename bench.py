@@ -267,6 +267,13 @@ def run_ours(args):
         if train:
             alg += B * n * 4 * h * 8  # REINFORCE rows written
         achieved = alg / (kms * 1e-3) / 1e9
+        traffic = None
+        tpath = ROOT / "profiles" / "r1_traffic.json"
+        if tpath.exists():
+            rec = json.loads(tpath.read_text()).get(
+                f"{args.workload}/rollout_kernel{'(grad)' if train else ''}")
+            if rec and rec.get("batch") == B:
+                traffic = rec["dram_bytes_read"] + rec["dram_bytes_write"]
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -283,7 +290,7 @@ def run_ours(args):
                                           trainer.launches_per_step()),
             "roofline": {"bound": "hbm", "kernel": "rollout_kernel" if not train else
                          "rollout_kernel(grad)", "achieved": achieved, "peak": peak,
-                         "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "kernel_ms": kms, "alg_bytes_per_launch": alg,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
         }

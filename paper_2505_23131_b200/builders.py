@@ -254,3 +254,18 @@ def sparse_dag(n: int, seed: int = 0, window: int = 64) -> DataflowGraph:
             edges.append((int(u), v))
         verts.append(Vertex(v, OpKind.OTHER, int(rng.integers(1 << 20, 1 << 30)), nbytes, f"op{v}"))
     return DataflowGraph(tuple(verts), tuple(edges))
+
+
+def relabel(graph: DataflowGraph, seed: int = 0) -> DataflowGraph:
+    """The same DAG under a random permutation of vertex ids -- destroys the
+    id locality of ``sparse_dag`` (predecessors within a 64-id window), so
+    per-message gathers of neighbour rows become random HBM accesses."""
+    import dataclasses
+
+    n = len(graph)
+    perm = np.random.default_rng(seed).permutation(n)
+    verts = [None] * n
+    for v, x in enumerate(graph.vertices):
+        verts[int(perm[v])] = dataclasses.replace(x, id=int(perm[v]))
+    edges = tuple((int(perm[a]), int(perm[b])) for a, b in graph.edges)
+    return DataflowGraph(tuple(verts), edges)

@@ -495,7 +495,7 @@ static int launch_gnn_tc(DevPolicy &P, cudaStream_t st) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int warps = H <= 32 ? 8 : 4, threads = warps * 32;
+    const int warps = 8, threads = warps * 32;
     const int tiles = (P.n + 7) / 8;
     const int tile_blocks = (tiles + warps - 1) / warps;
     auto grid_for = [&](const void *kern, int64_t smem, int want) {
@@ -511,7 +511,7 @@ static int launch_gnn_tc(DevPolicy &P, cudaStream_t st) {
         return cudaSuccess;
     };
     {
-        const int64_t smem = 8LL * (2 * (2 * H / 8) * 32 + warps * 8 * tile_stride(8));
+        const int64_t smem = 8LL * (2 * (2 * H / 8) * 32);
         const void *kern = (const void *)gnn_proj0_kernel<H>;
         FP_CUDA_RET(set_smem(kern, smem));
         gnn_proj0_kernel<H><<<dim3(grid_for(kern, smem, tile_blocks), P.n_enc), threads, smem, st>>>(P);
@@ -526,11 +526,15 @@ static int launch_gnn_tc(DevPolicy &P, cudaStream_t st) {
             gnn_agg_kernel<H><<<dim3(grid_for(kern, 0, agg_blocks), P.n_enc), 256, 0, st>>>(P, k);
             FP_CUDA_RET(cudaGetLastError());
         }
-        const int64_t smem = 8LL * node_smem_doubles(H, k, last, warps);
-        const void *kern = (const void *)gnn_node_kernel<H, BWD>;
+        const int64_t smem = 8LL * node_smem_doubles(H, k, last);
+        const void *kern = k == 0 ? (const void *)gnn_node_kernel<H, true, BWD>
+                                  : (const void *)gnn_node_kernel<H, false, BWD>;
         FP_CUDA_RET(set_smem(kern, smem));
-        gnn_node_kernel<H, BWD><<<dim3(grid_for(kern, smem, tile_blocks), P.n_enc), threads, smem,
-                                  st>>>(P, k, last);
+        const dim3 grid(grid_for(kern, smem, tile_blocks), P.n_enc);
+        if (k == 0)
+            gnn_node_kernel<H, true, BWD><<<grid, threads, smem, st>>>(P, k, last);
+        else
+            gnn_node_kernel<H, false, BWD><<<grid, threads, smem, st>>>(P, k, last);
         FP_CUDA_RET(cudaGetLastError());
     }
     if (P.forest)
@@ -541,7 +545,7 @@ static int launch_gnn_tc(DevPolicy &P, cudaStream_t st) {
             FP_CUDA_RET(cudaGetLastError());
         }
     {
-        const int64_t smem = 8LL * sel_smem_doubles(H, warps);
+        const int64_t smem = 8LL * sel_smem_doubles(H);
         const void *kern = (const void *)gnn_sel_kernel<H, BWD>;
         FP_CUDA_RET(set_smem(kern, smem));
         int occ = 1;

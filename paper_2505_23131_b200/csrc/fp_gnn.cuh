@@ -134,62 +134,78 @@ __global__ void __launch_bounds__(256) gnn_agg_kernel(DevPolicy P, int k) {
 template <int H>
 __global__ void __launch_bounds__(256) gnn_proj0_kernel(DevPolicy P) {
     constexpr int NT2 = 2 * H / 8;
-    constexpr int S = tile_stride(8);
     extern __shared__ __align__(16) double gsm[];
     const int e = blockIdx.y, lane = lane_id(), warp = threadIdx.x >> 5;
     const int warps = blockDim.x >> 5, n = P.n;
     const double *psw = P.W(gnn_role(e, 0, 0));
     double *Bf = gsm;
-    double *Xs = gsm + 2 * NT2 * 32 + warp * 8 * S;
     stage_frag(Bf, 7, 2, NT2, [&](int kk, int j) {
         return j < H ? psw[kk * H + j] : psw[(7 + kk) * H + (j - H)];
     });
     __syncthreads();
     const double *H0 = P.H[e][0];
+    const int r = lane >> 2, c = lane & 3;
     for (int tile = blockIdx.x * warps + warp; tile * 8 < n; tile += gridDim.x * warps) {
-        const int v0 = tile * 8;
-        for (int i = lane; i < 64; i += 32) {
-            const int r = i >> 3, c = i & 7, v = v0 + r;
-            Xs[r * S + c] = v < n && c < 7 ? H0[(size_t)v * 7 + c] : 0.0;
-        }
-        __syncwarp();
+        const int v = tile * 8 + r;
         double acc[NT2][2];
         zero_acc(acc);
-        tile_mma<NT2>(Xs, S, 2, Bf, acc);
-        const int v = v0 + (lane >> 2);
+#pragma unroll
+        for (int kt = 0; kt < 2; ++kt) {
+            const int col = kt * 4 + c;
+            const double a = v < n && col < 7 ? H0[(size_t)v * 7 + col] : 0.0;
+#pragma unroll
+            for (int nt = 0; nt < NT2; ++nt) dmma(acc[nt], a, Bf[(kt * NT2 + nt) * 32 + lane]);
+        }
         if (v < n) {
 #pragma unroll
             for (int nt = 0; nt < NT2; ++nt) {
-                const int col = nt * 8 + (lane & 3) * 2;
+                const int col = nt * 8 + c * 2;
                 double *dst = col < H ? P.Pm[e][0] + (size_t)v * H + col
                                       : P.Qm[e][0] + (size_t)v * H + (col - H);
                 *(double2 *)dst = make_double2(acc[nt][0], acc[nt][1]);
             }
         }
-        __syncwarp();
     }
 }
 
-// shared-memory doubles of gnn_node_kernel for (H, k, last), warps per block
-__host__ __device__ inline int node_smem_doubles(int H, int k, bool last, int warps) {
+// A fragment of k-step kt taken from a D fragment held in registers (the
+// previous GEMM's output, columns 8nt + 2c' + i on lane 4r + c'): lane (r, c)
+// needs column 4kt + c, which lives on lane 4r + 2(kt&1) + c/2 as element c&1
+// of n-tile kt/2.  Two shuffles per k-step; kt must be a compile-time index.
+template <int NT>
+__device__ __forceinline__ double d_to_a(const double (&acc)[NT][2], int kt) {
+    const int lane = lane_id();
+    const int src = (lane & ~3) + 2 * (kt & 1) + ((lane & 3) >> 1);
+    const double x0 = __shfl_sync(FP_FULL_MASK, acc[kt >> 1][0], src);
+    const double x1 = __shfl_sync(FP_FULL_MASK, acc[kt >> 1][1], src);
+    return (lane & 1) ? x1 : x0;
+}
+
+// shared-memory doubles (weight fragments) of gnn_node_kernel for (H, k, last)
+__host__ __device__ inline int node_smem_doubles(int H, int k, bool last) {
     const int NT = H / 8, dk = k == 0 ? 7 : H, KT1 = (dk + H + 3) / 4;
     int c = KT1 * NT * 32;                      // phi
     if (!last) c += (H / 4) * 2 * NT * 32;      // next psi [Ws | Wd]
     else c += 2 * 2 * NT * 32 + (2 * H / 4) * NT * 32 + (H / 4) * NT * 32;  // zs, zp, w1ad, w1b
-    return c + warps * 8 * tile_stride(2 * H);
+    return c;
 }
 
 // ---------------------------------------------------------------------------
-// Node MLPs of round k (DMMA): phi update + next projections or head tables
+// Node MLPs of round k (DMMA): phi update + next projections or head tables.
+// A operands come straight from global memory into fragment registers (each
+// k-step is one 32-byte sector per vertex row) or, for the chained GEMMs,
+// from the previous GEMM's accumulators by shuffles -- no shared-memory
+// staging of activations, so the only shared memory is the weights.
 // ---------------------------------------------------------------------------
-template <int H, bool BWD>
+template <int H, bool K0, bool BWD>
 __global__ void __launch_bounds__(256, 2) gnn_node_kernel(DevPolicy P, int k, int last) {
     constexpr int NT = H / 8;
-    constexpr int S = tile_stride(2 * H);
+    constexpr int DK = K0 ? 7 : H;
+    constexpr int K1 = DK + H;
+    constexpr int KT1 = (K1 + 3) / 4;
     extern __shared__ __align__(16) double gsm[];
     const int e = blockIdx.y, lane = lane_id(), warp = threadIdx.x >> 5;
     const int warps = blockDim.x >> 5, n = P.n;
-    const int dk = k == 0 ? 7 : H, K1 = dk + H, KT1 = (K1 + 3) / 4;
     const double s = P.slope;
     const bool feeds_sel = e == 0;
     const bool feeds_plc = P.n_enc == 1 || e == 1;
@@ -206,7 +222,6 @@ __global__ void __launch_bounds__(256, 2) gnn_node_kernel(DevPolicy P, int k, in
         stage_frag(Fnext, H, H / 4, 2 * NT, [&](int kk, int j) {
             return j < H ? nw[kk * H + j] : nw[(H + kk) * H + (j - H)];
         });
-        o += (H / 4) * 2 * NT * 32;
     } else {
         if (feeds_sel) {
             const double *zw = P.W(PR_SEL_Z_W);
@@ -225,48 +240,54 @@ __global__ void __launch_bounds__(256, 2) gnn_node_kernel(DevPolicy P, int k, in
             Fw1b = Fw1ad + (2 * H / 4) * NT * 32;
             stage_frag(Fw1b, H, H / 4, NT, [&](int kk, int j) { return w1[(H + kk) * H + j]; });
         }
-        o += 2 * NT * 32 + (2 * H / 4) * NT * 32 + (H / 4) * NT * 32;
     }
-    double *Xs = o + warp * 8 * S;
     __syncthreads();
 
     const double *Hk = P.H[e][k];
     const double *agg = P.AG[e][k];
-    const int r = lane >> 2, c2 = (lane & 3) * 2;
+    const int r = lane >> 2, c = lane & 3, c2 = c * 2;
     for (int tile = blockIdx.x * warps + warp; tile * 8 < n; tile += gridDim.x * warps) {
-        const int v0 = tile * 8;
-        const int v = v0 + r;
+        const int v = tile * 8 + r;
         const bool vok = v < n;
-        // A tile [H_k | agg], zero-padded to KT1*4 columns
-        for (int i = lane; i < 8 * KT1 * 4; i += 32) {
-            const int rr = i / (KT1 * 4), cc = i - rr * (KT1 * 4), vv = v0 + rr;
+        // ---- phi: A = [H_k | agg] (8 x K1) from global, fragments in registers ----
+        double a1[KT1];
+#pragma unroll
+        for (int kt = 0; kt < KT1; ++kt) {
+            const int col = kt * 4 + c;
             double x = 0.0;
-            if (vv < n) x = cc < dk ? Hk[(size_t)vv * dk + cc] : cc < K1 ? agg[(size_t)vv * H + cc - dk] : 0.0;
-            Xs[rr * S + cc] = x;
+            if (vok) {
+                if (col < DK) x = Hk[(size_t)v * DK + col];
+                else if (col < K1) x = agg[(size_t)v * H + col - DK];
+            }
+            a1[kt] = x;
         }
-        __syncwarp();
         double acc[NT][2];
         zero_acc(acc);
-        tile_mma<NT>(Xs, S, KT1, Fphi, acc);
-        __syncwarp();
-        // U + b -> H' = leaky(U); H' becomes the next GEMM's A tile (cols 0..H-1)
+#pragma unroll
+        for (int kt = 0; kt < KT1; ++kt)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) dmma(acc[nt], a1[kt], Fphi[(kt * NT + nt) * 32 + lane]);
+        // U + b -> H' = leaky(U), kept in the D fragment for the chained GEMMs
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
             const int col = nt * 8 + c2;
             const double u0 = acc[nt][0] + phb[col], u1 = acc[nt][1] + phb[col + 1];
-            const double h0 = gleaky(u0, s), h1 = gleaky(u1, s);
+            acc[nt][0] = gleaky(u0, s);
+            acc[nt][1] = gleaky(u1, s);
             if (vok) {
-                *(double2 *)(P.H[e][k + 1] + (size_t)v * H + col) = make_double2(h0, h1);
+                *(double2 *)(P.H[e][k + 1] + (size_t)v * H + col) = make_double2(acc[nt][0], acc[nt][1]);
                 if constexpr (BWD) *(double2 *)(P.U[e][k] + (size_t)v * H + col) = make_double2(u0, u1);
             }
-            Xs[r * S + col] = h0;
-            Xs[r * S + col + 1] = h1;
         }
-        __syncwarp();
         if (!last) {
             double pq[2 * NT][2];
             zero_acc(pq);
-            tile_mma<2 * NT>(Xs, S, H / 4, Fnext, pq);
+#pragma unroll
+            for (int kt = 0; kt < H / 4; ++kt) {
+                const double a = d_to_a<NT>(acc, kt);
+#pragma unroll
+                for (int nt = 0; nt < 2 * NT; ++nt) dmma(pq[nt], a, Fnext[(kt * 2 * NT + nt) * 32 + lane]);
+            }
             if (vok) {
 #pragma unroll
                 for (int nt = 0; nt < 2 * NT; ++nt) {
@@ -276,21 +297,23 @@ __global__ void __launch_bounds__(256, 2) gnn_node_kernel(DevPolicy P, int k, in
                     *(double2 *)dst = make_double2(pq[nt][0], pq[nt][1]);
                 }
             }
-            __syncwarp();
             continue;
         }
-        // ---- last round: head tables.  x (5 static features) at cols H..H+7 ----
-        {
-            const int rr = lane >> 2, cc = (lane & 3) * 2, vv = v0 + rr;
-            Xs[rr * S + H + cc] = vv < n && cc < 5 ? P.x[(size_t)vv * 5 + cc] : 0.0;
-            Xs[rr * S + H + cc + 1] = vv < n && cc + 1 < 5 ? P.x[(size_t)vv * 5 + cc + 1] : 0.0;
+        // ---- last round: head tables; x = the 5 static features (K padded to 8) ----
+        double ax[2];
+#pragma unroll
+        for (int kt = 0; kt < 2; ++kt) {
+            const int col = kt * 4 + c;
+            ax[kt] = vok && col < 5 ? P.x[(size_t)v * 5 + col] : 0.0;
         }
-        __syncwarp();
         if (feeds_sel) {
             const double *zb = P.W(PR_SEL_Z_B);
             double z[NT][2];
             zero_acc(z);
-            tile_mma<NT>(Xs + H, S, 2, Fzs, z);
+#pragma unroll
+            for (int kt = 0; kt < 2; ++kt)
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) dmma(z[nt], ax[kt], Fzs[(kt * NT + nt) * 32 + lane]);
             if (vok)
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt) {
@@ -303,23 +326,38 @@ __global__ void __launch_bounds__(256, 2) gnn_node_kernel(DevPolicy P, int k, in
             const double *zb = P.W(PR_PLC_Z_B);
             double z[NT][2];
             zero_acc(z);
-            tile_mma<NT>(Xs + H, S, 2, Fzp, z);
-            __syncwarp();  // x consumed before z overwrites cols H..2H-1
+#pragma unroll
+            for (int kt = 0; kt < 2; ++kt)
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) dmma(z[nt], ax[kt], Fzp[(kt * NT + nt) * 32 + lane]);
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) {
                 const int col = nt * 8 + c2;
-                const double z0 = z[nt][0] + zb[col], z1 = z[nt][1] + zb[col + 1];
+                z[nt][0] += zb[col];
+                z[nt][1] += zb[col + 1];
                 if constexpr (BWD)
-                    if (vok) *(double2 *)(P.Zp + (size_t)v * H + col) = make_double2(z0, z1);
-                Xs[r * S + H + col] = z0;
-                Xs[r * S + H + col + 1] = z1;
+                    if (vok) *(double2 *)(P.Zp + (size_t)v * H + col) = make_double2(z[nt][0], z[nt][1]);
             }
-            __syncwarp();
+            // A = [H' | z] @ [W1a; W1d], G = H' @ W1b
             double a[NT][2], g[NT][2];
             zero_acc(a);
             zero_acc(g);
-            tile_mma<NT>(Xs, S, 2 * H / 4, Fw1ad, a);
-            tile_mma<NT>(Xs, S, H / 4, Fw1b, g);
+#pragma unroll
+            for (int kt = 0; kt < H / 4; ++kt) {
+                const double ah = d_to_a<NT>(acc, kt);
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) {
+                    dmma(a[nt], ah, Fw1ad[(kt * NT + nt) * 32 + lane]);
+                    dmma(g[nt], ah, Fw1b[(kt * NT + nt) * 32 + lane]);
+                }
+            }
+#pragma unroll
+            for (int kt = 0; kt < H / 4; ++kt) {
+                const double az = d_to_a<NT>(z, kt);
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt)
+                    dmma(a[nt], az, Fw1ad[((H / 4 + kt) * NT + nt) * 32 + lane]);
+            }
             if (vok)
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt) {
@@ -328,21 +366,20 @@ __global__ void __launch_bounds__(256, 2) gnn_node_kernel(DevPolicy P, int k, in
                     *(double2 *)(P.G + (size_t)v * H + col) = make_double2(g[nt][0], g[nt][1]);
                 }
         }
-        __syncwarp();
     }
 }
 
 // ---------------------------------------------------------------------------
 // SEL head (DMMA): s[v] = leaky([H | Sb | St | Zs] @ head1.w + b1) . head2.w + b2
+// A fragments straight from global (path sums from the pointer-jumping
+// buffers, or summed along the explicit path lists for compact graphs).
 // ---------------------------------------------------------------------------
-__host__ __device__ inline int sel_smem_doubles(int H, int warps) {
-    return (4 * H / 4) * (H / 8) * 32 + warps * 8 * tile_stride(4 * H);
-}
+__host__ __device__ inline int sel_smem_doubles(int H) { return (4 * H / 4) * (H / 8) * 32; }
 
 template <int H, bool BWD>
 __global__ void __launch_bounds__(256, 2) gnn_sel_kernel(DevPolicy P) {
     constexpr int NT = H / 8;
-    constexpr int S = tile_stride(4 * H);
+    constexpr int KT = H;  // K = 4H
     extern __shared__ __align__(16) double gsm[];
     const int lane = lane_id(), warp = threadIdx.x >> 5;
     const int warps = blockDim.x >> 5, n = P.n;
@@ -365,38 +402,36 @@ __global__ void __launch_bounds__(256, 2) gnn_sel_kernel(DevPolicy P) {
     const double *w1 = P.W(PR_SEL_H1_W), *b1 = P.W(PR_SEL_H1_B), *w2 = P.W(PR_SEL_H2_W),
                  *b2 = P.W(PR_SEL_H2_B);
     double *Fw = gsm;
-    stage_frag(Fw, 4 * H, H, NT, [&](int kk, int j) { return w1[kk * H + j]; });
-    double *Xs = gsm + H * NT * 32 + warp * 8 * S;
+    stage_frag(Fw, 4 * H, KT, NT, [&](int kk, int j) { return w1[kk * H + j]; });
     __syncthreads();
     const double *Hs = P.H[0][P.K];
     const int rb = P.jump_rounds;
     const double *Sb = P.forest && rb > 0 ? P.PS[0][(rb - 1) & 1] : Hs;
     const double *St = P.forest && rb > 0 ? P.PS[1][(rb - 1) & 1] : Hs;
-    const int r = lane >> 2, c2 = (lane & 3) * 2;
+    const int r = lane >> 2, c = lane & 3, c2 = c * 2;
     for (int tile = blockIdx.x * warps + warp; tile * 8 < n; tile += gridDim.x * warps) {
-        const int v0 = tile * 8;
-        for (int i = lane; i < 8 * 4 * H; i += 32) {
-            const int rr = i / (4 * H), cc = i - rr * 4 * H, vv = v0 + rr;
-            const int b = cc / H, j = cc - b * H;
+        const int v = tile * 8 + r;
+        const bool vok = v < n;
+        double acc[NT][2];
+        zero_acc(acc);
+#pragma unroll 8
+        for (int kt = 0; kt < KT; ++kt) {
+            const int cc = kt * 4 + c, b = cc / H, j = cc - b * H;
             double x = 0.0;
-            if (vv < n) {
-                if (b == 0) x = Hs[(size_t)vv * H + j];
-                else if (b == 3) x = P.Zs[(size_t)vv * H + j];
-                else if (P.forest) x = (b == 1 ? Sb : St)[(size_t)vv * H + j];
+            if (vok) {
+                if (b == 0) x = Hs[(size_t)v * H + j];
+                else if (b == 3) x = P.Zs[(size_t)v * H + j];
+                else if (P.forest) x = (b == 1 ? Sb : St)[(size_t)v * H + j];
                 else {
                     const int *pp = b == 1 ? P.bp_ptr : P.tp_ptr;
                     const int *pi = b == 1 ? P.bp_idx : P.tp_idx;
-                    for (int q = pp[vv]; q < pp[vv + 1]; ++q) x += Hs[(size_t)pi[q] * H + j];
+                    for (int q = pp[v]; q < pp[v + 1]; ++q) x += Hs[(size_t)pi[q] * H + j];
                 }
-                if constexpr (BWD) P.emb[(size_t)vv * 4 * H + cc] = x;
+                if constexpr (BWD) P.emb[(size_t)v * 4 * H + cc] = x;
             }
-            Xs[rr * S + cc] = x;
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) dmma(acc[nt], x, Fw[(kt * NT + nt) * 32 + lane]);
         }
-        __syncwarp();
-        double acc[NT][2];
-        zero_acc(acc);
-        tile_mma<NT>(Xs, S, H, Fw, acc);
-        const int v = v0 + r;
         double part = 0.0;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
@@ -405,13 +440,12 @@ __global__ void __launch_bounds__(256, 2) gnn_sel_kernel(DevPolicy P) {
                 const int col = nt * 8 + c2 + i;
                 const double pre = acc[nt][i] + b1[col];
                 if constexpr (BWD)
-                    if (v < n) P.hidpre[(size_t)v * H + col] = pre;
+                    if (vok) P.hidpre[(size_t)v * H + col] = pre;
                 part = fma(gleaky(pre, s), w2[col], part);
             }
         part += __shfl_xor_sync(FP_FULL_MASK, part, 1);
         part += __shfl_xor_sync(FP_FULL_MASK, part, 2);
-        if ((lane & 3) == 0 && v < n) P.s[v] = part + b2[0];
-        __syncwarp();
+        if (c == 0 && vok) P.s[v] = part + b2[0];
     }
 }
 

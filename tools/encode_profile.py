@@ -21,9 +21,12 @@ from paper_2505_23131_b200.policy import PolicyConfig, PolicyContext  # noqa: E4
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=1000000)
 ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--shuffle", action="store_true", help="random vertex ids (no gather locality)")
 a = ap.parse_args()
 t0 = time.perf_counter()
 g = builders.sparse_dag(a.n, seed=0)
+if a.shuffle:
+    g = builders.relabel(g, seed=1)
 cl = ClusterSpec.uniform(8, rate=1e9, bandwidth=1e7)
 pc = PolicyConfig()
 ctx = PolicyContext(g, cl, pc)
@@ -39,5 +42,5 @@ for _ in range(a.reps):
     ev[1].record()
     torch.cuda.synchronize()
     ms.append(ev[0].elapsed_time(ev[1]))
-print(json.dumps({"n": a.n, "edges": len(g.edges), "prepare_ms_min": min(ms),
+print(json.dumps({"n": a.n, "edges": len(g.edges), "shuffle": a.shuffle, "prepare_ms_min": min(ms),
                   "prepare_ms": ms, "host_setup_s": setup}))
