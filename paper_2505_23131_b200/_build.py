@@ -55,15 +55,23 @@ def build(force: bool = False, verbose: bool = False, profile: bool = False) -> 
         flags += ["-Xptxas", "-v"]
     if profile:
         flags += ["-DFP_PHASE_PROFILE"]
+    # one nvcc per translation unit, all in parallel
+    procs = []
     for src in sources():
         obj = objdir / (src.stem + ".o")
         cmd = [nvcc(), "-c", str(src), "-o", str(obj)] + flags
-        r = subprocess.run(cmd, capture_output=True, text=True)
-        if r.returncode != 0:
-            raise RuntimeError(f"nvcc failed for {src.name}:\n{r.stderr}")
-        if verbose and r.stderr:
-            print(r.stderr, file=sys.stderr)
+        procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                                            text=True)))
         objs.append(str(obj))
+    failed = []
+    for src, pr in procs:
+        _, err = pr.communicate()
+        if pr.returncode != 0:
+            failed.append(f"nvcc failed for {src.name}:\n{err}")
+        elif verbose and err:
+            print(err, file=sys.stderr)
+    if failed:
+        raise RuntimeError("\n".join(failed))
     tmp = lib.with_suffix(".so.tmp")
     cmd = [nvcc(), "-shared", "-o", str(tmp)] + [str(o) for o in objs] + ARCH + [
         "-Xcompiler", "-fPIC"]

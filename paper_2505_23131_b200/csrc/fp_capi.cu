@@ -45,7 +45,7 @@ struct Arena {
 // warp's shared-memory slice, one wave.  Wide path (state beyond shared
 // memory): a persistent grid, each resident warp owning one HBM workspace
 // slice of L.gbytes and looping over episodes.
-template <int RPL, int WARPS, bool WIDE>
+template <int RPL, int WARPS, bool WIDE, bool SM1>
 __global__ void __launch_bounds__(WARPS * 32)
 sim_batch_kernel(DevProblem P, EpLayout L, const int32_t *__restrict__ assign, int B,
                  int strategy, const double *__restrict__ jit, long long jit_stride,
@@ -62,7 +62,7 @@ sim_batch_kernel(DevProblem P, EpLayout L, const int32_t *__restrict__ assign, i
         const int32_t *row = assign + (size_t)ep * P.n;
         for (int v = lane_id(); v < P.n; v += 32) as[v] = (uint8_t)row[v];
         __syncwarp();
-        SimOut o = sim_episode<RPL, WIDE>(P, nb, sb, L, strategy,
+        SimOut o = sim_episode<RPL, WIDE, SM1>(P, nb, sb, L, strategy,
                                           jit ? jit + (size_t)ep * jit_stride : nullptr,
                                           trace ? trace + (size_t)ep * trace_cap : nullptr,
                                           trace_cap, blocked ? blocked + (size_t)ep * P.n : nullptr);
@@ -108,8 +108,11 @@ static int launch_sim_t(const fp_problem *p, const int32_t *assign, int B, int s
         set_error("simulator scratch exceeds shared memory (too many devices / slots)");
         return FP_ERR_UNSUPPORTED;
     }
-    const void *kern = wide ? (const void *)sim_batch_kernel<RPL, WARPS, true>
-                            : (const void *)sim_batch_kernel<RPL, WARPS, false>;
+    const bool sm1 = p->dev.SM == 1;
+    const void *kern = wide ? (sm1 ? (const void *)sim_batch_kernel<RPL, WARPS, true, true>
+                                   : (const void *)sim_batch_kernel<RPL, WARPS, true, false>)
+                            : (sm1 ? (const void *)sim_batch_kernel<RPL, WARPS, false, true>
+                                   : (const void *)sim_batch_kernel<RPL, WARPS, false, false>);
     FP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t need_blocks = (B + WARPS - 1) / WARPS;
     const int grid = wide ? persistent_blocks(kern, WARPS * 32, smem, need_blocks)
@@ -120,14 +123,10 @@ static int launch_sim_t(const fp_problem *p, const int32_t *assign, int B, int s
         set_error("workspace too small for the HBM-resident simulator (see fp_sim_workspace_size)");
         return FP_ERR_INVALID;
     }
-    if (wide)
-        sim_batch_kernel<RPL, WARPS, true><<<grid, WARPS * 32, smem, stream>>>(
-            p->dev, L, assign, B, strategy, jit, jstride, mk, st, trace, cap, tlen, blocked,
-            (uint8_t *)ws);
-    else
-        sim_batch_kernel<RPL, WARPS, false><<<grid, WARPS * 32, smem, stream>>>(
-            p->dev, L, assign, B, strategy, jit, jstride, mk, st, trace, cap, tlen, blocked,
-            nullptr);
+    void *args[] = {(void *)&p->dev, (void *)&L, (void *)&assign, (void *)&B, (void *)&strategy,
+                    (void *)&jit, (void *)&jstride, (void *)&mk, (void *)&st, (void *)&trace,
+                    (void *)&cap, (void *)&tlen, (void *)&blocked, (void *)&ws};
+    FP_CUDA(cudaLaunchKernel(kern, dim3(grid), dim3(WARPS * 32), args, (size_t)smem, stream));
     FP_CUDA(cudaGetLastError());
     return FP_OK;
 }

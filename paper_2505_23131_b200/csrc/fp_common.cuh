@@ -143,4 +143,18 @@ __host__ __device__ __forceinline__ void uniform2(U4 r, double& u1, double& u2) 
     u2 = (double)((((uint64_t)r.w << 32) | r.z) >> 11) * s;
 }
 
+// Per-step Philox draws, 32 steps at a time: lane j computes the draw of
+// step (32*floor(step/32) + j) once, the step reads it with two shuffles --
+// keeps the 10-round Philox off every step's dependent chain.  Call once per
+// step from all 32 lanes (warp-uniform).
+__device__ __forceinline__ void step_draw(int step, uint32_t ctr_ep, uint32_t head, uint32_t k0,
+                                          uint32_t k1, double &c1, double &c2, double &u1,
+                                          double &u2) {
+    if ((step & 31) == 0)
+        uniform2(philox4x32_10(U4{ctr_ep, (uint32_t)(step + (threadIdx.x & 31)), head, 0u}, k0, k1),
+                 c1, c2);
+    u1 = __shfl_sync(FP_FULL_MASK, c1, step & 31);
+    u2 = __shfl_sync(FP_FULL_MASK, c2, step & 31);
+}
+
 }  // namespace fp

@@ -1,0 +1,1018 @@
+// Batched SEL/PLC episodes fused with the WC simulator, episode state resident
+// in shared memory, TWO warps per episode:
+//
+//   SEL warp (producer)  In per_episode mode the SEL logits are static per
+//        snapshot and the candidate set depends only on the
+//        vertices chosen so far — never on PLC decisions — so the whole vertex
+//        order is one independent chain: candidate bitset -> ascending list ->
+//        masked softmax over s[v] -> decision (Philox epsilon-mixture sample /
+//        greedy / forced / critical-path teacher) -> mixture log-prob and
+//        entropy (policy.py:186-204, 301-322) -> candidate update
+//        (policy.py:384-389).  It publishes order[t] through shared memory.
+//   PLC warp (consumer)  For v = order[t]: device features (lane = device,
+//        policy.py:226-247 over timeline.py:30-45), column standardization with
+//        the reference's sequential fp64 sums (policy.py:101-105; lane =
+//        column), pre-activations A[v] + S_d + xn_d @ M + c (lane = hidden
+//        column, fact 3), leaky, head2 via a transpose reduction, softmax over
+//        devices, decision, log-prob / entropy, timeline commit
+//        (timeline.py:47-58, bit-exact _rn fp64), S_d += G[v].
+//   The two chains overlap; the episode's latency is the longer (PLC) chain.
+//   After the last step the PLC warp runs sim_episode() on the assignment in
+//   shared memory (fp_sim.cuh) — no round trip through HBM.
+//
+// Optional REINFORCE rows: d log-prob / d entropy w.r.t. the SEL logits
+// (per-vertex smem accumulators, SEL warp) and the PLC pre-activations (per
+// vertex A rows, running per-device sums R_d for the G rows, M / w2 / b2
+// terms; PLC warp), consumed by the episode-reduction kernel (fp_train.cu).
+#pragma once
+
+#include <string>
+
+#include "fp_common.cuh"
+#include "fp_layout.cuh"
+#include "fp_policy.cuh"
+#include "fp_sim.cuh"
+
+namespace fp {
+
+__device__ __forceinline__ double lk(double x, double s) { return x > 0.0 ? x : s * x; }
+__device__ __forceinline__ double lkd(double x, double s) { return x > 0.0 ? 1.0 : s; }
+
+__device__ __forceinline__ void warp_argmax_first(double &v, int &i) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(FP_FULL_MASK, v, o);
+        const int oi = __shfl_xor_sync(FP_FULL_MASK, i, o);
+        if (ov > v || (ov == v && oi < i)) { v = ov; i = oi; }
+    }
+}
+
+__host__ __device__ inline int64_t grad_ep_stride(int n, int h, int d) {
+    return ((2LL * n + 12LL * h + 2 + 2LL * d * h) + 3) / 4 * 4;
+}
+
+template <int MAXD>
+struct PlcLog {  // log2(MAXD)
+    static constexpr int v = MAXD <= 1 ? 0 : MAXD <= 2 ? 1 : MAXD <= 4 ? 2 : MAXD <= 8 ? 3 :
+                             MAXD <= 16 ? 4 : 5;
+};
+
+// ---------------------------------------------------------------------------
+// SEL warp
+// ---------------------------------------------------------------------------
+template <bool GRAD>
+__device__ __forceinline__ void sel_chain(const DevProblem &PR, const DevPolicy &PO,
+                                          const fp_rollout_args &A, uint8_t *base /* nb == sb */,
+                                          const EpLayout &L, const double *s_sm, int ep,
+                                          bool want_lp, bool want_amax) {
+    const int lane = lane_id();
+    const int n = PR.n, W = PR.W;
+    uint32_t *cand = (uint32_t *)(base + L.cand);
+    int *npl = (int *)(base + L.npl);
+    int *clist = (int *)(base + L.clist);
+    double *ce = (double *)(base + L.ce);
+    double *cc = (double *)(base + L.cc);
+    double *dsl = (double *)(base + L.dsl);
+    double *dse = (double *)(base + L.dse);
+    volatile int *order = (volatile int *)(base + L.order);
+    const double eps = A.epsilon, ome = 1.0 - eps;
+    const uint32_t k0 = (uint32_t)A.seed, k1 = (uint32_t)(A.seed >> 32);
+    const uint32_t ctr_ep = A.episode_base + (uint32_t)ep;
+    const int mode = A.mode;
+    const int32_t *frow = mode == FP_MODE_FORCED ? A.forced + (size_t)ep * n * 2 : nullptr;
+    const int *__restrict__ pp = PR.pred_ptr;
+    const int *__restrict__ sp = PR.succ_ptr;
+    const int *__restrict__ si = PR.succ_idx;
+
+    for (int w = lane; w < W; w += 32) cand[w] = 0u;
+    __syncwarp();
+    for (int v = lane; v < n; v += 32) {
+        const int np = pp[v + 1] - pp[v];
+        npl[v] = np;
+        if constexpr (GRAD) { dsl[v] = 0.0; dse[v] = 0.0; }
+        if (np == 0) atomicOr(&cand[v >> 5], 1u << (v & 31));
+    }
+    __syncwarp();
+
+    FP_PHASE_DECL;
+    FP_PHASE_BEGIN(ps);
+    double dc1 = 0.0, dc2 = 0.0;  // draw cache (step_draw)
+    for (int step = 0; step < n; ++step) {
+        double u1 = 0.0, u2 = 0.0;
+        if (mode == FP_MODE_SAMPLE) step_draw(step, ctr_ep, 0u, k0, k1, dc1, dc2, u1, u2);
+        // compact the candidate bitset into an ascending list
+        const uint32_t cw = lane < W ? cand[lane] : 0u;
+        const int pc = __popc(cw);
+        const int incl = warp_inclusive_scan(pc);
+        const int k = __shfl_sync(FP_FULL_MASK, incl, 31);
+        if (k == 0) {  // cyclic graph: nothing is ever ready
+            if (lane == 0) order[step] = -1;
+            return;
+        }
+        {
+            int o = incl - pc;
+            uint32_t m = cw;
+            while (m) {
+                const int b = __ffs(m) - 1;
+                m &= m - 1;
+                clist[o++] = lane * 32 + b;
+            }
+        }
+        __syncwarp();
+        FP_PHASE_END(ps, 0);
+        const bool fast = k <= 32;  // candidate i on lane i, values in registers
+        int idx = -1;
+        double e0 = 0.0, cum0 = 0.0, tot;
+        int myv = -1;
+        if (fast) {
+            myv = lane < k ? clist[lane] : -1;
+            const double sv = lane < k ? s_sm[myv] : -INFINITY;
+            const double mx = warp_max_redux(sv);
+            e0 = lane < k ? exp(sv - mx) : 0.0;
+            cum0 = warp_inclusive_scan(e0);
+            tot = __shfl_sync(FP_FULL_MASK, cum0, 31);
+            if (mode == FP_MODE_FORCED) {
+                const unsigned hit = __ballot_sync(FP_FULL_MASK, lane < k && myv == frow[2 * step]);
+                idx = hit ? __ffs(hit) - 1 : -1;
+            } else if (mode == FP_MODE_TEACHER) {
+                const double tv = lane < k ? PR.tlev[myv] : -INFINITY;
+                const double bt = warp_max_redux(tv);
+                idx = __ffs(__ballot_sync(FP_FULL_MASK, lane < k && tv == bt)) - 1;
+            } else if (mode == FP_MODE_SAMPLE) {
+                if (u1 < eps) {
+                    idx = min((int)(u2 * (double)k), k - 1);
+                } else {
+                    const unsigned hit = __ballot_sync(FP_FULL_MASK, lane < k && cum0 > u2 * tot);
+                    idx = hit ? __ffs(hit) - 1 : k - 1;
+                }
+            }
+        } else {
+            double mx = -INFINITY;
+            for (int i = lane; i < k; i += 32) mx = fmax(mx, s_sm[clist[i]]);
+            mx = warp_max_redux(mx);
+            double carry = 0.0;
+            for (int b0 = 0; b0 < k; b0 += 32) {
+                const int i = b0 + lane;
+                const double e = i < k ? exp(s_sm[clist[i]] - mx) : 0.0;
+                const double cum = warp_inclusive_scan(e) + carry;
+                if (i < k) { ce[i] = e; cc[i] = cum; }
+                carry = __shfl_sync(FP_FULL_MASK, cum, 31);
+            }
+            tot = carry;
+            __syncwarp();
+            if (mode == FP_MODE_FORCED) {
+                const int fv = frow[2 * step];
+                for (int b0 = 0; b0 < k && idx < 0; b0 += 32) {
+                    const unsigned hit =
+                        __ballot_sync(FP_FULL_MASK, b0 + lane < k && clist[b0 + lane] == fv);
+                    if (hit) idx = b0 + __ffs(hit) - 1;
+                }
+            } else if (mode == FP_MODE_TEACHER) {
+                double bt = -INFINITY;
+                for (int i = lane; i < k; i += 32) bt = fmax(bt, PR.tlev[clist[i]]);
+                bt = warp_max_redux(bt);
+                for (int b0 = 0; b0 < k && idx < 0; b0 += 32) {
+                    const unsigned hit = __ballot_sync(
+                        FP_FULL_MASK, b0 + lane < k && PR.tlev[clist[b0 + lane]] == bt);
+                    if (hit) idx = b0 + __ffs(hit) - 1;
+                }
+            } else if (mode == FP_MODE_SAMPLE) {
+                if (u1 < eps) {
+                    idx = min((int)(u2 * (double)k), k - 1);
+                } else {
+                    const double target = u2 * tot;
+                    for (int b0 = 0; b0 < k && idx < 0; b0 += 32) {
+                        const unsigned hit =
+                            __ballot_sync(FP_FULL_MASK, b0 + lane < k && cc[b0 + lane] > target);
+                        if (hit) idx = b0 + __ffs(hit) - 1;
+                    }
+                    if (idx < 0) idx = k - 1;
+                }
+            }
+        }
+        FP_PHASE_END(ps, 1);
+        int amax = -1;
+        if (want_amax || mode == FP_MODE_GREEDY) {
+            // first maximum of p = e / tot (policy.py:309, 396)
+            double bp = -1.0;
+            int bi = 0x7fffffff;
+            for (int i = lane; i < k; i += 32) {
+                const double p = (fast ? e0 : ce[i]) / tot;
+                if (p > bp) { bp = p; bi = i; }
+            }
+            warp_argmax_first(bp, bi);
+            amax = bi;
+            if (mode == FP_MODE_GREEDY) idx = amax;
+        }
+        if (idx < 0) {  // forced vertex is not a candidate
+            if (lane == 0) order[step] = -2;
+            return;
+        }
+        const int v = clist[idx];
+        // publish early: the PLC warp only needs the vertex (a single 32-bit
+        // store replacing the -3 sentinel is the whole hand-off)
+        if (lane == 0) order[step] = v;
+        FP_PHASE_END(ps, 2);
+        if (want_lp) {
+            const double ek = eps / (double)k;
+            double entp = 0.0, lp = 0.0, pidx = 0.0, midx = 0.0, qp = 0.0;
+            for (int i = lane; i < k; i += 32) {
+                const double p = (fast ? e0 : ce[i]) / tot;
+                const double mix = __dadd_rn(__dmul_rn(p, ome), ek);
+                const double lm = log(__dadd_rn(mix, 1e-30));
+                entp += mix * lm;
+                if (i == idx) { lp = lm; pidx = p; midx = mix; }
+                if constexpr (GRAD) qp += -ome * (lm + mix / __dadd_rn(mix, 1e-30)) * p;
+            }
+            const double ent = -warp_sum(entp);
+            lp = warp_sum(lp);  // exactly one lane non-zero
+            if constexpr (GRAD) {
+                pidx = warp_sum(pidx);
+                midx = warp_sum(midx);
+                qp = warp_sum(qp);
+                const double c1 = ome * pidx / __dadd_rn(midx, 1e-30);
+                for (int i = lane; i < k; i += 32) {
+                    const double p = (fast ? e0 : ce[i]) / tot;
+                    const double mix = __dadd_rn(__dmul_rn(p, ome), ek);
+                    const double lm = log(__dadd_rn(mix, 1e-30));
+                    const double q = -ome * (lm + mix / __dadd_rn(mix, 1e-30));
+                    const int u = clist[i];
+                    dsl[u] += c1 * ((i == idx ? 1.0 : 0.0) - p);
+                    dse[u] += p * (q - qp);
+                }
+            }
+            if (lane == 0) {
+                const size_t o = (size_t)ep * n + step;
+                if (A.step_lp) A.step_lp[2 * o] = lp;
+                if (A.step_ent) A.step_ent[2 * o] = ent;
+            }
+        }
+        FP_PHASE_END(ps, 3);
+        if (lane == 0) {
+            const size_t o = (size_t)ep * n + step;
+            if (A.step_vd) A.step_vd[2 * o] = v;
+            if (A.step_argmax) A.step_argmax[2 * o] = clist[amax];
+            if (A.step_ncand) A.step_ncand[o] = k;
+            cand[v >> 5] &= ~(1u << (v & 31));
+        }
+        __syncwarp();
+        for (int j = sp[v] + lane; j < sp[v + 1]; j += 32) {
+            const int w = si[j];
+            if (atomicSub(&npl[w], 1) == 1) atomicOr(&cand[w >> 5], 1u << (w & 31));
+        }
+        __syncwarp();
+        FP_PHASE_END(ps, 4);
+    }
+    FP_PHASE_FLUSH(0);
+    if constexpr (GRAD) {
+        double *g = A.grad_ep + (size_t)ep * grad_ep_stride(n, PO.h, PR.d);
+        for (int v = lane; v < n; v += 32) { g[v] = dsl[v]; g[n + v] = dse[v]; }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// SEL warp, wide path (graphs whose state lives in HBM)
+//
+// The compact chain re-compacts the candidate bitset every step (O(n/32)
+// words) -- quadratic at 10k-100k ops.  Here the candidate set is a 32-ary
+// tree over vertex ids whose node j at level l summarises leaves
+// [j*32^l, (j+1)*32^l): m = max SEL logit of its candidates, z = sum of
+// exp(s - m) over them, c = candidate count (t = max t-level for the
+// critical-path teacher).  A warp updates one node per level with one
+// coalesced 32-child load, a REDUX max and a butterfly sum, so insert /
+// remove / sample / argmax are O(log32 n) warp steps.  Sampling descends by
+// the cumulative weight in ascending-id order, i.e. the reference's
+// searchsorted(cumsum(p), u * sum(p), 'right') (policy.py:313-316), and the
+// uniform branch descends by count to the idx-th candidate in ascending
+// order; the entropy (only when requested) is one pass over the candidates.
+// ---------------------------------------------------------------------------
+struct TreeRef {
+    double *tm, *tz, *tt;
+    int *tc;
+    const uint32_t *cand;
+    const double *s, *tlev;
+    const EpLayout *L;
+    int n;
+    bool teacher;
+
+    // child `i` of node j at level l (l == 1: leaf = vertex)
+    __device__ __forceinline__ void child(int l, int j, double &m, double &z, double &t,
+                                          int &c) const {
+        const int ci = (j << 5) + lane_id();
+        if (l == 1) {
+            const bool ok = ci < n && ((cand[j] >> (ci & 31)) & 1u);
+            m = ok ? s[ci] : -INFINITY;
+            z = ok ? 1.0 : 0.0;
+            c = ok ? 1 : 0;
+            t = ok && teacher ? tlev[ci] : -INFINITY;
+        } else {
+            const bool ok = ci < L->tl_cnt[l - 1];
+            const int idx = L->tl_off[l - 1] + ci;
+            m = ok ? tm[idx] : -INFINITY;
+            z = ok ? tz[idx] : 0.0;
+            c = ok ? tc[idx] : 0;
+            t = ok && teacher ? tt[idx] : -INFINITY;
+        }
+    }
+
+    __device__ __forceinline__ void recompute(int l, int j) const {
+        double m, z, t;
+        int c;
+        child(l, j, m, z, t, c);
+        const double M = warp_max_redux(m);
+        const double zz = c > 0 ? z * exp(m - M) : 0.0;
+        const double Z = warp_sum(zz);
+        const int C = __reduce_add_sync(FP_FULL_MASK, c);
+        const double T = teacher ? warp_max_redux(t) : -INFINITY;
+        if (lane_id() == 0) {
+            const int idx = L->tl_off[l] + j;
+            tm[idx] = M; tz[idx] = Z; tc[idx] = C;
+            if (teacher) tt[idx] = T;
+        }
+        __syncwarp();
+    }
+
+    // leaf v changed: refresh its ancestors bottom-up
+    __device__ __forceinline__ void update(int v) const {
+        for (int l = 1; l <= L->tl_n; ++l) recompute(l, v >> (5 * l));
+    }
+
+    __device__ __forceinline__ int root() const { return L->tl_off[L->tl_n]; }
+
+    // first leaf whose inclusive cumulative weight exceeds target (root units)
+    __device__ __forceinline__ int descend_weight(double target) const {
+        int j = 0;
+        double Mn = tm[root()];
+        for (int l = L->tl_n; l >= 1; --l) {
+            double m, z, t;
+            int c;
+            child(l, j, m, z, t, c);
+            const double w = c > 0 ? z * exp(m - Mn) : 0.0;
+            const double cum = warp_inclusive_scan(w);
+            const unsigned nonempty = __ballot_sync(FP_FULL_MASK, c > 0);
+            const unsigned hit = __ballot_sync(FP_FULL_MASK, c > 0 && cum > target);
+            const int sel = hit ? __ffs(hit) - 1 : 31 - __clz(nonempty);
+            const double prev = __shfl_sync(FP_FULL_MASK, cum - w, sel);
+            const double ms = __shfl_sync(FP_FULL_MASK, m, sel);
+            target = (target - prev) * exp(Mn - ms);
+            Mn = ms;
+            j = (j << 5) + sel;
+        }
+        return j;
+    }
+
+    // the idx-th candidate (0-based) in ascending id order
+    __device__ __forceinline__ int descend_count(int idx) const {
+        int j = 0;
+        for (int l = L->tl_n; l >= 1; --l) {
+            double m, z, t;
+            int c;
+            child(l, j, m, z, t, c);
+            const int cum = warp_inclusive_scan(c);
+            const unsigned hit = __ballot_sync(FP_FULL_MASK, cum > idx);
+            const int sel = __ffs(hit) - 1;
+            idx -= __shfl_sync(FP_FULL_MASK, cum - c, sel);
+            j = (j << 5) + sel;
+        }
+        return j;
+    }
+
+    // first candidate attaining the maximum logit (key 0) or t-level (key 1)
+    __device__ __forceinline__ int descend_max(bool by_tlev) const {
+        int j = 0;
+        const double best = by_tlev ? tt[root()] : tm[root()];
+        for (int l = L->tl_n; l >= 1; --l) {
+            double m, z, t;
+            int c;
+            child(l, j, m, z, t, c);
+            const double key = by_tlev ? t : m;
+            const int sel = __ffs(__ballot_sync(FP_FULL_MASK, c > 0 && key == best)) - 1;
+            j = (j << 5) + sel;
+        }
+        return j;
+    }
+};
+
+__device__ __forceinline__ bool ring_publish(volatile int *ring, volatile int *dead, int step,
+                                             int v) {
+    int ok = 1;
+    if (lane_id() == 0) {
+        const int slot = step & (kRing - 1);
+        while (ring[slot] != -3) {
+            if (*dead) { ok = 0; break; }
+        }
+        if (ok) ring[slot] = v;
+    }
+    return __shfl_sync(FP_FULL_MASK, ok, 0) != 0;
+}
+
+__device__ __forceinline__ void sel_chain_wide(const DevProblem &PR, const DevPolicy &PO,
+                                               const fp_rollout_args &A, uint8_t *nb,
+                                               uint8_t *sb, const EpLayout &L, int ep,
+                                               bool want_lp, bool want_amax) {
+    const int lane = lane_id();
+    const int n = PR.n, W = PR.W;
+    uint32_t *cand = (uint32_t *)(nb + L.cand);
+    int *npl = (int *)(nb + L.npl);
+    volatile int *ring = (volatile int *)(sb + L.ring);
+    volatile int *dead = (volatile int *)(sb + L.flag);
+    const double eps = A.epsilon, ome = 1.0 - eps;
+    const uint32_t k0 = (uint32_t)A.seed, k1 = (uint32_t)(A.seed >> 32);
+    const uint32_t ctr_ep = A.episode_base + (uint32_t)ep;
+    const int mode = A.mode;
+    const int32_t *frow = mode == FP_MODE_FORCED ? A.forced + (size_t)ep * n * 2 : nullptr;
+    const int *__restrict__ pp = PR.pred_ptr;
+    const int *__restrict__ sp = PR.succ_ptr;
+    const int *__restrict__ si = PR.succ_idx;
+    const double *__restrict__ s = PO.s;
+    TreeRef T{(double *)(nb + L.tm), (double *)(nb + L.tz), (double *)(nb + L.tt),
+              (int *)(nb + L.tc), cand, s, PR.tlev, &L, n, mode == FP_MODE_TEACHER};
+
+    for (int w = lane; w < W; w += 32) cand[w] = 0u;
+    __syncwarp();
+    for (int v = lane; v < n; v += 32) {
+        const int np = pp[v + 1] - pp[v];
+        npl[v] = np;
+        if (np == 0) atomicOr(&cand[v >> 5], 1u << (v & 31));
+    }
+    __syncwarp();
+    for (int l = 1; l <= L.tl_n; ++l)
+        for (int j = 0; j < L.tl_cnt[l]; ++j) T.recompute(l, j);
+
+    const int rt = T.root();
+    double dc1 = 0.0, dc2 = 0.0;  // draw cache (step_draw)
+    for (int step = 0; step < n; ++step) {
+        double u1 = 0.0, u2 = 0.0;
+        if (mode == FP_MODE_SAMPLE) step_draw(step, ctr_ep, 0u, k0, k1, dc1, dc2, u1, u2);
+        const int k = T.tc[rt];
+        if (k == 0) {  // cyclic graph: nothing is ever ready
+            ring_publish(ring, dead, step, -1);
+            return;
+        }
+        const double Mr = T.tm[rt], Zr = T.tz[rt];
+        int v = -1;
+        if (mode == FP_MODE_FORCED) {
+            const int fv = frow[2 * step];
+            if (fv >= 0 && fv < n && ((cand[fv >> 5] >> (fv & 31)) & 1u)) v = fv;
+        } else if (mode == FP_MODE_TEACHER) {
+            v = T.descend_max(true);
+        } else if (mode == FP_MODE_SAMPLE) {
+            v = u1 < eps ? T.descend_count(min((int)(u2 * (double)k), k - 1))
+                         : T.descend_weight(u2 * Zr);
+        }
+        int amax = -1;
+        if (want_amax || mode == FP_MODE_GREEDY) {
+            amax = T.descend_max(false);
+            if (mode == FP_MODE_GREEDY) v = amax;
+        }
+        if (v < 0) {  // forced vertex is not a candidate
+            ring_publish(ring, dead, step, -2);
+            return;
+        }
+        if (!ring_publish(ring, dead, step, v)) return;
+        if (want_lp) {
+            const double ek = eps / (double)k;
+            const double p = exp(s[v] - Mr) / Zr;
+            const double mix = __dadd_rn(__dmul_rn(p, ome), ek);
+            const double lp = log(__dadd_rn(mix, 1e-30));
+            double entp = 0.0;
+            for (int w = lane; w < W; w += 32) {
+                uint32_t m = cand[w];
+                while (m) {
+                    const int u = (w << 5) + __ffs(m) - 1;
+                    m &= m - 1;
+                    const double pu = exp(s[u] - Mr) / Zr;
+                    const double mu = __dadd_rn(__dmul_rn(pu, ome), ek);
+                    entp += mu * log(__dadd_rn(mu, 1e-30));
+                }
+            }
+            const double ent = -warp_sum(entp);
+            if (lane == 0) {
+                const size_t o = (size_t)ep * n + step;
+                if (A.step_lp) A.step_lp[2 * o] = lp;
+                if (A.step_ent) A.step_ent[2 * o] = ent;
+            }
+        }
+        if (lane == 0) {
+            const size_t o = (size_t)ep * n + step;
+            if (A.step_vd) A.step_vd[2 * o] = v;
+            if (A.step_argmax) A.step_argmax[2 * o] = amax;
+            if (A.step_ncand) A.step_ncand[o] = k;
+            atomicAnd(&cand[v >> 5], ~(1u << (v & 31)));
+        }
+        __syncwarp();
+        T.update(v);
+        // successors whose last predecessor was just placed become candidates
+        for (int j0 = sp[v]; j0 < sp[v + 1]; j0 += 32) {
+            const int j = j0 + lane;
+            int w = -1;
+            if (j < sp[v + 1]) {
+                w = si[j];
+                if (--npl[w] == 0) atomicOr(&cand[w >> 5], 1u << (w & 31));
+                else w = -1;
+            }
+            __syncwarp();
+            unsigned ready = __ballot_sync(FP_FULL_MASK, w >= 0);
+            while (ready) {
+                const int src = __ffs(ready) - 1;
+                ready &= ready - 1;
+                T.update(__shfl_sync(FP_FULL_MASK, w, src));
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// PLC warp
+// ---------------------------------------------------------------------------
+template <int MAXD, int HPL, bool GRAD, bool WIDE = false>
+__device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &PO,
+                                         const fp_rollout_args &A, uint8_t *nb, uint8_t *sb,
+                                         const EpLayout &L, int ep, bool want_lp,
+                                         bool want_amax) {
+    static_assert(!(WIDE && GRAD), "REINFORCE rows are produced by the compact path only");
+    const int lane = lane_id();
+    const int n = PR.n, D = PR.d, h = PO.h;
+    constexpr int LOGD = PlcLog<MAXD>::v;
+    double *tstart = (double *)(nb + L.tstart);
+    double *tend = (double *)(nb + L.tend);
+    double *xd = (double *)(sb + L.xd);
+    double *xn = (double *)(sb + L.xn);
+    double *stats = (double *)(sb + L.stats);
+    const volatile int *order = (const volatile int *)(nb + L.order);
+    volatile int *ring = (volatile int *)(sb + L.ring);
+    volatile int *dead = (volatile int *)(sb + L.flag);
+    uint8_t *dev = nb + L.assign;
+    const double eps = A.epsilon, ome = 1.0 - eps, slope = PO.slope;
+    const uint32_t k0 = (uint32_t)A.seed, k1 = (uint32_t)(A.seed >> 32);
+    const uint32_t ctr_ep = A.episode_base + (uint32_t)ep;
+    const int mode = A.mode;
+    const int32_t *frow = mode == FP_MODE_FORCED ? A.forced + (size_t)ep * n * 2 : nullptr;
+    const double *__restrict__ Atab = PO.A;
+    const double *__restrict__ Gtab = PO.G;
+    const int *__restrict__ pp = PR.pred_ptr;
+    const int *__restrict__ pi = PR.pred_idx;
+    const uint8_t *__restrict__ ent = PR.is_entry;
+    const double *__restrict__ flops = PR.flops;
+    const double *__restrict__ tdur = PR.tdur;
+    const double *__restrict__ edur = PR.edur;
+    const double b2p = PO.W(PR_PLC_H2_B)[0];
+    double *rsl = (double *)(sb + L.rsum);    // [D][h] running lp sums (grad)
+    double *rse = rsl + D * h;                // [D][h] running entropy sums
+
+    for (int v = lane; v < n; v += 32) { tstart[v] = 0.0; tend[v] = 0.0; dev[v] = 0xFF; }
+    double avail = 0.0, aflops = 0.0;  // lane d < D
+    double Mr[5][HPL], cr[HPL], w2r[HPL], Sd[MAXD][HPL];
+    double dMl[GRAD ? 5 : 1][HPL], dMe[GRAD ? 5 : 1][HPL], dwl[HPL], dwe[HPL];
+    double db2l = 0.0, db2e = 0.0;
+    {
+        const double *w2p = PO.W(PR_PLC_H2_W);
+#pragma unroll
+        for (int t = 0; t < HPL; ++t) {
+            const int j = lane + 32 * t;
+            const bool ok = j < h;
+#pragma unroll
+            for (int c = 0; c < 5; ++c) Mr[c][t] = ok ? PO.M[c * h + j] : 0.0;
+            cr[t] = ok ? PO.c[j] : 0.0;
+            w2r[t] = ok ? w2p[j] : 0.0;
+            dwl[t] = dwe[t] = 0.0;
+#pragma unroll
+            for (int d = 0; d < MAXD; ++d) Sd[d][t] = 0.0;
+            if constexpr (GRAD) {
+#pragma unroll
+                for (int c = 0; c < 5; ++c) dMl[c][t] = dMe[c][t] = 0.0;
+            }
+        }
+        if constexpr (GRAD)
+            for (int i = lane; i < 2 * D * h; i += 32) rsl[i] = 0.0;
+    }
+    __syncwarp();
+    int status = FP_EP_OK;
+    FP_PHASE_DECL;
+    FP_PHASE_BEGIN(pp_);
+    double dc1 = 0.0, dc2 = 0.0;  // draw cache (step_draw)
+    for (int step = 0; step < n; ++step) {
+        double u1 = 0.0, u2 = 0.0;
+        if (mode == FP_MODE_SAMPLE) step_draw(step, ctr_ep, 1u, k0, k1, dc1, dc2, u1, u2);
+        int v;
+        if constexpr (WIDE) {
+            // single-producer / single-consumer ring: the SEL warp refills a
+            // slot only after this warp hands it back (-3)
+            const int slot = step & (kRing - 1);
+            while ((v = ring[slot]) == -3) { }
+            __syncwarp();
+            if (lane == 0) ring[slot] = -3;
+        } else {
+            while ((v = order[step]) == -3) { }
+        }
+        if (v < 0) { status = v == -1 ? FP_EP_DEADLOCK : FP_EP_BAD_ACTION; break; }
+        FP_PHASE_END(pp_, 10);
+        double Av[HPL], Gv[HPL];
+#pragma unroll
+        for (int t = 0; t < HPL; ++t) {
+            const int j = lane + 32 * t;
+            Av[t] = j < h ? Atab[(size_t)v * h + j] : 0.0;
+            Gv[t] = j < h ? Gtab[(size_t)v * h + j] : 0.0;
+        }
+        // ---- device features, lane = device (policy.py:240-246) ----
+        double f4 = 0.0;
+        if (lane < D) {
+            double f1 = 0.0, f2 = 0.0, f3 = 0.0;
+            bool any_local = false;
+            const int p0 = pp[v], p1 = pp[v + 1];
+            for (int j = p0; j < p1; ++j) {
+                const int p = pi[j];
+                const int dp = dev[p];
+                // arrival = end + transfer (0.0 on the same device), timeline.py:30-35
+                const double arr =
+                    ent[p] ? 0.0 : __dadd_rn(tend[p], tdur[(p * D + dp) * D + lane]);
+                f3 = j == p0 ? arr : fmax(f3, arr);
+                if (dp == lane) {
+                    f1 = __dadd_rn(f1, flops[p]);
+                    f2 = any_local ? fmin(f2, tstart[p]) : tstart[p];
+                    any_local = true;
+                }
+            }
+            f4 = fmax(avail, f3);
+            double *xr = xd + lane * 5;
+            xr[0] = aflops; xr[1] = f1; xr[2] = f2; xr[3] = f3; xr[4] = f4;
+        }
+        __syncwarp();
+        FP_PHASE_END(pp_, 11);
+        // ---- column statistics: lane c < 5 sums over devices in order ----
+        if (lane < 5) {
+            double col[MAXD];
+#pragma unroll
+            for (int d = 0; d < MAXD; ++d) col[d] = d < D ? xd[d * 5 + lane] : 0.0;
+            double sum = 0.0;
+#pragma unroll
+            for (int d = 0; d < MAXD; ++d)
+                if (d < D) sum = __dadd_rn(sum, col[d]);
+            // x / D == x * (1/D) exactly when D is a power of two (same real
+            // value, one rounding): the reference's mean bit for bit
+            const bool pow2 = (D & (D - 1)) == 0;
+            const double invD = 1.0 / (double)D;
+            const double mean = pow2 ? __dmul_rn(sum, invD) : __ddiv_rn(sum, (double)D);
+            double sq = 0.0;
+#pragma unroll
+            for (int d = 0; d < MAXD; ++d)
+                if (d < D) {
+                    const double df = __dsub_rn(col[d], mean);
+                    sq = __dadd_rn(sq, __dmul_rn(df, df));
+                }
+            const double sd = __dsqrt_rn(pow2 ? __dmul_rn(sq, invD) : __ddiv_rn(sq, (double)D));
+            stats[lane] = mean;
+            // the guard decision is exact (std computed as the reference does);
+            // the scaling uses one reciprocal per column (<= 1 ulp from x / std)
+            stats[5 + lane] = 1.0 / (sd < 1e-12 ? 1.0 : sd);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < (5 * MAXD + 31) / 32; ++t) {
+            const int i = lane + 32 * t;
+            if (i < 5 * D) {
+                const int c = i % 5;
+                xn[i] = __dmul_rn(__dsub_rn(xd[i], stats[c]), stats[5 + c]);
+            }
+        }
+        __syncwarp();
+        FP_PHASE_END(pp_, 12);
+        // ---- pre-activations + head2 partial sums (lane = hidden column) ----
+        double pre[MAXD][HPL];
+        double part[MAXD];
+#pragma unroll
+        for (int d = 0; d < MAXD; ++d) {
+            part[d] = 0.0;
+#pragma unroll
+            for (int t = 0; t < HPL; ++t) pre[d][t] = 0.0;
+            if (d < D) {
+                const double x0 = xn[d * 5], x1 = xn[d * 5 + 1], x2 = xn[d * 5 + 2],
+                             x3 = xn[d * 5 + 3], x4 = xn[d * 5 + 4];
+#pragma unroll
+                for (int t = 0; t < HPL; ++t) {
+                    double a = Av[t] + Sd[d][t] + cr[t];
+                    a = fma(x0, Mr[0][t], a);
+                    a = fma(x1, Mr[1][t], a);
+                    a = fma(x2, Mr[2][t], a);
+                    a = fma(x3, Mr[3][t], a);
+                    a = fma(x4, Mr[4][t], a);
+                    pre[d][t] = a;
+                    part[d] = fma(lk(a, slope), w2r[t], part[d]);
+                }
+            }
+        }
+        // transpose reduction: after LOGD halving rounds lane l holds a partial
+        // for device (l >> (5 - LOGD)) & (MAXD-1); the xor rounds finish it
+        {
+#pragma unroll
+            for (int r = 0; r < LOGD; ++r) {
+                const int o = 16 >> r;
+                const bool upper = (lane & o) != 0;
+                const int half = MAXD >> (r + 1);
+#pragma unroll
+                for (int i = 0; i < MAXD / 2; ++i) {
+                    if (i < half) {
+                        const double send = upper ? part[i] : part[i + half];
+                        const double keep = upper ? part[i + half] : part[i];
+                        part[i] = keep + __shfl_xor_sync(FP_FULL_MASK, send, o);
+                    }
+                }
+            }
+#pragma unroll
+            for (int o = 16 >> LOGD; o > 0; o >>= 1)
+                part[0] += __shfl_xor_sync(FP_FULL_MASK, part[0], o);
+        }
+        const double lgall = __shfl_sync(FP_FULL_MASK, part[0], (lane & (MAXD - 1)) << (5 - LOGD));
+        FP_PHASE_END(pp_, 13);
+        const double lg = lane < D ? lgall + b2p : -INFINITY;
+        const double lmx = warp_max_redux(lg);
+        const double ed = lane < D ? exp(lg - lmx) : 0.0;
+        const double ecum = warp_scan_pow2<LOGD>(ed);
+        const double etot = __shfl_sync(FP_FULL_MASK, ecum, D - 1);
+        const double pd = lane < D ? ed / etot : -1.0;
+        int amax = -1;
+        if (want_amax || mode == FP_MODE_GREEDY) {
+            double am = pd;
+            int ai = lane < D ? lane : 0x7fffffff;
+            warp_argmax_first(am, ai);
+            amax = ai;
+        }
+        FP_PHASE_END(pp_, 14);
+        int jdx;
+        if (mode == FP_MODE_FORCED) {
+            jdx = frow[2 * step + 1];
+            if (jdx < 0 || jdx >= D) {
+                status = FP_EP_BAD_ACTION;
+                if (WIDE && lane == 0) *dead = 1;  // release a producer blocked on the ring
+                break;
+            }
+        } else if (mode == FP_MODE_TEACHER) {
+            // argmin earliest start, first device on ties (heuristics.py:85-91)
+            const double tv = lane < D ? f4 : INFINITY;
+            const double best = warp_min_redux(tv);
+            jdx = __ffs(__ballot_sync(FP_FULL_MASK, lane < D && tv == best)) - 1;
+        } else if (mode == FP_MODE_GREEDY) {
+            jdx = amax;
+        } else {
+            if (u1 < eps) {
+                jdx = min((int)(u2 * (double)D), D - 1);
+            } else {
+                const unsigned hit = __ballot_sync(FP_FULL_MASK, lane < D && ecum > u2 * etot);
+                jdx = hit ? __ffs(hit) - 1 : D - 1;
+            }
+        }
+        FP_PHASE_END(pp_, 15);
+        if (want_lp) {
+            const double ekd = eps / (double)D;
+            double mixd = 0.0, lmd = 0.0;
+            if (lane < D) {
+                mixd = __dadd_rn(__dmul_rn(pd, ome), ekd);
+                lmd = log(__dadd_rn(mixd, 1e-30));
+            }
+            const double entv = -warp_sum(lane < D ? mixd * lmd : 0.0);
+            const double lp = __shfl_sync(FP_FULL_MASK, lmd, jdx);
+            if (lane == 0) {
+                const size_t o = (size_t)ep * n + step;
+                if (A.step_lp) A.step_lp[2 * o + 1] = lp;
+                if (A.step_ent) A.step_ent[2 * o + 1] = entv;
+            }
+            if constexpr (GRAD) {
+                const double pj = __shfl_sync(FP_FULL_MASK, pd, jdx);
+                const double mj = __shfl_sync(FP_FULL_MASK, mixd, jdx);
+                const double q = lane < D ? -ome * (lmd + mixd / __dadd_rn(mixd, 1e-30)) : 0.0;
+                const double qpd = warp_sum(lane < D ? q * pd : 0.0);
+                const double gl = lane < D ? ome * pj / __dadd_rn(mj, 1e-30) *
+                                                 ((lane == jdx ? 1.0 : 0.0) - pd) : 0.0;
+                const double ge = lane < D ? pd * (q - qpd) : 0.0;
+                double arl[HPL], are[HPL];
+#pragma unroll
+                for (int t = 0; t < HPL; ++t) arl[t] = are[t] = 0.0;
+#pragma unroll
+                for (int d = 0; d < MAXD; ++d) {
+                    if (d >= D) continue;
+                    const double gld = __shfl_sync(FP_FULL_MASK, gl, d);
+                    const double ged = __shfl_sync(FP_FULL_MASK, ge, d);
+                    if (lane == 0) { db2l += gld; db2e += ged; }
+                    const double x0 = xn[d * 5], x1 = xn[d * 5 + 1], x2 = xn[d * 5 + 2],
+                                 x3 = xn[d * 5 + 3], x4 = xn[d * 5 + 4];
+#pragma unroll
+                    for (int t = 0; t < HPL; ++t) {
+                        const double dl = gld * w2r[t] * lkd(pre[d][t], slope);
+                        const double de = ged * w2r[t] * lkd(pre[d][t], slope);
+                        const double lv = lk(pre[d][t], slope);
+                        dwl[t] = fma(gld, lv, dwl[t]);
+                        dwe[t] = fma(ged, lv, dwe[t]);
+                        arl[t] += dl;
+                        are[t] += de;
+                        const int j = lane + 32 * t;
+                        if (j < h) { rsl[d * h + j] += dl; rse[d * h + j] += de; }
+                        dMl[0][t] = fma(x0, dl, dMl[0][t]); dMe[0][t] = fma(x0, de, dMe[0][t]);
+                        dMl[1][t] = fma(x1, dl, dMl[1][t]); dMe[1][t] = fma(x1, de, dMe[1][t]);
+                        dMl[2][t] = fma(x2, dl, dMl[2][t]); dMe[2][t] = fma(x2, de, dMe[2][t]);
+                        dMl[3][t] = fma(x3, dl, dMl[3][t]); dMe[3][t] = fma(x3, de, dMe[3][t]);
+                        dMl[4][t] = fma(x4, dl, dMl[4][t]); dMe[4][t] = fma(x4, de, dMe[4][t]);
+                    }
+                }
+                double *row = A.grad_rows + ((size_t)ep * n + v) * 4 * h;
+#pragma unroll
+                for (int t = 0; t < HPL; ++t) {
+                    const int j = lane + 32 * t;
+                    if (j >= h) continue;
+                    row[j] = arl[t];
+                    row[h + j] = are[t];
+                    row[2 * h + j] = rsl[jdx * h + j];
+                    row[3 * h + j] = rse[jdx * h + j];
+                }
+            }
+        }
+        FP_PHASE_END(pp_, 16);
+        // ---- commit (timeline.py:47-58) ----
+        if (lane == jdx) {
+            aflops = __dadd_rn(aflops, flops[v]);
+            if (!ent[v]) {
+                const double en = __dadd_rn(f4, edur[v * D + jdx]);
+                tstart[v] = f4;
+                tend[v] = en;
+                avail = en;
+            }
+            dev[v] = (uint8_t)jdx;
+            if (A.step_vd) A.step_vd[2 * ((size_t)ep * n + step) + 1] = jdx;
+        }
+        if (lane == 0 && A.step_argmax) A.step_argmax[2 * ((size_t)ep * n + step) + 1] = amax;
+#pragma unroll
+        for (int d = 0; d < MAXD; ++d)
+            if (d == jdx)
+#pragma unroll
+                for (int t = 0; t < HPL; ++t) Sd[d][t] += Gv[t];
+        __syncwarp();
+        FP_PHASE_END(pp_, 17);
+    }
+    FP_PHASE_FLUSH(0);
+    if constexpr (GRAD) if (status == FP_EP_OK) {
+        double *q = A.grad_ep + (size_t)ep * grad_ep_stride(n, h, D) + 2 * n;
+#pragma unroll
+        for (int t = 0; t < HPL; ++t) {
+            const int j = lane + 32 * t;
+            if (j >= h) continue;
+#pragma unroll
+            for (int c = 0; c < 5; ++c) { q[c * h + j] = dMl[c][t]; q[5 * h + c * h + j] = dMe[c][t]; }
+            q[10 * h + j] = dwl[t];
+            q[11 * h + j] = dwe[t];
+            for (int d = 0; d < D; ++d) {
+                q[12 * h + 2 + d * h + j] = rsl[d * h + j];
+                q[12 * h + 2 + D * h + d * h + j] = rse[d * h + j];
+            }
+        }
+        if (lane == 0) { q[12 * h] = db2l; q[12 * h + 1] = db2e; }
+    }
+    return status;
+}
+
+template <int MAXD, int HPL, bool GRAD, int EPB, bool SM1>
+__global__ void __launch_bounds__(EPB * 64, 8 / EPB)
+rollout_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    constexpr int RPL = (MAXD + MAXD * MAXD + 31) / 32;
+    const int lane = lane_id();
+    const int warp = threadIdx.x >> 5;
+    const int slot = warp >> 1;  // episode slot in the block
+    const bool is_plc = warp & 1;
+    const int ep = blockIdx.x * EPB + slot;
+    const int n = PR.n;
+    // block-shared SEL logits (every episode of the batch uses one snapshot)
+    double *s_sm = (double *)smem;
+    for (int v = threadIdx.x; v < n; v += blockDim.x) s_sm[v] = PO.s[v];
+    uint8_t *base = smem + fp_align(8 * n, 16) + (size_t)slot * L.bytes;
+    if (!is_plc) {
+        volatile int *order = (volatile int *)(base + L.order);
+        for (int t = lane; t < n; t += 32) order[t] = -3;  // hand-off sentinel
+    }
+    __syncthreads();
+    if (ep >= A.B) return;
+    const bool want_lp = GRAD || A.step_lp != nullptr || A.step_ent != nullptr;
+    const bool want_amax = A.step_argmax != nullptr;
+    if (!is_plc) {
+        sel_chain<GRAD>(PR, PO, A, base, L, s_sm, ep, want_lp, want_amax);
+        return;
+    }
+    int status = plc_chain<MAXD, HPL, GRAD>(PR, PO, A, base, base, L, ep, want_lp, want_amax);
+    const uint8_t *dev = base + L.assign;
+    for (int v = lane; v < n; v += 32) A.assign[(size_t)ep * n + v] = dev[v] == 0xFF ? -1 : dev[v];
+    double mk = 0.0;
+    if (status == FP_EP_OK && A.simulate) {
+        __syncwarp();
+        SimOut o = sim_episode<RPL, false, SM1>(PR, base, base, L, A.strategy, nullptr,
+                                    A.trace ? A.trace + (size_t)ep * A.trace_cap : nullptr,
+                                    A.trace_cap, nullptr);
+        status = o.status;
+        mk = o.makespan;
+        if (lane == 0 && A.trace_len) A.trace_len[ep] = o.n_events;
+    }
+    if (lane == 0) {
+        if (A.makespan) A.makespan[ep] = mk;
+        A.status[ep] = status;
+    }
+}
+
+template <int MAXD, int HPL, bool GRAD>
+int launch_rollout(const fp_problem *p, const fp_policy *pol, const fp_rollout_args &a,
+                          cudaStream_t st) {
+    constexpr int EPB = 1;
+    const DevProblem &PR = p->dev;
+    const EpLayout L = make_layout(PR.n, PR.W, PR.R, PR.SM, true,
+                                   GRAD ? 2 * PR.d * pol->dev.h : 0);
+    const int64_t smem = fp_align(8 * PR.n, 16) + (int64_t)L.bytes * EPB;
+    if (smem > 227 * 1024) {
+        set_error("episode state exceeds shared memory for this graph size");
+        return FP_ERR_UNSUPPORTED;
+    }
+    auto kern = PR.SM == 1 ? rollout_kernel<MAXD, HPL, GRAD, EPB, true>
+                           : rollout_kernel<MAXD, HPL, GRAD, EPB, false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FP_ERR_CUDA; }
+    const int grid = (a.B + EPB - 1) / EPB;
+    kern<<<grid, EPB * 64, smem, st>>>(PR, pol->dev, a, L);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FP_ERR_CUDA; }
+    return FP_OK;
+}
+
+// Wide path: persistent grid, one SEL + one PLC warp per resident episode,
+// n-sized state in the HBM workspace slice of this block, small scratch and
+// the hand-off ring in shared memory.  After the PLC chain the same warp
+// scores the assignment with the hierarchical-bitset simulator.
+template <int MAXD, int HPL, bool SM1>
+__global__ void __launch_bounds__(64, 8)
+rollout_wide_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    constexpr int RPL = (MAXD + MAXD * MAXD + 31) / 32;
+    const int lane = lane_id();
+    const bool is_plc = (threadIdx.x >> 5) & 1;
+    const int n = PR.n;
+    uint8_t *sb = smem;
+    uint8_t *nb = (uint8_t *)A.workspace + (size_t)blockIdx.x * L.gbytes;
+    const bool want_lp = A.step_lp != nullptr || A.step_ent != nullptr;
+    const bool want_amax = A.step_argmax != nullptr;
+    for (int ep = blockIdx.x; ep < A.B; ep += gridDim.x) {
+        if (!is_plc) {
+            volatile int *ring = (volatile int *)(sb + L.ring);
+            for (int t = lane; t < kRing; t += 32) ring[t] = -3;
+            if (lane == 0) *(volatile int *)(sb + L.flag) = 0;
+        }
+        __syncthreads();
+        if (!is_plc) {
+            sel_chain_wide(PR, PO, A, nb, sb, L, ep, want_lp, want_amax);
+        } else {
+            int status = plc_chain<MAXD, HPL, false, true>(PR, PO, A, nb, sb, L, ep, want_lp,
+                                                           want_amax);
+            const uint8_t *dev = nb + L.assign;
+            for (int v = lane; v < n; v += 32)
+                A.assign[(size_t)ep * n + v] = dev[v] == 0xFF ? -1 : dev[v];
+            double mk = 0.0;
+            if (status == FP_EP_OK && A.simulate) {
+                __syncwarp();
+                SimOut o = sim_episode<RPL, true, SM1>(
+                    PR, nb, sb, L, A.strategy, nullptr,
+                    A.trace ? A.trace + (size_t)ep * A.trace_cap : nullptr, A.trace_cap, nullptr);
+                status = o.status;
+                mk = o.makespan;
+                if (lane == 0 && A.trace_len) A.trace_len[ep] = o.n_events;
+            }
+            if (lane == 0) {
+                if (A.makespan) A.makespan[ep] = mk;
+                A.status[ep] = status;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+template <int MAXD, int HPL>
+int launch_rollout_wide(const fp_problem *p, const fp_policy *pol,
+                               const fp_rollout_args &a, int64_t *ws_needed, cudaStream_t st) {
+    const DevProblem &PR = p->dev;
+    const EpLayout L = make_layout(PR.n, PR.W, PR.R, PR.SM, true, 0, true);
+    const int64_t smem = L.bytes;
+    if (smem > 227 * 1024) {
+        set_error("episode scratch exceeds shared memory (too many devices / slots)");
+        return FP_ERR_UNSUPPORTED;
+    }
+    auto kern = PR.SM == 1 ? rollout_wide_kernel<MAXD, HPL, true> : rollout_wide_kernel<MAXD, HPL, false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FP_ERR_CUDA; }
+    const int grid = persistent_blocks((const void *)kern, 64, smem, a.B);
+    const int64_t need = (int64_t)grid * L.gbytes;
+    if (ws_needed) { *ws_needed = need; return FP_OK; }
+    if (!a.workspace || a.workspace_bytes < need) {
+        set_error("workspace too small for the wide rollout (see fp_rollout_workspace_size)");
+        return FP_ERR_INVALID;
+    }
+    kern<<<grid, 64, smem, st>>>(PR, pol->dev, a, L);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FP_ERR_CUDA; }
+    return FP_OK;
+}
+
+}  // namespace fp

@@ -84,7 +84,7 @@ __device__ __forceinline__ int pend_pop_hier(uint32_t *b, const EpLayout &L) {
 // nb: this episode's n-sized state (shared memory, or its HBM workspace slice
 // on the wide path); sb: its small shared-memory scratch.  nb + L.assign must
 // hold the assignment (made visible with __syncwarp).  All 32 lanes must call.
-template <int RPL, bool HIER = false>
+template <int RPL, bool HIER = false, bool SM1 = false>
 __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *nb, uint8_t *sb,
                                               const EpLayout &L, int strategy,
                                               const double *__restrict__ jit,
@@ -127,14 +127,22 @@ __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *nb, 
         missing[v] = miss;
     }
     for (int i = lane; i < R * BW; i += 32) bits[i] = 0u;
+    // SM1: every resource has at most one slot (the reference's default
+    // cluster), so each resource's in-flight task lives in its owning lane's
+    // registers (ipv / iend) instead of the shared-memory pool; the pool is
+    // only mirrored for the trace sort.
     int fr[RPL];
+    int ipv[SM1 ? RPL : 1];
+    double iend[SM1 ? RPL : 1];
 #pragma unroll
     for (int q = 0; q < RPL; ++q) {
         const int r = lane + 32 * q;
         fr[q] = r < R ? P.slots[r] : 0;
+        if constexpr (SM1) { ipv[q] = -1; iend[q] = 0.0; }
         if (r < R) {
             cnt[r] = 0;
-            for (int i = 0; i < SM; ++i) pv[r * SM + i] = -1;
+            if constexpr (!SM1)
+                for (int i = 0; i < SM; ++i) pv[r * SM + i] = -1;
         }
     }
     __syncwarp();
@@ -163,54 +171,67 @@ __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *nb, 
         for (int q = 0; q < RPL; ++q) {
             const int r = lane + 32 * q;
             if (r >= R) continue;
-            int c = cnt[r];
-            if (fr[q] > 0 && c > 0) {
-                uint32_t *wb = bits + r * BW;
-                int w = 0;
-                int slot = r * SM;
-                int f = fr[q];
-                while (f > 0 && c > 0) {
-                    int pos;
-                    if constexpr (HIER) {
-                        pos = pend_pop_hier<HIER>(wb, L);
-                    } else {
-                        uint32_t word = wb[w];
-                        while (word == 0u) word = wb[++w];
-                        const int b = __ffs(word) - 1;
-                        wb[w] = word & ~(1u << b);
-                        pos = (w << 5) + b;
+            if (fr[q] > 0) {
+                int c = cnt[r];
+                if (c > 0) {
+                    uint32_t *wb = bits + r * BW;
+                    int w = 0;
+                    int slot = r * SM;
+                    int f = fr[q];
+                    while (f > 0 && c > 0) {
+                        int pos;
+                        if constexpr (HIER) {
+                            pos = pend_pop_hier<HIER>(wb, L);
+                        } else {
+                            uint32_t word = wb[w];
+                            while (word == 0u) word = wb[++w];
+                            const int b = __ffs(word) - 1;
+                            wb[w] = word & ~(1u << b);
+                            pos = (w << 5) + b;
+                        }
+                        const int v = rvert[pos];
+                        double dur;
+                        int kind, tb;
+                        if (r < d) {
+                            kind = 0; tb = -1;
+                            dur = edur[v * d + r];
+                            if (jit) dur = __dmul_rn(dur, jit[v * d + r]);
+                        } else {
+                            const int ta = (r - d) / d;
+                            kind = 1; tb = (r - d) - ta * d;
+                            dur = tdur[(v * d + ta) * d + tb];
+                            if (jit) dur = __dmul_rn(dur, jit[n * d + (v * d + ta) * d + tb]);
+                        }
+                        const double end = __dadd_rn(t, dur);
+                        if constexpr (SM1) {
+                            ipv[q] = v;
+                            iend[q] = end;
+                            if (tracing) { pend[slot] = end; pv[slot] = v; }
+                        } else {
+                            while (pv[slot] >= 0) ++slot;
+                            pend[slot] = end;
+                            pv[slot] = v;
+                        }
+                        if (tracing) {
+                            const int k = atomicAdd(&ctr[0], 1);
+                            skey[k] = sim_task_key(krk[v], kind, v, tb);
+                            sidx[k] = slot;
+                        }
+                        --f;
+                        --c;
                     }
-                    const int v = rvert[pos];
-                    double dur;
-                    int kind, tb;
-                    if (r < d) {
-                        kind = 0; tb = -1;
-                        dur = edur[v * d + r];
-                        if (jit) dur = __dmul_rn(dur, jit[v * d + r]);
-                    } else {
-                        const int ta = (r - d) / d;
-                        kind = 1; tb = (r - d) - ta * d;
-                        dur = tdur[(v * d + ta) * d + tb];
-                        if (jit) dur = __dmul_rn(dur, jit[n * d + (v * d + ta) * d + tb]);
-                    }
-                    while (pv[slot] >= 0) ++slot;
-                    pend[slot] = __dadd_rn(t, dur);
-                    pv[slot] = v;
-                    if (tracing) {
-                        const int k = atomicAdd(&ctr[0], 1);
-                        skey[k] = sim_task_key(krk[v], kind, v, tb);
-                        sidx[k] = slot;
-                    }
-                    --f;
-                    --c;
+                    fr[q] = f;
+                    cnt[r] = c;
                 }
-                fr[q] = f;
-                cnt[r] = c;
             }
-            // in-flight scan of this resource's slots (the wait phase's min)
-            for (int i = 0; i < SM; ++i) {
-                const int s = r * SM + i;
-                if (pv[s] >= 0) { lmin = fmin(lmin, pend[s]); ++live; }
+            // in-flight tasks of this resource (the wait phase's min)
+            if constexpr (SM1) {
+                if (ipv[q] >= 0) { lmin = fmin(lmin, iend[q]); ++live; }
+            } else {
+                for (int i = 0; i < SM; ++i) {
+                    const int s = r * SM + i;
+                    if (pv[s] >= 0) { lmin = fmin(lmin, pend[s]); ++live; }
+                }
             }
         }
         __syncwarp();
@@ -256,11 +277,18 @@ __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *nb, 
         for (int q = 0; q < RPL; ++q) {
             const int r = lane + 32 * q;
             if (r >= R) continue;
-            for (int i = 0; i < SM; ++i) {
+            for (int i = 0; i < (SM1 ? 1 : SM); ++i) {
                 const int s = r * SM + i;
-                const int v = pv[s];
-                if (v < 0 || pend[s] != tmin) continue;
-                pv[s] = -1;
+                int v;
+                if constexpr (SM1) {
+                    v = ipv[q];
+                    if (v < 0 || iend[q] != tmin) continue;
+                    ipv[q] = -1;
+                } else {
+                    v = pv[s];
+                    if (v < 0 || pend[s] != tmin) continue;
+                    pv[s] = -1;
+                }
                 fr[q] += 1;
                 if (tracing) {
                     const int k = atomicAdd(&ctr[1], 1);
