@@ -41,6 +41,9 @@ extern "C" {
 /* launch flags (fp_sim_batch flags, fp_rollout_args.flags) */
 #define FP_FLAG_WIDE 1  /* force the HBM-resident (wide) episode path even when the
                            compact shared-memory path would fit (tests / benchmarks) */
+#define FP_FLAG_TIE_RANDOM 2 /* FP_MODE_TEACHER: break equal-t-level selection ties
+                                uniformly at random (Philox), as critical_path_assign's
+                                trials do (heuristics.py:76-83, 114-117) */
 
 /* per-episode status codes written by batched kernels */
 #define FP_EP_OK 0

@@ -17,6 +17,7 @@ from ._build import LIB as _LIB_PATH
 FP_OK, FP_ERR_INVALID, FP_ERR_CUDA, FP_ERR_UNSUPPORTED, FP_ERR_DEADLOCK, FP_ERR_OVERFLOW = range(6)
 EP_OK, EP_DEADLOCK, EP_TRACE_OVERFLOW, EP_BAD_ACTION = range(4)
 FLAG_WIDE = 1  # force the HBM-resident episode path
+FLAG_TIE_RANDOM = 2  # teacher mode: random tie-breaks among equal t-levels
 
 _lib = None
 

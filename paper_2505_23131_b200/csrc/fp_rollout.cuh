@@ -97,9 +97,11 @@ __device__ __forceinline__ void sel_chain(const DevProblem &PR, const DevPolicy 
     FP_PHASE_DECL;
     FP_PHASE_BEGIN(ps);
     double dc1 = 0.0, dc2 = 0.0;  // draw cache (step_draw)
+    const bool tie_rand = mode == FP_MODE_TEACHER && (A.flags & FP_FLAG_TIE_RANDOM);
     for (int step = 0; step < n; ++step) {
         double u1 = 0.0, u2 = 0.0;
-        if (mode == FP_MODE_SAMPLE) step_draw(step, ctr_ep, 0u, k0, k1, dc1, dc2, u1, u2);
+        if (mode == FP_MODE_SAMPLE || tie_rand)
+            step_draw(step, ctr_ep, 0u, k0, k1, dc1, dc2, u1, u2);
         // compact the candidate bitset into an ascending list
         const uint32_t cw = lane < W ? cand[lane] : 0u;
         const int pc = __popc(cw);
@@ -137,7 +139,12 @@ __device__ __forceinline__ void sel_chain(const DevProblem &PR, const DevPolicy 
             } else if (mode == FP_MODE_TEACHER) {
                 const double tv = lane < k ? PR.tlev[myv] : -INFINITY;
                 const double bt = warp_max_redux(tv);
-                idx = __ffs(__ballot_sync(FP_FULL_MASK, lane < k && tv == bt)) - 1;
+                unsigned top = __ballot_sync(FP_FULL_MASK, lane < k && tv == bt);
+                if (tie_rand) {  // the r-th of the tied candidates, ascending id
+                    const int cnt = __popc(top);
+                    for (int r = min((int)(u1 * (double)cnt), cnt - 1); r > 0; --r) top &= top - 1;
+                }
+                idx = __ffs(top) - 1;
             } else if (mode == FP_MODE_SAMPLE) {
                 if (u1 < eps) {
                     idx = min((int)(u2 * (double)k), k - 1);
@@ -171,10 +178,21 @@ __device__ __forceinline__ void sel_chain(const DevProblem &PR, const DevPolicy 
                 double bt = -INFINITY;
                 for (int i = lane; i < k; i += 32) bt = fmax(bt, PR.tlev[clist[i]]);
                 bt = warp_max_redux(bt);
+                int r = 0;
+                if (tie_rand) {
+                    int cnt = 0;
+                    for (int b0 = 0; b0 < k; b0 += 32)
+                        cnt += __popc(__ballot_sync(
+                            FP_FULL_MASK, b0 + lane < k && PR.tlev[clist[b0 + lane]] == bt));
+                    r = min((int)(u1 * (double)cnt), cnt - 1);
+                }
                 for (int b0 = 0; b0 < k && idx < 0; b0 += 32) {
-                    const unsigned hit = __ballot_sync(
+                    unsigned hit = __ballot_sync(
                         FP_FULL_MASK, b0 + lane < k && PR.tlev[clist[b0 + lane]] == bt);
-                    if (hit) idx = b0 + __ffs(hit) - 1;
+                    const int c = __popc(hit);
+                    if (r >= c) { r -= c; continue; }
+                    for (; r > 0; --r) hit &= hit - 1;
+                    idx = b0 + __ffs(hit) - 1;
                 }
             } else if (mode == FP_MODE_SAMPLE) {
                 if (u1 < eps) {
@@ -441,9 +459,11 @@ __device__ __forceinline__ void sel_chain_wide(const DevProblem &PR, const DevPo
 
     const int rt = T.root();
     double dc1 = 0.0, dc2 = 0.0;  // draw cache (step_draw)
+    const bool tie_rand = mode == FP_MODE_TEACHER && (A.flags & FP_FLAG_TIE_RANDOM);
     for (int step = 0; step < n; ++step) {
         double u1 = 0.0, u2 = 0.0;
-        if (mode == FP_MODE_SAMPLE) step_draw(step, ctr_ep, 0u, k0, k1, dc1, dc2, u1, u2);
+        if (mode == FP_MODE_SAMPLE || tie_rand)
+            step_draw(step, ctr_ep, 0u, k0, k1, dc1, dc2, u1, u2);
         const int k = T.tc[rt];
         if (k == 0) {  // cyclic graph: nothing is ever ready
             ring_publish(ring, dead, step, -1);
@@ -456,6 +476,46 @@ __device__ __forceinline__ void sel_chain_wide(const DevProblem &PR, const DevPo
             if (fv >= 0 && fv < n && ((cand[fv >> 5] >> (fv & 31)) & 1u)) v = fv;
         } else if (mode == FP_MODE_TEACHER) {
             v = T.descend_max(true);
+            if (tie_rand) {  // r-th tied candidate: one pass over the candidate bitset
+                const double bt = T.tt[rt];
+                int cnt = 0;
+                for (int w = lane; w < W; w += 32) {
+                    uint32_t m = cand[w];
+                    while (m) {
+                        const int u = (w << 5) + __ffs(m) - 1;
+                        m &= m - 1;
+                        cnt += PR.tlev[u] == bt;
+                    }
+                }
+                cnt = __reduce_add_sync(FP_FULL_MASK, cnt);
+                int r = min((int)(u1 * (double)cnt), cnt - 1);
+                for (int w0 = 0; w0 < W; w0 += 32) {
+                    const int w = w0 + lane;
+                    uint32_t tied = 0;
+                    if (w < W) {
+                        uint32_t m = cand[w];
+                        while (m) {
+                            const int b = __ffs(m) - 1;
+                            m &= m - 1;
+                            if (PR.tlev[(w << 5) + b] == bt) tied |= 1u << b;
+                        }
+                    }
+                    const int c = __popc(tied);
+                    const int before = warp_inclusive_scan(c) - c;
+                    const int total = __shfl_sync(FP_FULL_MASK, before + c, 31);
+                    if (r >= total) { r -= total; continue; }
+                    const unsigned own = __ballot_sync(FP_FULL_MASK, r >= before && r < before + c);
+                    const int src = __ffs(own) - 1;
+                    int pick = -1;
+                    if (lane == src) {
+                        uint32_t m = tied;
+                        for (int q = r - before; q > 0; --q) m &= m - 1;
+                        pick = (w << 5) + __ffs(m) - 1;
+                    }
+                    v = __shfl_sync(FP_FULL_MASK, pick, src);
+                    break;
+                }
+            }
         } else if (mode == FP_MODE_SAMPLE) {
             v = u1 < eps ? T.descend_count(min((int)(u2 * (double)k), k - 1))
                          : T.descend_weight(u2 * Zr);

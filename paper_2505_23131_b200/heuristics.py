@@ -61,6 +61,40 @@ class CriticalPathRule:
         return top[int(rng.integers(len(top)))]
 
 
+def critical_path_assign(graph, cluster, trials: int = 50, seed: int = 0,
+                         strategy: str = "fifo", features=None, return_all: bool = False):
+    """List scheduling with randomised selection tie-breaks, best of ``trials``
+    (reference heuristics.py:94-131): every trial is one critical-path-teacher
+    episode inside the rollout kernel (largest t-level, ties broken uniformly
+    at random by Philox keyed on (seed, trial, step); earliest-start device,
+    first on ties), all trials run as one batch with the fused simulator, and
+    the first trial with the smallest makespan wins.  The reference draws its
+    tie-breaks from numpy PCG64 streams, so individual trials match it in
+    distribution, not draw for draw; without ties every trial is the
+    deterministic CriticalPathRule episode."""
+    if trials < 1:
+        raise ValueError("trials must be >= 1")
+    from .params import init_policy_params
+    from .policy import PolicyConfig, PolicyContext
+
+    # the teacher's actions do not depend on the policy; a minimal policy
+    # provides the tables the kernel reads
+    pc = PolicyConfig(hidden=8, k_rounds=1)
+    ctx = PolicyContext(graph, cluster, pc, features)
+    rb = ctx.rollout_batch(init_policy_params(pc, seed=0), trials, 0.0, seed, mode="teacher",
+                           simulate=True, strategy=strategy, tie_random=True)
+    st = rb.status.cpu().numpy()
+    if (st != 0).any():
+        raise RuntimeError(f"critical-path trial failed with status {int(st[st != 0][0])}")
+    mk = rb.makespan.cpu().numpy()
+    assign = rb.assign.cpu().numpy()
+    i = int(np.argmin(mk))  # first minimum (strict < over trials in order)
+    best = Assignment(tuple(int(x) for x in assign[i]), "critical_path")
+    if return_all:
+        return best, float(mk[i]), assign, mk
+    return best
+
+
 class ForcedActions:
     """Teacher that replays a recorded (vertex, device) sequence — the
     teacher-forced parity harness of north_star (one list per episode, or a

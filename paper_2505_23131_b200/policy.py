@@ -295,7 +295,7 @@ class PolicyContext:
                       strategy: str = "fifo", trace_steps: bool = False, grad: bool = False,
                       sim_trace: bool = False, episode_base: int = 0, prepare: bool = True,
                       stream=None, out: RolloutBatch | None = None,
-                      wide: bool = False) -> RolloutBatch:
+                      wide: bool = False, tie_random: bool = False) -> RolloutBatch:
         import torch
 
         if mode not in N.MODE:
@@ -321,7 +321,8 @@ class PolicyContext:
                                        out.step_argmax, out.step_ncand, out.makespan,
                                        out.status, out.grad_rows, out.grad_ep, out.trace)],
             out.trace.shape[1] // 16 if out.trace is not None else 0,
-            N.ptr(out.trace_len).value, N.FLAG_WIDE if wide else 0)
+            N.ptr(out.trace_len).value,
+            (N.FLAG_WIDE if wide else 0) | (N.FLAG_TIE_RANDOM if tie_random else 0))
         ws = self.workspace(B, wide=wide, grad=out.grad_rows is not None)
         args.workspace = N.ptr(ws).value
         args.workspace_bytes = 0 if ws is None else ws.numel()
