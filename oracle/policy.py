@@ -347,9 +347,11 @@ def sample(probs, eps, how):
 
 
 def rollout(P, ctx, eps, mode="uniform", seed=0, episode=0, forced=None, teacher=False,
-            greedy=False):
+            greedy=False, per_step=False):
     """One episode.  mode: "uniform" (Philox draws), "forced" (``forced`` =
     [(v, d)] per step), "teacher" (CriticalPathRule) or "greedy".
+    per_step: re-encode before every decision with the dynamic columns of the
+    vertices placed so far (reference policy.py:353-371).
     Returns dict(assign, steps=[...], lps=[tape], ents=[tape])."""
     g, D = ctx.g, ctx.cl.device_count
     n = len(g)
@@ -357,11 +359,15 @@ def rollout(P, ctx, eps, mode="uniform", seed=0, episode=0, forced=None, teacher
     cands = sorted(g.entry_vertices())
     left = [len(g.preds(v)) for v in range(n)]
     placed, placed_dev = [], []
-    Hs, Hp = encode(P, ctx, "sel"), encode(P, ctx, "plc")
+    dyn = np.zeros((n, 2))
+    if not per_step:
+        Hs, Hp = encode(P, ctx, "sel"), encode(P, ctx, "plc")
     tlev = ctx.f.t_level
     steps, lps, ents = [], [], []
     for t in range(n):
         cand = tuple(cands)
+        if per_step:
+            Hs, Hp = encode(P, ctx, "sel", dyn), encode(P, ctx, "plc", dyn)
         ps = sel_probs(P, ctx, Hs, cands)
         if mode == "forced":
             fv = forced[t][0]
@@ -394,6 +400,8 @@ def rollout(P, ctx, eps, mode="uniform", seed=0, episode=0, forced=None, teacher
             how = ("uniform",) + philox_uniforms(seed, episode, t, 1)
         j, lpp, entp = sample(pp, eps, how)
         tl.commit(v, j)
+        dyn[v, 0] = 1.0
+        dyn[v, 1] = (j + 1) / D
         placed.append(v)
         placed_dev.append(j)
         cands.remove(v)

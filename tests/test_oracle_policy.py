@@ -114,3 +114,39 @@ def test_philox_known_answers():
                                                       0x9B00DBD8]
     assert OP.philox4x32_10((0xFFFFFFFF,) * 4, (0xFFFFFFFF,) * 2) == [
         0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD]
+
+
+def test_oracle_per_step_matches_reference_golden():
+    """per_step message passing (reference policy.py:353-371): the oracle's
+    forced replays of the reference's teacher / greedy / sampled episodes give
+    the recorded log-probs and entropies (1e-10)."""
+    import json
+    from conftest import GOLDEN
+    from helpers import graph_from_golden
+    from oracle import policy as OP
+    from paper_2505_23131_b200.cluster import ClusterSpec
+    from paper_2505_23131_b200.params import init_policy_params
+    from paper_2505_23131_b200.policy import PolicyConfig
+
+    doc = json.loads((GOLDEN / "policy_per_step.json").read_text())
+    for case in doc["cases"]:
+        g = graph_from_golden(case["graph"])
+        cl = ClusterSpec.from_dict(case["cluster"])
+        pc = PolicyConfig.from_dict(case["policy"])
+        assert pc.mp_mode == "per_step"
+        ctx = OP.Ctx(g, cl, pc.hidden, pc.k_rounds, pc.leaky_slope, pc.shared_encoder)
+        P = OP.leaves(init_policy_params(pc, seed=0), need=False)
+        assert case["teacher"]["encode_invocations"] == 2 * len(g)
+        runs = [case["teacher"], case["greedy"]] + case["sampled"]
+        for run in runs:
+            want = run["trace"]
+            ro = OP.rollout(P, ctx, run["epsilon"], mode="forced",
+                            forced=[(w["vertex"], w["device"]) for w in want], per_step=True)
+            for s, w in zip(ro["steps"], want):
+                assert list(s["candidates"]) == w["candidates"]
+                for k in ("sel_logprob", "plc_logprob", "sel_entropy", "plc_entropy"):
+                    assert abs(s[k] - w[k]) <= 1e-10 * max(1.0, abs(w[k])), (case["tag"], k)
+        # the teacher episode itself: CriticalPathRule actions from the oracle
+        ro = OP.rollout(P, ctx, 0.2, mode="teacher", per_step=True)
+        assert [(s["vertex"], s["device"]) for s in ro["steps"]] == \
+            [(w["vertex"], w["device"]) for w in case["teacher"]["trace"]]
