@@ -64,14 +64,14 @@ def workload(name: str):
 # --------------------------------------------------------------------------- CPU
 def _cpu_worker(args):
     """Reference-algorithm episodes on one core until the deadline."""
-    wl, seed0, deadline, train = args
+    wl, seed0, deadline, train, per_step = args
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     from oracle import policy as OP
     from oracle import sim as osim
     from paper_2505_23131_b200.params import init_policy_params
     from paper_2505_23131_b200.policy import PolicyConfig
     g, cl, _ = workload(wl)
-    pc = PolicyConfig()
+    pc = PolicyConfig(mp_mode="per_step" if per_step else "per_episode")
     params = init_policy_params(pc, seed=0)
     ctx = OP.Ctx(g, cl, pc.hidden, pc.k_rounds, pc.leaky_slope, pc.shared_encoder)
     packed = osim.pack(g, [0] * len(g), cl, ctx.f, "fifo", 0)
@@ -83,19 +83,21 @@ def _cpu_worker(args):
                                     seed=seed0, episode=done)
         else:
             ro = OP.rollout(OP.leaves(params), ctx, EPSILON, mode="uniform", seed=seed0,
-                            episode=done)
+                            episode=done, per_step=per_step)
         osim.sim_batch(packed, np.asarray([ro["assign"]], dtype=np.int32))
         done += 1
     return done, time.perf_counter() - t0
 
 
-def cpu_throughput(wl: str, seconds: float, procs: int, train: bool = False):
+def cpu_throughput(wl: str, seconds: float, procs: int, train: bool = False,
+                   per_step: bool = False):
     deadline = time.perf_counter() + seconds
     if procs == 1:
-        res = [_cpu_worker((wl, 1000, deadline, train))]
+        res = [_cpu_worker((wl, 1000, deadline, train, per_step))]
     else:
         with mp.get_context("fork").Pool(procs) as pool:
-            res = pool.map(_cpu_worker, [(wl, 1000 + i, deadline, train) for i in range(procs)])
+            res = pool.map(_cpu_worker, [(wl, 1000 + i, deadline, train, per_step)
+                                         for i in range(procs)])
     eps = sum(r[0] for r in res)
     wall = max(r[1] for r in res)
     return eps / wall, eps, wall
@@ -157,7 +159,7 @@ def run_ours(args):
 
     g, cl, desc = workload(args.workload)
     n = len(g)
-    pc = PolicyConfig()
+    pc = PolicyConfig(mp_mode=args.mp_mode)
     params = init_policy_params(pc, seed=0)
     ctx = PolicyContext(g, cl, pc)
     B = args.batch
@@ -266,13 +268,25 @@ def run_ours(args):
         alg = B * per_ep + per_launch
         if train:
             alg += B * n * 4 * h * 8  # REINFORCE rows written
+        per_step = args.mp_mode == "per_step"
+        K = pc.k_rounds
+        jumps = ctx.jump_rounds() if hasattr(ctx, "jump_rounds") else 0
+        prep_launches = 2 * K + 2 + jumps  # proj0, K x (aggregation, node), [jumps], SEL head
+        if per_step:
+            # per step: 2 encoders x K rounds of aggregation over B*n rows (the
+            # HBM-bound part) -- node MLP traffic not counted
+            M = 2 * len(g.edges)
+            alg = n * K * 2 * (B * M * (8 * h + 12) + B * n * (16 * h + 4))
+            launches = prep_launches + 1 + n * (2 + 2 * K) + 3
+        else:
+            launches = prep_launches + 1
         achieved = alg / (kms * 1e-3) / 1e9
         traffic = None
         tpath = ROOT / "profiles" / "r1_traffic.json"
         if tpath.exists():
             rec = json.loads(tpath.read_text()).get(
                 f"{args.workload}/rollout_kernel{'(grad)' if train else ''}")
-            if rec and rec.get("batch") == B:
+            if rec and rec.get("batch") == B and not per_step:
                 traffic = rec["dram_bytes_read"] + rec["dram_bytes_write"]
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -280,16 +294,18 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (builder graph; random-init policy seed 0; Philox episodes)",
             "config": {"workload": desc, "episodes_per_gpu": B, "global_batch": B * world,
-                       "mode": args.mode, "epsilon": EPSILON, "policy": "hidden 32, K 2",
+                       "mode": args.mode, "epsilon": EPSILON, "policy": f"hidden 32, K 2, {args.mp_mode}",
                        "parallelism": f"episode-dp{world}",
                        "l2": "flushed between timed steps (256 MiB write)"},
             "e2e": {"value": e2e_value, "unit": UNIT,
                     "h2d_bytes_per_step": int(host_params.numel() * 8),
                     "d2h_bytes_per_step": int(B * n * 4 + B * 8)},
-            "gpu_launches": args.steps * ((pc.k_rounds + 2) if not train else
+            "gpu_launches": args.steps * (launches if not train else
                                           trainer.launches_per_step()),
-            "roofline": {"bound": "hbm", "kernel": "rollout_kernel" if not train else
-                         "rollout_kernel(grad)", "achieved": achieved, "peak": peak,
+            "roofline": {"bound": "hbm", "kernel": ("per_step rollout (batched aggregation)"
+                                                    if per_step else "rollout_kernel")
+                         if not train else "rollout_kernel(grad)", "achieved": achieved,
+                         "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "kernel_ms": kms, "alg_bytes_per_launch": alg,
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
@@ -298,7 +314,7 @@ def run_ours(args):
             line["clocks"] = clk.summary(local)
         if world == 1 and not args.no_cpu:
             v, eps_done, wall = cpu_throughput(args.workload, args.cpu_seconds, os.cpu_count(),
-                                               train)
+                                               train, args.mp_mode == "per_step")
             line["cpu_baseline"] = {
                 "value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                 "sample": f"{eps_done} episodes in {wall:.1f}s across {os.cpu_count()} "
@@ -317,10 +333,11 @@ def run_reference(args):
     total_eps = 0
     wall = 0.0
     for _ in range(args.warmup):
-        cpu_throughput(args.workload, 1.0, procs, args.mode == "train")
+        cpu_throughput(args.workload, 1.0, procs, args.mode == "train",
+                       args.mp_mode == "per_step")
     for _ in range(args.steps):
         v, e, w = cpu_throughput(args.workload, args.ref_step_seconds, procs,
-                                 args.mode == "train")
+                                 args.mode == "train", args.mp_mode == "per_step")
         vals.append(v)
         total_eps += e
         wall += w
@@ -331,7 +348,8 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": desc, "mode": args.mode,
-                                        "epsilon": EPSILON, "policy": "hidden 32, K 2"},
+                                        "epsilon": EPSILON,
+                                        "policy": f"hidden 32, K 2, {args.mp_mode}"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port",
                          "sample": f"{total_eps} episodes over {args.steps} steps of "
                                    f"{args.ref_step_seconds}s on {procs} processes"},
@@ -348,6 +366,8 @@ def main():
     ap.add_argument("--workload", default="ffnn")
     ap.add_argument("--batch", type=int, default=1024)
     ap.add_argument("--mode", default="rollout", choices=("rollout", "train"))
+    ap.add_argument("--mp-mode", default="per_episode", choices=("per_episode", "per_step"),
+                    help="message passing once per snapshot (reference default) or per step")
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-step-seconds", type=float, default=5.0)

@@ -41,6 +41,9 @@ extern "C" {
 /* launch flags (fp_sim_batch flags, fp_rollout_args.flags) */
 #define FP_FLAG_WIDE 1  /* force the HBM-resident (wide) episode path even when the
                            compact shared-memory path would fit (tests / benchmarks) */
+#define FP_FLAG_PER_STEP 4   /* mp_mode = "per_step" (policy.py:353-371): re-encode both
+                                GNNs with the placement columns before every decision
+                                (B x n-row batched encode per step; forward only) */
 #define FP_FLAG_TIE_RANDOM 2 /* FP_MODE_TEACHER: break equal-t-level selection ties
                                 uniformly at random (Philox), as critical_path_assign's
                                 trials do (heuristics.py:76-83, 114-117) */

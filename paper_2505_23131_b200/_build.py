@@ -46,7 +46,9 @@ def build(force: bool = False, verbose: bool = False, profile: bool = False) -> 
     lib = PROF_LIB if profile else LIB
     if not force and not stale(lib):
         return lib
-    objdir = PKG / ("build_prof" if profile else "build")
+    # objects outside the tree: only the linked .so travels to the GPU box
+    import tempfile
+    objdir = Path(tempfile.gettempdir()) / ("fp_b200_build_prof" if profile else "fp_b200_build")
     objdir.mkdir(exist_ok=True)
     objs = []
     flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",

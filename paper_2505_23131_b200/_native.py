@@ -18,6 +18,7 @@ FP_OK, FP_ERR_INVALID, FP_ERR_CUDA, FP_ERR_UNSUPPORTED, FP_ERR_DEADLOCK, FP_ERR_
 EP_OK, EP_DEADLOCK, EP_TRACE_OVERFLOW, EP_BAD_ACTION = range(4)
 FLAG_WIDE = 1  # force the HBM-resident episode path
 FLAG_TIE_RANDOM = 2  # teacher mode: random tie-breaks among equal t-levels
+FLAG_PER_STEP = 4  # mp_mode="per_step": re-encode before every decision
 
 _lib = None
 

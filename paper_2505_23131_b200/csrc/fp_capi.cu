@@ -145,6 +145,13 @@ static int launch_sim(const fp_problem *p, const int32_t *assign, int B, int str
 #undef FP_SIM_ARGS
 }
 
+int sim_launch_compact(const fp_problem *p, const int32_t *assign, int B, int strategy,
+                       double *makespan, int32_t *status, fp_event *trace, int trace_cap,
+                       int32_t *trace_len, cudaStream_t stream) {
+    return launch_sim(p, assign, B, strategy, nullptr, 0, makespan, status, trace, trace_cap,
+                      trace_len, nullptr, nullptr, 0, 0, nullptr, stream);
+}
+
 }  // namespace fp
 
 using namespace fp;

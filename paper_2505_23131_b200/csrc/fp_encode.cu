@@ -491,12 +491,12 @@ static int launch_encode(DevPolicy &P, cudaStream_t st) {
 // Split encoder: aggregation kernels (HBM) + DMMA node-MLP kernels, for
 // hidden widths that tile by 8 (every PolicyConfig the reference ships).
 template <int H, bool BWD>
-static int launch_gnn_tc(DevPolicy &P, cudaStream_t st) {
+static int launch_gnn_tc(DevPolicy &P, cudaStream_t st, bool sel_head = true) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int warps = 8, threads = warps * 32;
-    const int tiles = (P.n + 7) / 8;
+    const int tiles = (P.rows + 7) / 8;
     const int tile_blocks = (tiles + warps - 1) / warps;
     auto grid_for = [&](const void *kern, int64_t smem, int want) {
         int occ = 1;
@@ -518,7 +518,7 @@ static int launch_gnn_tc(DevPolicy &P, cudaStream_t st) {
         FP_CUDA_RET(cudaGetLastError());
     }
     constexpr int VPW = H / 2 >= 32 ? 1 : 32 / (H / 2);
-    const int agg_blocks = (P.n + 8 * VPW - 1) / (8 * VPW);
+    const int agg_blocks = (P.rows + 8 * VPW - 1) / (8 * VPW);
     for (int k = 0; k < P.K; ++k) {
         const bool last = k == P.K - 1;
         {
@@ -537,6 +537,7 @@ static int launch_gnn_tc(DevPolicy &P, cudaStream_t st) {
             gnn_node_kernel<H, false, BWD><<<grid, threads, smem, st>>>(P, k, last);
         FP_CUDA_RET(cudaGetLastError());
     }
+    if (!sel_head) return FP_OK;
     if (P.forest)
         for (int r = 0; r < P.jump_rounds; ++r) {
             const int64_t total = (int64_t)P.n * H;
@@ -560,6 +561,18 @@ static int launch_gnn_tc(DevPolicy &P, cudaStream_t st) {
 template <int H>
 static int launch_gnn_tc_any(DevPolicy &P, cudaStream_t st) {
     return P.forest ? launch_gnn_tc<H, false>(P, st) : launch_gnn_tc<H, true>(P, st);
+}
+
+int gnn_encode_rows(DevPolicy &P, cudaStream_t st, bool bwd, bool sel_head) {
+    switch (P.h) {
+#define FP_CASE(HH) \
+        case HH: return bwd ? launch_gnn_tc<HH, true>(P, st, sel_head) : launch_gnn_tc<HH, false>(P, st, sel_head);
+        FP_CASE(8) FP_CASE(16) FP_CASE(32) FP_CASE(64)
+#undef FP_CASE
+        default:
+            set_error("the batched encoder needs hidden in {8, 16, 32, 64}");
+            return FP_ERR_UNSUPPORTED;
+    }
 }
 
 int policy_prepare(fp_policy *pol, const double *params, cudaStream_t st) {
@@ -743,6 +756,7 @@ int fp_policy_create(const fp_problem *p, const fp_policy_desc *desc, fp_policy 
     DevPolicy &P = pol->dev;
     std::memset(&P, 0, sizeof(P));
     P.n = n; P.h = h; P.K = K; P.n_enc = n_enc; P.slope = desc->leaky_slope;
+    P.rows = n; P.batch = 1; P.D = p->dev.d; P.ps_dev = nullptr;
     for (int r = 0; r < PR_COUNT; ++r) P.off[r] = desc->param_offsets[r];
     P.x = (const double *)(b + o_x);
     P.adj_ptr = (const int *)(b + o_ap); P.adj_nbr = (const int *)(b + o_an);

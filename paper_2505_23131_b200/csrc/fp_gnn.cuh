@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(256) gnn_agg_kernel(DevPolicy P, int k) {
     const int lane = lane_id();
     const int sub = HL >= 32 ? 0 : lane / HL;
     const int l = HL >= 32 ? lane : lane % HL;
-    const int n = P.n;
+    const int n = P.n, rows = P.rows;
     const int dk = k == 0 ? 7 : H;
     const double *psw = P.W(gnn_role(e, k, 0)), *psb = P.W(gnn_role(e, k, 1));
     // parameter rows sit at arbitrary offsets of the flat vector: scalar loads
@@ -97,10 +97,11 @@ __global__ void __launch_bounds__(256) gnn_agg_kernel(DevPolicy P, int k) {
     const double s = P.slope;
     const int warps = blockDim.x >> 5;
     const int gw = blockIdx.x * warps + (threadIdx.x >> 5);
-    for (int vb = gw * VPW; vb < n; vb += gridDim.x * warps * VPW) {
-        const int v = vb + sub;
-        if (v >= n || (HL < 32 && lane >= VPW * HL)) continue;
-        const double2 q = Qm[(size_t)v * HL + l];
+    for (int vb = gw * VPW; vb < rows; vb += gridDim.x * warps * VPW) {
+        const int r = vb + sub;  // row = episode * n + vertex
+        if (r >= rows || (HL < 32 && lane >= VPW * HL)) continue;
+        const int v = r % n, base = r - v;
+        const double2 q = Qm[(size_t)r * HL + l];
         double ax = 0.0, ay = 0.0;
         const int m1 = P.adj_ptr[v + 1];
         for (int m = P.adj_ptr[v]; m < m1; m += 4) {
@@ -109,7 +110,7 @@ __global__ void __launch_bounds__(256) gnn_agg_kernel(DevPolicy P, int k) {
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const bool ok = m + u < m1;
-                w[u] = ok ? P.adj_nbr[m + u] : 0;
+                w[u] = ok ? base + P.adj_nbr[m + u] : base;
                 ev[u] = ok ? P.adj_e[m + u] : 0.0;
             }
             double2 p[4];
@@ -124,7 +125,7 @@ __global__ void __launch_bounds__(256) gnn_agg_kernel(DevPolicy P, int k) {
                     ay += gleaky(p[u].y + q.y + ev[u] * we.y + bb.y, s);
                 }
         }
-        agg[(size_t)v * HL + l] = make_double2(ax, ay);
+        agg[(size_t)r * HL + l] = make_double2(ax, ay);
     }
 }
 
@@ -143,20 +144,33 @@ __global__ void __launch_bounds__(256) gnn_proj0_kernel(DevPolicy P) {
         return j < H ? psw[kk * H + j] : psw[(7 + kk) * H + (j - H)];
     });
     __syncthreads();
-    const double *H0 = P.H[e][0];
+    double *H0 = P.H[e][0];
     const int r = lane >> 2, c = lane & 3;
-    for (int tile = blockIdx.x * warps + warp; tile * 8 < n; tile += gridDim.x * warps) {
-        const int v = tile * 8 + r;
+    const int rows = P.rows;
+    for (int tile = blockIdx.x * warps + warp; tile * 8 < rows; tile += gridDim.x * warps) {
+        const int v = tile * 8 + r;  // row
         double acc[NT2][2];
         zero_acc(acc);
 #pragma unroll
         for (int kt = 0; kt < 2; ++kt) {
             const int col = kt * 4 + c;
-            const double a = v < n && col < 7 ? H0[(size_t)v * 7 + col] : 0.0;
+            double a = 0.0;
+            if (v < rows && col < 7) {
+                if (P.ps_dev) {
+                    // per_step input row [x_static | dyn], dyn = (1, (d+1)/D) once
+                    // placed (reference policy.py:390-391); materialised for phi
+                    const int dv = P.ps_dev[v];
+                    a = col < 5 ? P.x[(size_t)(v % n) * 5 + col]
+                        : dv < 0 ? 0.0 : col == 5 ? 1.0 : __ddiv_rn((double)(dv + 1), (double)P.D);
+                    H0[(size_t)v * 7 + col] = a;
+                } else {
+                    a = H0[(size_t)v * 7 + col];
+                }
+            }
 #pragma unroll
             for (int nt = 0; nt < NT2; ++nt) dmma(acc[nt], a, Bf[(kt * NT2 + nt) * 32 + lane]);
         }
-        if (v < n) {
+        if (v < rows) {
 #pragma unroll
             for (int nt = 0; nt < NT2; ++nt) {
                 const int col = nt * 8 + c * 2;
@@ -246,9 +260,10 @@ __global__ void __launch_bounds__(256, 2) gnn_node_kernel(DevPolicy P, int k, in
     const double *Hk = P.H[e][k];
     const double *agg = P.AG[e][k];
     const int r = lane >> 2, c = lane & 3, c2 = c * 2;
-    for (int tile = blockIdx.x * warps + warp; tile * 8 < n; tile += gridDim.x * warps) {
-        const int v = tile * 8 + r;
-        const bool vok = v < n;
+    const int rows = P.rows;
+    for (int tile = blockIdx.x * warps + warp; tile * 8 < rows; tile += gridDim.x * warps) {
+        const int v = tile * 8 + r;  // row (= vertex unless batched)
+        const bool vok = v < rows;
         // ---- phi: A = [H_k | agg] (8 x K1) from global, fragments in registers ----
         double a1[KT1];
 #pragma unroll
@@ -304,7 +319,7 @@ __global__ void __launch_bounds__(256, 2) gnn_node_kernel(DevPolicy P, int k, in
 #pragma unroll
         for (int kt = 0; kt < 2; ++kt) {
             const int col = kt * 4 + c;
-            ax[kt] = vok && col < 5 ? P.x[(size_t)v * 5 + col] : 0.0;
+            ax[kt] = vok && col < 5 ? P.x[(size_t)(v % n) * 5 + col] : 0.0;
         }
         if (feeds_sel) {
             const double *zb = P.W(PR_SEL_Z_B);

@@ -1,0 +1,554 @@
+// per_step message passing (reference policy.py:353-371, mp_mode="per_step";
+// Appendix I of the paper): both encoders re-run before EVERY decision with
+// the dynamic input columns dyn[v] = (1, (d+1)/D) of the vertices placed so
+// far, so SEL logits and the PLC tables change every step and nothing can be
+// precomputed per snapshot.  This is the genuinely batched GNN workload: the
+// B episodes advance in lockstep, and each step is
+//
+//   1. one encode of all B x n rows (gnn_proj0 with the per-episode dyn
+//      columns, then K x (aggregation + DMMA node MLPs) -- the same kernels
+//      as the per-snapshot encoder, run over a B*n-row batch);
+//   2. ps_step_kernel, one warp per episode: SEL logits of the current
+//      candidates from this step's H_sel (path sums over the explicit b/t
+//      path lists, head1 as a lane-per-column mat-vec), masked softmax +
+//      decision, then the PLC step on this step's A / G rows
+//      (h_d = sum of G over the vertices placed on d, recomputed because G
+//      changed), device features, standardisation, softmax over devices,
+//      decision, timeline commit -- the per_episode kernels' math, with the
+//      episode state in the workspace between launches.
+//
+// After n steps the assignments are scored by the compact simulator.
+// Forward only (sampling / greedy / forced / teacher, log-probs, entropies):
+// the per_step REINFORCE backward would differentiate through n encodes.
+#include "fp_rollout.cuh"
+
+namespace fp {
+
+constexpr int kPsWarps = 4;
+
+struct PsState {
+    int *dev;        // [B*n] device of each vertex, -1 unplaced (also the dyn columns)
+    int *npl;        // [B*n] unplaced predecessors
+    uint32_t *cand;  // [B][W] candidate bitsets
+    int *order;      // [B*n] placement order
+    double *tstart, *tend;   // [B*n] timeline
+    double *avail, *aflops;  // [B][32]
+    int *cid;        // [B*n] candidate list scratch
+    double *cs;      // [B*n] candidate logits scratch
+    int *stat;       // [B] FP_EP_* (non-zero: episode stopped)
+};
+
+struct PsLayout {
+    int64_t dev, npl, cand, order, tstart, tend, avail, aflops, cid, cs, stat;
+    int64_t H[2][kMaxRounds + 1], Pm[2][kMaxRounds], Qm[2][kMaxRounds], AG[2][kMaxRounds];
+    int64_t Zs, A, G;
+    int64_t bytes;
+};
+
+static PsLayout ps_layout(int n, int B, int h, int K, int n_enc, int W) {
+    PsLayout L{};
+    int64_t o = 0;
+    const int64_t R = (int64_t)n * B;
+    auto take = [&](int64_t bytes) {
+        o = (o + 255) / 256 * 256;
+        const int64_t at = o;
+        o += std::max<int64_t>(bytes, 8);
+        return at;
+    };
+    L.dev = take(4 * R); L.npl = take(4 * R); L.cand = take(4LL * B * W); L.order = take(4 * R);
+    L.tstart = take(8 * R); L.tend = take(8 * R);
+    L.avail = take(8LL * B * 32); L.aflops = take(8LL * B * 32);
+    L.cid = take(4 * R); L.cs = take(8 * R); L.stat = take(4LL * B);
+    for (int e = 0; e < n_enc; ++e) {
+        L.H[e][0] = take(8 * R * 7);
+        for (int k = 0; k < K; ++k) {
+            L.H[e][k + 1] = take(8 * R * h);
+            L.Pm[e][k] = take(8 * R * h);
+            L.Qm[e][k] = take(8 * R * h);
+            L.AG[e][k] = take(8 * R * h);
+        }
+    }
+    L.Zs = take(8 * R * h); L.A = take(8 * R * h); L.G = take(8 * R * h);
+    L.bytes = (o + 255) / 256 * 256;
+    return L;
+}
+
+__global__ void ps_init_kernel(DevProblem PR, PsState S, int B) {
+    const int lane = lane_id();
+    const int ep = blockIdx.x * kPsWarps + (threadIdx.x >> 5);
+    if (ep >= B) return;
+    const int n = PR.n, W = PR.W;
+    const size_t base = (size_t)ep * n;
+    for (int w = lane; w < W; w += 32) S.cand[(size_t)ep * W + w] = 0u;
+    if (lane < 32) { S.avail[ep * 32 + lane] = 0.0; S.aflops[ep * 32 + lane] = 0.0; }
+    __syncwarp();
+    for (int v = lane; v < n; v += 32) {
+        const int np = PR.pred_ptr[v + 1] - PR.pred_ptr[v];
+        S.dev[base + v] = -1;
+        S.npl[base + v] = np;
+        S.tstart[base + v] = 0.0;
+        S.tend[base + v] = 0.0;
+        if (np == 0) atomicOr(&S.cand[(size_t)ep * W + (v >> 5)], 1u << (v & 31));
+    }
+    if (lane == 0) S.stat[ep] = FP_EP_OK;
+}
+
+// One decision step (SEL then PLC) of every live episode.
+template <int MAXD, int HPL>
+__global__ void __launch_bounds__(kPsWarps * 32)
+ps_step_kernel(DevProblem PR, DevPolicy PO, DevPolicy PB, fp_rollout_args A, PsState S,
+               int step) {
+    constexpr int LOGD = PlcLog<MAXD>::v;
+    __shared__ double xd_sm[kPsWarps][32 * 5], xn_sm[kPsWarps][32 * 5], st_sm[kPsWarps][16];
+    const int lane = lane_id(), warp = threadIdx.x >> 5;
+    const int ep = blockIdx.x * kPsWarps + warp;
+    if (ep >= A.B || S.stat[ep] != FP_EP_OK) return;
+    const int n = PR.n, W = PR.W, D = PR.d, h = PO.h;
+    const size_t base = (size_t)ep * n;
+    const double eps = A.epsilon, ome = 1.0 - eps, slope = PO.slope;
+    const uint32_t k0 = (uint32_t)A.seed, k1 = (uint32_t)(A.seed >> 32);
+    const uint32_t ctr_ep = A.episode_base + (uint32_t)ep;
+    const int mode = A.mode;
+    const bool want_lp = A.step_lp != nullptr || A.step_ent != nullptr;
+    const bool want_amax = A.step_argmax != nullptr;
+    const size_t o = base + step;
+    const double *Hs = PB.H[0][PO.K];
+    int *cid = S.cid + base;
+    double *cs = S.cs + base;
+    uint32_t *cand = S.cand + (size_t)ep * W;
+
+    // ---------------- SEL: logits of the current candidates ----------------
+    const uint32_t cw = lane < W ? cand[lane] : 0u;
+    const int pc = __popc(cw);
+    const int incl = warp_inclusive_scan(pc);
+    const int k = __shfl_sync(FP_FULL_MASK, incl, 31);
+    if (k == 0) {
+        if (lane == 0) S.stat[ep] = FP_EP_DEADLOCK;
+        return;
+    }
+    {
+        int q = incl - pc;
+        uint32_t m = cw;
+        while (m) {
+            const int b = __ffs(m) - 1;
+            m &= m - 1;
+            cid[q++] = lane * 32 + b;
+        }
+    }
+    __syncwarp();
+    const double *w1 = PO.W(PR_SEL_H1_W), *b1 = PO.W(PR_SEL_H1_B), *w2 = PO.W(PR_SEL_H2_W);
+    const double b2 = PO.W(PR_SEL_H2_B)[0];
+    for (int i = 0; i < k; ++i) {
+        const int v = cid[i];
+        double em[4][HPL];
+#pragma unroll
+        for (int t = 0; t < HPL; ++t) {
+            const int j = lane + 32 * t;
+            em[0][t] = em[1][t] = em[2][t] = em[3][t] = 0.0;
+            if (j >= h) continue;
+            em[0][t] = Hs[(base + v) * h + j];
+            double hb = 0.0, ht = 0.0;
+            for (int q = PO.bp_ptr[v]; q < PO.bp_ptr[v + 1]; ++q) hb += Hs[(base + PO.bp_idx[q]) * h + j];
+            for (int q = PO.tp_ptr[v]; q < PO.tp_ptr[v + 1]; ++q) ht += Hs[(base + PO.tp_idx[q]) * h + j];
+            em[1][t] = hb;
+            em[2][t] = ht;
+            em[3][t] = PB.Zs[(base + v) * h + j];
+        }
+        double acc[HPL];
+#pragma unroll
+        for (int t = 0; t < HPL; ++t) acc[t] = 0.0;
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+            for (int ii = 0; ii < h; ++ii) {
+                double ev = 0.0;
+#pragma unroll
+                for (int t = 0; t < HPL; ++t) {
+                    const double x = __shfl_sync(FP_FULL_MASK, em[b][t], ii & 31);
+                    if ((ii >> 5) == t) ev = x;
+                }
+#pragma unroll
+                for (int t = 0; t < HPL; ++t) {
+                    const int j = lane + 32 * t;
+                    if (j < h) acc[t] = fma(ev, w1[(b * h + ii) * h + j], acc[t]);
+                }
+            }
+        double part = 0.0;
+#pragma unroll
+        for (int t = 0; t < HPL; ++t) {
+            const int j = lane + 32 * t;
+            if (j < h) part = fma(lk(acc[t] + b1[j], slope), w2[j], part);
+        }
+        part = warp_sum(part);
+        if (lane == 0) cs[i] = part + b2;
+    }
+    __syncwarp();
+    // masked softmax over the candidates in ascending-id order (policy.py:204)
+    double mx = -INFINITY;
+    for (int i = lane; i < k; i += 32) mx = fmax(mx, cs[i]);
+    mx = warp_max_redux(mx);
+    double tot = 0.0;
+    {
+        double carry = 0.0;
+        for (int b0 = 0; b0 < k; b0 += 32) {
+            const int i = b0 + lane;
+            const double e = i < k ? exp(cs[i] - mx) : 0.0;
+            const double cum = warp_inclusive_scan(e) + carry;
+            carry = __shfl_sync(FP_FULL_MASK, cum, 31);
+        }
+        tot = carry;
+    }
+    int idx = -1;
+    double su1 = 0.0, su2 = 0.0;
+    if (mode == FP_MODE_SAMPLE)
+        uniform2(philox4x32_10(U4{ctr_ep, (uint32_t)step, 0u, 0u}, k0, k1), su1, su2);
+    if (mode == FP_MODE_FORCED) {
+        const int fv = A.forced[2 * o];
+        for (int b0 = 0; b0 < k && idx < 0; b0 += 32) {
+            const unsigned hit = __ballot_sync(FP_FULL_MASK, b0 + lane < k && cid[b0 + lane] == fv);
+            if (hit) idx = b0 + __ffs(hit) - 1;
+        }
+    } else if (mode == FP_MODE_TEACHER) {
+        double bt = -INFINITY;
+        for (int i = lane; i < k; i += 32) bt = fmax(bt, PR.tlev[cid[i]]);
+        bt = warp_max_redux(bt);
+        for (int b0 = 0; b0 < k && idx < 0; b0 += 32) {
+            const unsigned hit =
+                __ballot_sync(FP_FULL_MASK, b0 + lane < k && PR.tlev[cid[b0 + lane]] == bt);
+            if (hit) idx = b0 + __ffs(hit) - 1;
+        }
+    } else if (mode == FP_MODE_SAMPLE) {
+        if (su1 < eps) {
+            idx = min((int)(su2 * (double)k), k - 1);
+        } else {
+            const double target = su2 * tot;
+            double carry = 0.0;
+            for (int b0 = 0; b0 < k && idx < 0; b0 += 32) {
+                const int i = b0 + lane;
+                const double e = i < k ? exp(cs[i] - mx) : 0.0;
+                const double cum = warp_inclusive_scan(e) + carry;
+                const unsigned hit = __ballot_sync(FP_FULL_MASK, i < k && cum > target);
+                if (hit) idx = b0 + __ffs(hit) - 1;
+                carry = __shfl_sync(FP_FULL_MASK, cum, 31);
+            }
+            if (idx < 0) idx = k - 1;
+        }
+    }
+    int amax = -1;
+    if (want_amax || mode == FP_MODE_GREEDY) {
+        double bp = -1.0;
+        int bi = 0x7fffffff;
+        for (int i = lane; i < k; i += 32) {
+            const double p = exp(cs[i] - mx) / tot;
+            if (p > bp) { bp = p; bi = i; }
+        }
+        warp_argmax_first(bp, bi);
+        amax = bi;
+        if (mode == FP_MODE_GREEDY) idx = amax;
+    }
+    if (idx < 0) {
+        if (lane == 0) S.stat[ep] = FP_EP_BAD_ACTION;
+        return;
+    }
+    const int v = cid[idx];
+    if (want_lp) {
+        const double ek = eps / (double)k;
+        double entp = 0.0, lp = 0.0;
+        for (int i = lane; i < k; i += 32) {
+            const double p = exp(cs[i] - mx) / tot;
+            const double mix = __dadd_rn(__dmul_rn(p, ome), ek);
+            const double lm = log(__dadd_rn(mix, 1e-30));
+            entp += mix * lm;
+            if (i == idx) lp = lm;
+        }
+        const double ent = -warp_sum(entp);
+        lp = warp_sum(lp);
+        if (lane == 0) {
+            if (A.step_lp) A.step_lp[2 * o] = lp;
+            if (A.step_ent) A.step_ent[2 * o] = ent;
+        }
+    }
+    if (lane == 0) {
+        if (A.step_vd) A.step_vd[2 * o] = v;
+        if (A.step_argmax) A.step_argmax[2 * o] = cid[amax];
+        if (A.step_ncand) A.step_ncand[o] = k;
+        cand[v >> 5] &= ~(1u << (v & 31));
+    }
+    __syncwarp();
+    for (int j = PR.succ_ptr[v] + lane; j < PR.succ_ptr[v + 1]; j += 32) {
+        const int w = PR.succ_idx[j];
+        if (atomicSub(&S.npl[base + w], 1) == 1) atomicOr(&cand[w >> 5], 1u << (w & 31));
+    }
+
+    // ---------------- PLC ----------------
+    double *xd = xd_sm[warp], *xn = xn_sm[warp], *stats = st_sm[warp];
+    const int *pp = PR.pred_ptr, *pi = PR.pred_idx;
+    const uint8_t *ent = PR.is_entry;
+    double f4 = 0.0;
+    if (lane < D) {
+        double f1 = 0.0, f2 = 0.0, f3 = 0.0;
+        bool any_local = false;
+        for (int j = pp[v]; j < pp[v + 1]; ++j) {
+            const int p = pi[j];
+            const int dp = S.dev[base + p];
+            const double arr =
+                ent[p] ? 0.0 : __dadd_rn(S.tend[base + p], PR.tdur[(p * D + dp) * D + lane]);
+            f3 = j == pp[v] ? arr : fmax(f3, arr);
+            if (dp == lane) {
+                f1 = __dadd_rn(f1, PR.flops[p]);
+                f2 = any_local ? fmin(f2, S.tstart[base + p]) : S.tstart[base + p];
+                any_local = true;
+            }
+        }
+        f4 = fmax(S.avail[ep * 32 + lane], f3);
+        double *xr = xd + lane * 5;
+        xr[0] = S.aflops[ep * 32 + lane]; xr[1] = f1; xr[2] = f2; xr[3] = f3; xr[4] = f4;
+    }
+    __syncwarp();
+    if (lane < 5) {
+        double sum = 0.0;
+        for (int d = 0; d < D; ++d) sum = __dadd_rn(sum, xd[d * 5 + lane]);
+        const bool pow2 = (D & (D - 1)) == 0;
+        const double invD = 1.0 / (double)D;
+        const double mean = pow2 ? __dmul_rn(sum, invD) : __ddiv_rn(sum, (double)D);
+        double sq = 0.0;
+        for (int d = 0; d < D; ++d) {
+            const double df = __dsub_rn(xd[d * 5 + lane], mean);
+            sq = __dadd_rn(sq, __dmul_rn(df, df));
+        }
+        const double sd = __dsqrt_rn(pow2 ? __dmul_rn(sq, invD) : __ddiv_rn(sq, (double)D));
+        stats[lane] = mean;
+        stats[5 + lane] = 1.0 / (sd < 1e-12 ? 1.0 : sd);
+    }
+    __syncwarp();
+    for (int i = lane; i < 5 * D; i += 32) {
+        const int c = i % 5;
+        xn[i] = __dmul_rn(__dsub_rn(xd[i], stats[c]), stats[5 + c]);
+    }
+    __syncwarp();
+    // h_d = sum of this step's G rows over the vertices placed on d
+    double Sd[MAXD][HPL];
+#pragma unroll
+    for (int d = 0; d < MAXD; ++d)
+#pragma unroll
+        for (int t = 0; t < HPL; ++t) Sd[d][t] = 0.0;
+    for (int i = 0; i < step; ++i) {
+        const int u = S.order[base + i];
+        const int du = S.dev[base + u];
+#pragma unroll
+        for (int t = 0; t < HPL; ++t) {
+            const int j = lane + 32 * t;
+            const double g = j < h ? PB.G[(base + u) * h + j] : 0.0;
+#pragma unroll
+            for (int d = 0; d < MAXD; ++d)
+                if (d == du) Sd[d][t] += g;
+        }
+    }
+    const double *w2p = PO.W(PR_PLC_H2_W);
+    const double b2p = PO.W(PR_PLC_H2_B)[0];
+    double part[MAXD];
+#pragma unroll
+    for (int d = 0; d < MAXD; ++d) {
+        part[d] = 0.0;
+        if (d < D) {
+#pragma unroll
+            for (int t = 0; t < HPL; ++t) {
+                const int j = lane + 32 * t;
+                if (j >= h) continue;
+                double a = PB.A[(base + v) * h + j] + Sd[d][t] + PO.c[j];
+#pragma unroll
+                for (int c = 0; c < 5; ++c) a = fma(xn[d * 5 + c], PO.M[c * h + j], a);
+                part[d] = fma(lk(a, slope), w2p[j], part[d]);
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < LOGD; ++r) {
+        const int off = 16 >> r;
+        const bool upper = (lane & off) != 0;
+        const int half = MAXD >> (r + 1);
+#pragma unroll
+        for (int i = 0; i < MAXD / 2; ++i) {
+            if (i < half) {
+                const double send = upper ? part[i] : part[i + half];
+                const double keep = upper ? part[i + half] : part[i];
+                part[i] = keep + __shfl_xor_sync(FP_FULL_MASK, send, off);
+            }
+        }
+    }
+#pragma unroll
+    for (int off = 16 >> LOGD; off > 0; off >>= 1) part[0] += __shfl_xor_sync(FP_FULL_MASK, part[0], off);
+    const double lgall = __shfl_sync(FP_FULL_MASK, part[0], (lane & (MAXD - 1)) << (5 - LOGD));
+    const double lg = lane < D ? lgall + b2p : -INFINITY;
+    const double lmx = warp_max_redux(lg);
+    const double ed = lane < D ? exp(lg - lmx) : 0.0;
+    const double ecum = warp_scan_pow2<LOGD>(ed);
+    const double etot = __shfl_sync(FP_FULL_MASK, ecum, D - 1);
+    const double pd = lane < D ? ed / etot : -1.0;
+    int pam = -1;
+    if (want_amax || mode == FP_MODE_GREEDY) {
+        double am = pd;
+        int ai = lane < D ? lane : 0x7fffffff;
+        warp_argmax_first(am, ai);
+        pam = ai;
+    }
+    int jdx;
+    if (mode == FP_MODE_FORCED) {
+        jdx = A.forced[2 * o + 1];
+        if (jdx < 0 || jdx >= D) {
+            if (lane == 0) S.stat[ep] = FP_EP_BAD_ACTION;
+            return;
+        }
+    } else if (mode == FP_MODE_TEACHER) {
+        const double tv = lane < D ? f4 : INFINITY;
+        const double best = warp_min_redux(tv);
+        jdx = __ffs(__ballot_sync(FP_FULL_MASK, lane < D && tv == best)) - 1;
+    } else if (mode == FP_MODE_GREEDY) {
+        jdx = pam;
+    } else {
+        double u1, u2;
+        uniform2(philox4x32_10(U4{ctr_ep, (uint32_t)step, 1u, 0u}, k0, k1), u1, u2);
+        if (u1 < eps) {
+            jdx = min((int)(u2 * (double)D), D - 1);
+        } else {
+            const unsigned hit = __ballot_sync(FP_FULL_MASK, lane < D && ecum > u2 * etot);
+            jdx = hit ? __ffs(hit) - 1 : D - 1;
+        }
+    }
+    if (want_lp) {
+        const double ekd = eps / (double)D;
+        double mixd = 0.0, lmd = 0.0;
+        if (lane < D) {
+            mixd = __dadd_rn(__dmul_rn(pd, ome), ekd);
+            lmd = log(__dadd_rn(mixd, 1e-30));
+        }
+        const double entv = -warp_sum(lane < D ? mixd * lmd : 0.0);
+        const double lp = __shfl_sync(FP_FULL_MASK, lmd, jdx);
+        if (lane == 0) {
+            if (A.step_lp) A.step_lp[2 * o + 1] = lp;
+            if (A.step_ent) A.step_ent[2 * o + 1] = entv;
+        }
+    }
+    // commit (timeline.py:47-58) + the dyn columns of the next encode
+    if (lane == jdx) {
+        S.aflops[ep * 32 + jdx] = __dadd_rn(S.aflops[ep * 32 + jdx], PR.flops[v]);
+        if (!ent[v]) {
+            const double en = __dadd_rn(f4, PR.edur[v * D + jdx]);
+            S.tstart[base + v] = f4;
+            S.tend[base + v] = en;
+            S.avail[ep * 32 + jdx] = en;
+        }
+        S.dev[base + v] = jdx;
+        S.order[base + step] = v;
+        if (A.step_vd) A.step_vd[2 * o + 1] = jdx;
+    }
+    if (lane == 0 && A.step_argmax) A.step_argmax[2 * o + 1] = pam;
+}
+
+// assignments out (unplaced -> 0 for the simulator, fixed up afterwards)
+__global__ void ps_finish_kernel(PsState S, fp_rollout_args A, int n, int fixup) {
+    const int64_t total = (int64_t)A.B * n;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int ep = (int)(i / n);
+        const int d = S.dev[i];
+        if (!fixup) {
+            A.assign[i] = d < 0 ? 0 : d;
+        } else if (S.stat[ep] != FP_EP_OK) {
+            A.assign[i] = d;
+            if (i % n == 0) {
+                A.status[ep] = S.stat[ep];
+                if (A.makespan) A.makespan[ep] = 0.0;
+            }
+        }
+    }
+}
+
+template <int MAXD, int HPL>
+static void ps_launch_step(const fp_problem *p, const fp_policy *pol, const DevPolicy &PB,
+                           const fp_rollout_args &a, const PsState &S, int step,
+                           cudaStream_t st) {
+    ps_step_kernel<MAXD, HPL><<<(a.B + kPsWarps - 1) / kPsWarps, kPsWarps * 32, 0, st>>>(
+        p->dev, pol->dev, PB, a, S, step);
+}
+
+int per_step_rollout(const fp_problem *p, const fp_policy *pol, const fp_rollout_args &a,
+                     int64_t *ws_needed, cudaStream_t st) {
+    const DevProblem &PR = p->dev;
+    const DevPolicy &PO = pol->dev;
+    if (PO.forest || PR.n > 1024) {
+        set_error("per_step message passing supports graphs up to 1024 ops");
+        return FP_ERR_UNSUPPORTED;
+    }
+    if (a.grad_rows) {
+        set_error("per_step rollouts are forward only (no REINFORCE rows)");
+        return FP_ERR_UNSUPPORTED;
+    }
+    if (PO.h % 8 != 0 || PO.h > 64) {
+        set_error("per_step message passing needs hidden in {8, 16, 32, 64}");
+        return FP_ERR_UNSUPPORTED;
+    }
+    const int n = PR.n, B = a.B;
+    const PsLayout L = ps_layout(n, B, PO.h, PO.K, PO.n_enc, PR.W);
+    if (ws_needed) { *ws_needed = L.bytes; return FP_OK; }
+    if (!a.workspace || a.workspace_bytes < L.bytes) {
+        set_error("workspace too small for the per_step rollout (see fp_rollout_workspace_size)");
+        return FP_ERR_INVALID;
+    }
+    if (!PO.params) { set_error("fp_policy_prepare must run before a per_step rollout"); return FP_ERR_INVALID; }
+    uint8_t *w = (uint8_t *)a.workspace;
+    PsState S;
+    S.dev = (int *)(w + L.dev); S.npl = (int *)(w + L.npl); S.cand = (uint32_t *)(w + L.cand);
+    S.order = (int *)(w + L.order); S.tstart = (double *)(w + L.tstart);
+    S.tend = (double *)(w + L.tend); S.avail = (double *)(w + L.avail);
+    S.aflops = (double *)(w + L.aflops); S.cid = (int *)(w + L.cid); S.cs = (double *)(w + L.cs);
+    S.stat = (int *)(w + L.stat);
+    DevPolicy PB = PO;  // weights + graph constants shared; activations over B*n rows
+    PB.rows = n * B;
+    PB.batch = B;
+    PB.ps_dev = S.dev;
+    for (int e = 0; e < PO.n_enc; ++e) {
+        PB.H[e][0] = (double *)(w + L.H[e][0]);
+        for (int k = 0; k < PO.K; ++k) {
+            PB.H[e][k + 1] = (double *)(w + L.H[e][k + 1]);
+            PB.Pm[e][k] = (double *)(w + L.Pm[e][k]);
+            PB.Qm[e][k] = (double *)(w + L.Qm[e][k]);
+            PB.AG[e][k] = (double *)(w + L.AG[e][k]);
+        }
+    }
+    PB.Zs = (double *)(w + L.Zs); PB.A = (double *)(w + L.A); PB.G = (double *)(w + L.G);
+    ps_init_kernel<<<(B + kPsWarps - 1) / kPsWarps, kPsWarps * 32, 0, st>>>(PR, S, B);
+    const int D = PR.d, h = PO.h;
+    for (int step = 0; step < n; ++step) {
+        int rc = gnn_encode_rows(PB, st, false, false);
+        if (rc) return rc;
+        if (h <= 32) {
+            if (D <= 4) ps_launch_step<4, 1>(p, pol, PB, a, S, step, st);
+            else if (D <= 8) ps_launch_step<8, 1>(p, pol, PB, a, S, step, st);
+            else if (D <= 16) ps_launch_step<16, 1>(p, pol, PB, a, S, step, st);
+            else ps_launch_step<32, 1>(p, pol, PB, a, S, step, st);
+        } else {
+            if (D <= 8) ps_launch_step<8, 2>(p, pol, PB, a, S, step, st);
+            else if (D <= 16) ps_launch_step<16, 2>(p, pol, PB, a, S, step, st);
+            else ps_launch_step<32, 2>(p, pol, PB, a, S, step, st);
+        }
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FP_ERR_CUDA; }
+    }
+    const int fb = (int)std::min<int64_t>(((int64_t)B * n + 255) / 256, 4096);
+    ps_finish_kernel<<<fb, 256, 0, st>>>(S, a, n, 0);
+    // status of episodes that finished cleanly, then the simulator's verdict
+    fp_rollout_args a2 = a;
+    if (a.simulate) {
+        int rc = sim_launch_compact(p, a.assign, B, a.strategy, a.makespan, a.status, a.trace,
+                                    a.trace_cap, a.trace_len, st);
+        if (rc) return rc;
+    } else {
+        cudaMemsetAsync(a.status, 0, sizeof(int32_t) * B, st);
+    }
+    ps_finish_kernel<<<fb, 256, 0, st>>>(S, a2, n, 1);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FP_ERR_CUDA; }
+    return FP_OK;
+}
+
+}  // namespace fp

@@ -43,6 +43,11 @@ __host__ __device__ inline int gnn_role(int enc, int k, int r) {
 
 struct DevPolicy {
     int n, h, K, n_enc;  // n_enc = 1 (shared) or 2
+    // encoder row batch: rows = batch * n (batch > 1 only for per_step
+    // message passing, where row b*n + v is vertex v of episode b and
+    // ps_dev[b*n + v] its device so far, -1 = unplaced)
+    int rows, batch, D;
+    const int *ps_dev;
     double slope;
     const double *params;          // flat float64 (set by prepare)
     double *grad;                  // flat float64 gradient (backward)
@@ -75,6 +80,10 @@ struct DevPolicy {
 
     __device__ __forceinline__ const double *W(int role) const { return params + off[role]; }
 };
+
+// GNN encode of every row of P (fp_encode.cu): aggregation + DMMA node MLPs
+// (+ forest path sums and the SEL head when sel_head).  0 or FP_ERR_*.
+int gnn_encode_rows(DevPolicy &P, cudaStream_t st, bool bwd, bool sel_head);
 
 }  // namespace fp
 

@@ -36,6 +36,10 @@ struct DevProblem {
 };
 
 void set_error(const std::string &msg);
+// compact-path batched simulation (no workspace): fp_capi.cu
+int sim_launch_compact(const fp_problem *p, const int32_t *assign, int B, int strategy,
+                       double *makespan, int32_t *status, fp_event *trace, int trace_cap,
+                       int32_t *trace_len, cudaStream_t stream);
 // blocks of a persistent launch: occupancy x SMs, capped at blocks_needed
 int persistent_blocks(const void *kern, int threads, int64_t smem, int64_t blocks_needed);
 

@@ -57,8 +57,12 @@ static int dispatch_grad(const fp_problem *p, const fp_policy *pol, const fp_rol
                 : launch_rollout<MAXD, HPL, false>(p, pol, a, st);
 }
 
+int per_step_rollout(const fp_problem *p, const fp_policy *pol, const fp_rollout_args &a,
+                     int64_t *ws_needed, cudaStream_t st);  // fp_per_step.cu
+
 static int dispatch(const fp_problem *p, const fp_policy *pol, const fp_rollout_args &a,
                     int64_t *ws_needed, cudaStream_t st) {
+    if (a.flags & FP_FLAG_PER_STEP) return per_step_rollout(p, pol, a, ws_needed, st);
     const int D = p->dev.d, h = pol->dev.h;
     if (h <= 32) {
         if (D <= 4) return dispatch_grad<4, 1>(p, pol, a, ws_needed, st);

@@ -200,8 +200,12 @@ class PolicyContext:
 
     def __init__(self, graph: DataflowGraph, cluster: ClusterSpec, config: PolicyConfig,
                  features: StaticGraphFeatures | None = None, forest: bool | None = None):
-        if config.mp_mode != "per_episode":
-            raise NotImplementedError("mp_mode='per_step' is not implemented by the CUDA rollout")
+        if config.mp_mode not in ("per_episode", "per_step"):
+            raise ValueError(f"unknown mp_mode {config.mp_mode!r}")
+        # per_step (policy.py:353-371): both encoders re-run before every
+        # decision with the placement columns -- a B x n-row batched encode per
+        # step on the GPU (forward only)
+        self.per_step = config.mp_mode == "per_step"
         self.graph = graph
         self.cluster = cluster
         self.config = config
@@ -251,6 +255,14 @@ class PolicyContext:
             self._lib.fp_policy_destroy(h)
             self.handle = None
 
+    def jump_rounds(self) -> int:
+        """Pointer-jumping launches per prepare (forest-form paths only)."""
+        if not self.forest:
+            return 0
+        longest = max(int(self.features.path_lengths("b").max(initial=1)),
+                      int(self.features.path_lengths("t").max(initial=1)))
+        return int(np.ceil(np.log2(longest))) if longest > 1 else 0
+
     def set_encoder(self, fused: bool):
         """Select the fused per-vertex encoder (reference FMA order) instead of
         the default aggregation + DMMA node-MLP kernels."""
@@ -273,7 +285,8 @@ class PolicyContext:
         flat = self.flat_params(params)
         self._flat = flat
         N.check(N.lib().fp_policy_prepare(self.handle, N.ptr(flat), N.stream_ptr(stream)))
-        self.encode_count += 2
+        if not self.per_step:  # per_step encodes are counted by the rollout
+            self.encode_count += 2
         return flat
 
     def read_table(self, name: str) -> np.ndarray:
@@ -322,12 +335,15 @@ class PolicyContext:
                                        out.status, out.grad_rows, out.grad_ep, out.trace)],
             out.trace.shape[1] // 16 if out.trace is not None else 0,
             N.ptr(out.trace_len).value,
-            (N.FLAG_WIDE if wide else 0) | (N.FLAG_TIE_RANDOM if tie_random else 0))
+            (N.FLAG_WIDE if wide else 0) | (N.FLAG_TIE_RANDOM if tie_random else 0) |
+            (N.FLAG_PER_STEP if self.per_step else 0))
         ws = self.workspace(B, wide=wide, grad=out.grad_rows is not None)
         args.workspace = N.ptr(ws).value
         args.workspace_bytes = 0 if ws is None else ws.numel()
         N.check(N.lib().fp_rollout_batch(self.sim.handle, self.handle, ctypes.byref(args),
                                          N.stream_ptr(stream)))
+        if self.per_step:
+            self.encode_count += 2 * n * B
         out._forced = ft
         return out
 
@@ -338,10 +354,10 @@ class PolicyContext:
         import torch
 
         need = ctypes.c_int64()
+        flags = (N.FLAG_WIDE if wide else 0) | (N.FLAG_PER_STEP if self.per_step else 0)
         N.check(N.lib().fp_rollout_workspace_size(
-            self.sim.handle, self.handle, ctypes.c_int32(B),
-            ctypes.c_int32(N.FLAG_WIDE if wide else 0), ctypes.c_int32(int(grad)),
-            ctypes.byref(need)))
+            self.sim.handle, self.handle, ctypes.c_int32(B), ctypes.c_int32(flags),
+            ctypes.c_int32(int(grad)), ctypes.byref(need)))
         if need.value == 0:
             return None
         ws = getattr(self, "_ws", None)
