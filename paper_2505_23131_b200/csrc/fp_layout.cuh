@@ -20,10 +20,10 @@ constexpr int kMaxTreeLevels = 6; // 32-ary candidate tree: n <= 32^6
 struct EpLayout {
     // ---- n-sized group (nb) ----
     int ce, cc, dsl, dse, tstart, tend, cand, npl, clist, order;
-    int rdy, missing, cons, assign, bits;
+    int rdy, missing, assign, bits;
     int tm, tz, tc, tt;  // candidate tree nodes (wide rollout): max, scaled sum, count, teacher max
     // ---- small group (sb) ----
-    int xd, xn, stats, rsum, flag, ring;
+    int xd, xn, stats, rsum, flag, ring, simres;
     int cnt, pend, pv, pseq, skey, sidx, elist, ctr;
     int bytes;   // shared-memory bytes per episode
     int64_t gbytes;  // HBM workspace bytes per episode (wide), 0 for the compact path
@@ -89,7 +89,7 @@ __host__ __device__ inline EpLayout make_layout(int n, int W, int R, int SM, boo
     const int P = R * SM;
     L.ce = L.cc = L.dsl = L.dse = L.tstart = L.tend = L.cand = L.npl = L.clist = L.order = 0;
     L.tm = L.tz = L.tc = L.tt = 0;
-    L.xd = L.xn = L.stats = L.rsum = L.flag = L.ring = 0;
+    L.xd = L.xn = L.stats = L.rsum = L.flag = L.ring = L.simres = 0;
     if (with_rollout) {
         if (!wide) {
             L.ce = take_n(8 * n, 16);
@@ -114,12 +114,12 @@ __host__ __device__ inline EpLayout make_layout(int n, int W, int R, int SM, boo
         L.stats = take_s(8 * 16, 8);
         L.rsum = take_s(8 * rsum_doubles, 8);
         L.flag = take_s(16, 16);
+        L.simres = take_s(16, 16);
     }
     L.pend = take_s(8 * P, 8);
     L.skey = take_s(8 * P, 8);
     L.rdy = take_n(4LL * n, 4);
     L.missing = take_n(4LL * n, 4);
-    L.cons = take_n(4LL * n, 4);
     L.bits = take_n(4LL * R * L.BW, 4);
     L.cnt = take_s(4 * R, 4);
     L.pv = take_s(4 * P, 4);

@@ -61,7 +61,7 @@ struct PlcLog {  // log2(MAXD)
 // SEL warp
 // ---------------------------------------------------------------------------
 template <bool GRAD>
-__device__ __forceinline__ void sel_chain(const DevProblem &PR, const DevPolicy &PO,
+__device__ __forceinline__ bool sel_chain(const DevProblem &PR, const DevPolicy &PO,
                                           const fp_rollout_args &A, uint8_t *base /* nb == sb */,
                                           const EpLayout &L, const double *s_sm, int ep,
                                           bool want_lp, bool want_amax) {
@@ -109,7 +109,7 @@ __device__ __forceinline__ void sel_chain(const DevProblem &PR, const DevPolicy 
         const int k = __shfl_sync(FP_FULL_MASK, incl, 31);
         if (k == 0) {  // cyclic graph: nothing is ever ready
             if (lane == 0) order[step] = -1;
-            return;
+            return false;
         }
         {
             int o = incl - pc;
@@ -224,7 +224,7 @@ __device__ __forceinline__ void sel_chain(const DevProblem &PR, const DevPolicy 
         }
         if (idx < 0) {  // forced vertex is not a candidate
             if (lane == 0) order[step] = -2;
-            return;
+            return false;
         }
         const int v = clist[idx];
         // publish early: the PLC warp only needs the vertex (a single 32-bit
@@ -286,6 +286,7 @@ __device__ __forceinline__ void sel_chain(const DevProblem &PR, const DevPolicy 
         double *g = A.grad_ep + (size_t)ep * grad_ep_stride(n, PO.h, PR.d);
         for (int v = lane; v < n; v += 32) { g[v] = dsl[v]; g[n + v] = dse[v]; }
     }
+    return true;
 }
 
 // ---------------------------------------------------------------------------
@@ -896,6 +897,10 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
                 avail = en;
             }
             dev[v] = (uint8_t)jdx;
+            if constexpr (!WIDE) {  // release the placement to the overlapped simulator
+                __threadfence_block();
+                *(volatile int *)(sb + L.flag) = step + 1;
+            }
             if (A.step_vd) A.step_vd[2 * ((size_t)ep * n + step) + 1] = jdx;
         }
         if (lane == 0 && A.step_argmax) A.step_argmax[2 * ((size_t)ep * n + step) + 1] = amax;
@@ -943,32 +948,66 @@ rollout_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
     double *s_sm = (double *)smem;
     for (int v = threadIdx.x; v < n; v += blockDim.x) s_sm[v] = PO.s[v];
     uint8_t *base = smem + fp_align(8 * n, 16) + (size_t)slot * L.bytes;
+    volatile int *flag = (volatile int *)(base + L.flag);  // [0] placed, [1] PLC abort
     if (!is_plc) {
         volatile int *order = (volatile int *)(base + L.order);
         for (int t = lane; t < n; t += 32) order[t] = -3;  // hand-off sentinel
+        if (lane == 0) { flag[0] = 0; flag[1] = 0; }
     }
     __syncthreads();
     if (ep >= A.B) return;
     const bool want_lp = GRAD || A.step_lp != nullptr || A.step_ent != nullptr;
     const bool want_amax = A.step_argmax != nullptr;
+    double *simres = (double *)(base + L.simres);  // makespan, status
+    int status = FP_EP_OK;
     if (!is_plc) {
-        sel_chain<GRAD>(PR, PO, A, base, L, s_sm, ep, want_lp, want_amax);
-        return;
+        // SEL warp: the vertex order, then -- while the PLC warp is still
+        // placing -- the simulation, chasing the placement frontier
+        const bool ok = sel_chain<GRAD>(PR, PO, A, base, L, s_sm, ep, want_lp, want_amax);
+        if (ok && A.simulate) {
+            const volatile int *order = (const volatile int *)(base + L.order);
+            int *pos = (int *)(base + L.clist);     // SEL scratch, free now
+            int *maxsucc = (int *)(base + L.npl);
+            for (int i = lane; i < n; i += 32) pos[order[i]] = i;
+            __syncwarp();
+            int iw = -1;
+            for (int v = lane; v < n; v += 32) {
+                int m = -1;
+                for (int j = PR.succ_ptr[v]; j < PR.succ_ptr[v + 1]; ++j) m = max(m, pos[PR.succ_idx[j]]);
+                maxsucc[v] = m;
+                if (!PR.is_entry[v]) {
+                    bool all_entry = true;
+                    for (int j = PR.pred_ptr[v]; j < PR.pred_ptr[v + 1]; ++j)
+                        all_entry &= PR.is_entry[PR.pred_idx[j]] != 0;
+                    if (all_entry) iw = max(iw, pos[v]);
+                }
+            }
+            iw = __reduce_max_sync(FP_FULL_MASK, iw);
+            __syncwarp();
+            SimOut o = sim_episode<RPL, false, SM1, true>(
+                PR, base, base, L, A.strategy, nullptr,
+                A.trace ? A.trace + (size_t)ep * A.trace_cap : nullptr, A.trace_cap, nullptr,
+                SimSync{flag, flag + 1, maxsucc, iw});
+            if (lane == 0) {
+                simres[0] = o.makespan;
+                ((int *)simres)[2] = o.status;
+                if (A.trace_len) A.trace_len[ep] = o.n_events;
+            }
+        }
+    } else {
+        status = plc_chain<MAXD, HPL, GRAD>(PR, PO, A, base, base, L, ep, want_lp, want_amax);
+        if (status != FP_EP_OK && lane == 0) flag[1] = 1;  // release a waiting simulator
+        const uint8_t *dev = base + L.assign;
+        for (int v = lane; v < n; v += 32)
+            A.assign[(size_t)ep * n + v] = dev[v] == 0xFF ? -1 : dev[v];
     }
-    int status = plc_chain<MAXD, HPL, GRAD>(PR, PO, A, base, base, L, ep, want_lp, want_amax);
-    const uint8_t *dev = base + L.assign;
-    for (int v = lane; v < n; v += 32) A.assign[(size_t)ep * n + v] = dev[v] == 0xFF ? -1 : dev[v];
-    double mk = 0.0;
-    if (status == FP_EP_OK && A.simulate) {
-        __syncwarp();
-        SimOut o = sim_episode<RPL, false, SM1>(PR, base, base, L, A.strategy, nullptr,
-                                    A.trace ? A.trace + (size_t)ep * A.trace_cap : nullptr,
-                                    A.trace_cap, nullptr);
-        status = o.status;
-        mk = o.makespan;
-        if (lane == 0 && A.trace_len) A.trace_len[ep] = o.n_events;
-    }
-    if (lane == 0) {
+    __syncthreads();
+    if (is_plc && lane == 0) {
+        double mk = 0.0;
+        if (status == FP_EP_OK && A.simulate) {
+            mk = simres[0];
+            status = ((const int *)simres)[2];
+        }
         if (A.makespan) A.makespan[ep] = mk;
         A.status[ep] = status;
     }

@@ -84,17 +84,48 @@ __device__ __forceinline__ int pend_pop_hier(uint32_t *b, const EpLayout &L) {
 // nb: this episode's n-sized state (shared memory, or its HBM workspace slice
 // on the wide path); sb: its small shared-memory scratch.  nb + L.assign must
 // hold the assignment (made visible with __syncwarp).  All 32 lanes must call.
-template <int RPL, bool HIER = false, bool SM1 = false>
+// Overlap with the placement chain (OVL): the simulator may run while the
+// PLC warp is still placing vertices (in the SEL order).  A task only needs
+// the devices of vertices it touches: starting a pending task needs nothing
+// new, and retiring (exec or transfer of) v needs the devices of all of v's
+// successors (consumer devices, readiness of w on A_w).  So before retiring
+// the tasks of an instant the simulator waits until the placement counter
+// passes the largest SEL position among their successors (maxsucc[v]), and
+// before seeding the initially pending execs until it passes the last of
+// them (initwait).  Any vertex that becomes startable is the successor of a
+// retired task (or initially pending), so every pending task is placed.
+struct SimSync {
+    const volatile int *placed;  // vertices placed so far (PLC warp, release)
+    const volatile int *abort;   // PLC chain failed: stop waiting
+    const int *maxsucc;          // [n] max SEL position over successors, -1 if none
+    int initwait;                // max SEL position over the initially pending execs
+};
+
+__device__ __forceinline__ bool sim_wait_placed(const SimSync &S, int need) {
+    int ok = 1;
+    if (need >= 0 && lane_id() == 0) {
+        while (*S.placed <= need) {
+            if (*S.abort) { ok = 0; break; }
+            __nanosleep(32);  // leave the issue slots to the placing warps
+        }
+        __threadfence_block();  // acquire: the devices written before the counter
+    }
+    ok = __shfl_sync(FP_FULL_MASK, ok, 0);
+    __syncwarp();
+    return ok != 0;
+}
+
+template <int RPL, bool HIER = false, bool SM1 = false, bool OVL = false>
 __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *nb, uint8_t *sb,
                                               const EpLayout &L, int strategy,
                                               const double *__restrict__ jit,
                                               fp_event *__restrict__ trace, int trace_cap,
-                                              uint8_t *__restrict__ blocked) {
+                                              uint8_t *__restrict__ blocked,
+                                              SimSync sync = SimSync{nullptr, nullptr, nullptr, -1}) {
     const int lane = lane_id();
     const int n = P.n, d = P.d, R = P.R, SM = P.SM, BW = L.BW;
     uint32_t *rdy = (uint32_t *)(nb + L.rdy);
     int *missing = (int *)(nb + L.missing);
-    uint32_t *cons = (uint32_t *)(nb + L.cons);
     const uint8_t *assign = nb + L.assign;
     uint32_t *bits = (uint32_t *)(nb + L.bits);
     int *cnt = (int *)(sb + L.cnt);
@@ -119,9 +150,6 @@ __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *nb, 
     for (int v = lane; v < n; v += 32) {
         const bool e = ent[v];
         rdy[v] = e ? dmask : 0u;
-        uint32_t c = 0;
-        for (int j = sp[v]; j < sp[v + 1]; ++j) c |= 1u << assign[si[j]];
-        cons[v] = c;
         int miss = 0;
         for (int j = P.pred_ptr[v]; j < P.pred_ptr[v + 1]; ++j) miss += !ent[P.pred_idx[j]];
         missing[v] = miss;
@@ -146,6 +174,8 @@ __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *nb, 
         }
     }
     __syncwarp();
+    if constexpr (OVL)
+        if (!sim_wait_placed(sync, sync.initwait)) return SimOut{0.0, FP_EP_BAD_ACTION, 0};
     for (int v = lane; v < n; v += 32)
         if (!ent[v] && missing[v] == 0) {
             pend_push<HIER>(bits + assign[v] * BW, L, rpos[v]);
@@ -272,6 +302,21 @@ __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *nb, 
         FP_PHASE_END(pq_, 23);
         if (tracing && lane == 0) ctr[1] = 0;
         __syncwarp();
+        if constexpr (OVL) {  // the retiring tasks' successors must be placed
+            int need = -1;
+#pragma unroll
+            for (int q = 0; q < RPL; ++q) {
+                const int r = lane + 32 * q;
+                if (r >= R) continue;
+                for (int i = 0; i < (SM1 ? 1 : SM); ++i) {
+                    const int v = SM1 ? ipv[q] : pv[r * SM + i];
+                    const double e = SM1 ? iend[q] : pend[r * SM + i];
+                    if (v >= 0 && e == tmin) need = max(need, sync.maxsucc[v]);
+                }
+            }
+            need = __reduce_max_sync(FP_FULL_MASK, need);
+            if (!sim_wait_placed(sync, need)) return SimOut{0.0, FP_EP_BAD_ACTION, 0};
+        }
         int done_exec = 0;
 #pragma unroll
         for (int q = 0; q < RPL; ++q) {
@@ -300,7 +345,10 @@ __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *nb, 
                     dev = r;
                     atomicOr(&rdy[v], 1u << r);
                     ++done_exec;
-                    uint32_t m = cons[v] & ~(1u << r);
+                    // consumer devices of v (_simcore.pyx:84-97), known once placed
+                    uint32_t m = 0u;
+                    for (int j = sp[v]; j < sp[v + 1]; ++j) m |= 1u << assign[si[j]];
+                    m &= ~(1u << r);
                     const int pos = rpos[v];
                     while (m) {
                         const int dst = __ffs(m) - 1;

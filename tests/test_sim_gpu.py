@@ -166,7 +166,7 @@ def test_wide_workspace_contract(torch_cuda):
     import ctypes
     from paper_2505_23131_b200 import _native as N
     from paper_2505_23131_b200.simulate import SimProblem
-    g = builders.sparse_dag(3000, seed=0)
+    g = builders.sparse_dag(5000, seed=0)
     prob = SimProblem(g, ClusterSpec.uniform(8, rate=1e9, bandwidth=1e7))
     assert prob.workspace(4) is not None          # beyond shared memory: wide path
     assert SimProblem(builders.build_ffnn(8, 4, 16, 4, 2),
