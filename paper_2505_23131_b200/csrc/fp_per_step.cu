@@ -8,10 +8,10 @@
 //   1. one encode of all B x n rows (gnn_proj0 with the per-episode dyn
 //      columns, then K x (aggregation + DMMA node MLPs) -- the same kernels
 //      as the per-snapshot encoder, run over a B*n-row batch);
-//   2. ps_step_kernel, one warp per episode: SEL logits of the current
-//      candidates from this step's H_sel (path sums over the explicit b/t
-//      path lists, head1 as a lane-per-column mat-vec), masked softmax +
-//      decision, then the PLC step on this step's A / G rows
+//   2. ps_step_kernel, one 4-warp block per episode: SEL logits of the
+//      current candidates from this step's H_sel (path sums over the explicit
+//      b/t path lists, head1 as a lane-per-column mat-vec; candidates spread
+//      over the warps), masked softmax + decision, then the PLC step on this step's A / G rows
 //      (h_d = sum of G over the vertices placed on d, recomputed because G
 //      changed), device features, standardisation, softmax over devices,
 //      decision, timeline commit -- the per_episode kernels' math, with the
@@ -93,16 +93,22 @@ __global__ void ps_init_kernel(DevProblem PR, PsState S, int B) {
     if (lane == 0) S.stat[ep] = FP_EP_OK;
 }
 
-// One decision step (SEL then PLC) of every live episode.
+// One decision step (SEL then PLC) of every live episode: one block of
+// kPsWarps warps per episode.  All warps compute candidate logits (candidate
+// i on warp i mod kPsWarps: path sums + head1 mat-vec), warp 0 then runs the
+// softmax / decision and the PLC step.
 template <int MAXD, int HPL>
 __global__ void __launch_bounds__(kPsWarps * 32)
 ps_step_kernel(DevProblem PR, DevPolicy PO, DevPolicy PB, fp_rollout_args A, PsState S,
                int step) {
     constexpr int LOGD = PlcLog<MAXD>::v;
-    __shared__ double xd_sm[kPsWarps][32 * 5], xn_sm[kPsWarps][32 * 5], st_sm[kPsWarps][16];
+    __shared__ double xd_sm[32 * 5], xn_sm[32 * 5], st_sm[16];
+    __shared__ double cs[1024];
+    __shared__ int cid[1024];
+    __shared__ int k_sm;
     const int lane = lane_id(), warp = threadIdx.x >> 5;
-    const int ep = blockIdx.x * kPsWarps + warp;
-    if (ep >= A.B || S.stat[ep] != FP_EP_OK) return;
+    const int ep = blockIdx.x;
+    if (ep >= A.B || S.stat[ep] != FP_EP_OK) return;  // block-uniform
     const int n = PR.n, W = PR.W, D = PR.d, h = PO.h;
     const size_t base = (size_t)ep * n;
     const double eps = A.epsilon, ome = 1.0 - eps, slope = PO.slope;
@@ -113,20 +119,13 @@ ps_step_kernel(DevProblem PR, DevPolicy PO, DevPolicy PB, fp_rollout_args A, PsS
     const bool want_amax = A.step_argmax != nullptr;
     const size_t o = base + step;
     const double *Hs = PB.H[0][PO.K];
-    int *cid = S.cid + base;
-    double *cs = S.cs + base;
     uint32_t *cand = S.cand + (size_t)ep * W;
 
     // ---------------- SEL: logits of the current candidates ----------------
-    const uint32_t cw = lane < W ? cand[lane] : 0u;
-    const int pc = __popc(cw);
-    const int incl = warp_inclusive_scan(pc);
-    const int k = __shfl_sync(FP_FULL_MASK, incl, 31);
-    if (k == 0) {
-        if (lane == 0) S.stat[ep] = FP_EP_DEADLOCK;
-        return;
-    }
-    {
+    if (warp == 0) {
+        const uint32_t cw = lane < W ? cand[lane] : 0u;
+        const int pc = __popc(cw);
+        const int incl = warp_inclusive_scan(pc);
         int q = incl - pc;
         uint32_t m = cw;
         while (m) {
@@ -134,11 +133,17 @@ ps_step_kernel(DevProblem PR, DevPolicy PO, DevPolicy PB, fp_rollout_args A, PsS
             m &= m - 1;
             cid[q++] = lane * 32 + b;
         }
+        if (lane == 31) k_sm = incl;
     }
-    __syncwarp();
+    __syncthreads();
+    const int k = k_sm;
+    if (k == 0) {
+        if (threadIdx.x == 0) S.stat[ep] = FP_EP_DEADLOCK;
+        return;
+    }
     const double *w1 = PO.W(PR_SEL_H1_W), *b1 = PO.W(PR_SEL_H1_B), *w2 = PO.W(PR_SEL_H2_W);
     const double b2 = PO.W(PR_SEL_H2_B)[0];
-    for (int i = 0; i < k; ++i) {
+    for (int i = warp; i < k; i += kPsWarps) {
         const int v = cid[i];
         double em[4][HPL];
 #pragma unroll
@@ -148,7 +153,9 @@ ps_step_kernel(DevProblem PR, DevPolicy PO, DevPolicy PB, fp_rollout_args A, PsS
             if (j >= h) continue;
             em[0][t] = Hs[(base + v) * h + j];
             double hb = 0.0, ht = 0.0;
+#pragma unroll 4
             for (int q = PO.bp_ptr[v]; q < PO.bp_ptr[v + 1]; ++q) hb += Hs[(base + PO.bp_idx[q]) * h + j];
+#pragma unroll 4
             for (int q = PO.tp_ptr[v]; q < PO.tp_ptr[v + 1]; ++q) ht += Hs[(base + PO.tp_idx[q]) * h + j];
             em[1][t] = hb;
             em[2][t] = ht;
@@ -159,6 +166,7 @@ ps_step_kernel(DevProblem PR, DevPolicy PO, DevPolicy PB, fp_rollout_args A, PsS
         for (int t = 0; t < HPL; ++t) acc[t] = 0.0;
 #pragma unroll
         for (int b = 0; b < 4; ++b)
+#pragma unroll 8
             for (int ii = 0; ii < h; ++ii) {
                 double ev = 0.0;
 #pragma unroll
@@ -181,7 +189,8 @@ ps_step_kernel(DevProblem PR, DevPolicy PO, DevPolicy PB, fp_rollout_args A, PsS
         part = warp_sum(part);
         if (lane == 0) cs[i] = part + b2;
     }
-    __syncwarp();
+    __syncthreads();
+    if (warp != 0) return;
     // masked softmax over the candidates in ascending-id order (policy.py:204)
     double mx = -INFINITY;
     for (int i = lane; i < k; i += 32) mx = fmax(mx, cs[i]);
@@ -280,7 +289,7 @@ ps_step_kernel(DevProblem PR, DevPolicy PO, DevPolicy PB, fp_rollout_args A, PsS
     }
 
     // ---------------- PLC ----------------
-    double *xd = xd_sm[warp], *xn = xn_sm[warp], *stats = st_sm[warp];
+    double *xd = xd_sm, *xn = xn_sm, *stats = st_sm;
     const int *pp = PR.pred_ptr, *pi = PR.pred_idx;
     const uint8_t *ent = PR.is_entry;
     double f4 = 0.0;
@@ -331,16 +340,24 @@ ps_step_kernel(DevProblem PR, DevPolicy PO, DevPolicy PB, fp_rollout_args A, PsS
     for (int d = 0; d < MAXD; ++d)
 #pragma unroll
         for (int t = 0; t < HPL; ++t) Sd[d][t] = 0.0;
-    for (int i = 0; i < step; ++i) {
-        const int u = S.order[base + i];
-        const int du = S.dev[base + u];
+    for (int i0 = 0; i0 < step; i0 += 32) {
+        // 32 placed vertices at a time: lane i loads (u, d_u), then the G rows
+        // are summed in placement order (independent row loads in flight)
+        const int cnt = min(32, step - i0);
+        const int my_u = lane < cnt ? S.order[base + i0 + lane] : 0;
+        const int my_d = lane < cnt ? S.dev[base + my_u] : -1;
+#pragma unroll 4
+        for (int i = 0; i < cnt; ++i) {
+            const int u = __shfl_sync(FP_FULL_MASK, my_u, i);
+            const int du = __shfl_sync(FP_FULL_MASK, my_d, i);
 #pragma unroll
-        for (int t = 0; t < HPL; ++t) {
-            const int j = lane + 32 * t;
-            const double g = j < h ? PB.G[(base + u) * h + j] : 0.0;
+            for (int t = 0; t < HPL; ++t) {
+                const int j = lane + 32 * t;
+                const double g = j < h ? PB.G[(base + u) * h + j] : 0.0;
 #pragma unroll
-            for (int d = 0; d < MAXD; ++d)
-                if (d == du) Sd[d][t] += g;
+                for (int d = 0; d < MAXD; ++d)
+                    if (d == du) Sd[d][t] += g;
+            }
         }
     }
     const double *w2p = PO.W(PR_PLC_H2_W);
@@ -467,8 +484,7 @@ template <int MAXD, int HPL>
 static void ps_launch_step(const fp_problem *p, const fp_policy *pol, const DevPolicy &PB,
                            const fp_rollout_args &a, const PsState &S, int step,
                            cudaStream_t st) {
-    ps_step_kernel<MAXD, HPL><<<(a.B + kPsWarps - 1) / kPsWarps, kPsWarps * 32, 0, st>>>(
-        p->dev, pol->dev, PB, a, S, step);
+    ps_step_kernel<MAXD, HPL><<<a.B, kPsWarps * 32, 0, st>>>(p->dev, pol->dev, PB, a, S, step);
 }
 
 int per_step_rollout(const fp_problem *p, const fp_policy *pol, const fp_rollout_args &a,
