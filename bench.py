@@ -228,26 +228,53 @@ def run_ours(args):
     assert (st == 0).all(), "episode failures in the timed region"
 
     # ---- end-to-end through the public API with host buffers ----
+    # Every step: H2D of its parameters from pinned host memory, the public
+    # rollout_batch / trainer.step call, D2H of its assignments + makespans
+    # into pinned host memory.  Steps are pipelined the way a serving loop
+    # would run them: the D2H copies go on a side stream and the device
+    # outputs are double-buffered, so step i's copies overlap step i+1's
+    # kernels; the whole run is timed once on the host clock (synchronized on
+    # both sides), no per-step device timing.
     host_params = torch.from_numpy(ctx.layout.flatten(params)).pin_memory()
-    host_assign = torch.empty((B, n), dtype=torch.int32).pin_memory()
-    host_mk = torch.empty(B, dtype=torch.float64).pin_memory()
-    dev_params = torch.empty_like(flat)
-    e2e_ms = []
-    for i in range(args.warmup + args.steps):
-        flush.fill_(float(i))
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        dev_params.copy_(host_params, non_blocking=True)
+    host_assign = [torch.empty((B, n), dtype=torch.int32).pin_memory() for _ in range(2)]
+    host_mk = [torch.empty(B, dtype=torch.float64).pin_memory() for _ in range(2)]
+    dev_params = [torch.empty_like(flat) for _ in range(2)]
+    outs = [out, ctx.alloc_batch(B, grad=train)]
+    copy_stream = torch.cuda.Stream()
+    done_ev = [torch.cuda.Event() for _ in range(2)]
+    free_ev = [torch.cuda.Event() for _ in range(2)]
+
+    def e2e_step(i):
+        sl = i % 2
+        comp = torch.cuda.current_stream()
+        dev_params[sl].copy_(host_params, non_blocking=True)
+        if i >= 2:
+            comp.wait_event(free_ev[sl])  # step i-2's results are on the host
         if train:
-            trainer.load_flat(dev_params)
-            trainer.step(seed=0x9000 + i, out=out)
+            trainer.load_flat(dev_params[sl])
+            trainer.step(seed=0x9000 + i, out=outs[sl])
         else:
-            ctx.rollout_batch(dev_params, B, EPSILON, 0x9000 + i, episode_base=ep_base, out=out)
-        host_assign.copy_(out.assign, non_blocking=True)
-        host_mk.copy_(out.makespan, non_blocking=True)
-        torch.cuda.synchronize()
-        if i >= args.warmup:
-            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+            ctx.rollout_batch(dev_params[sl], B, EPSILON, 0x9000 + i, episode_base=ep_base,
+                              out=outs[sl])
+        done_ev[sl].record(comp)
+        with torch.cuda.stream(copy_stream):
+            copy_stream.wait_event(done_ev[sl])
+            host_assign[sl].copy_(outs[sl].assign, non_blocking=True)
+            host_mk[sl].copy_(outs[sl].makespan, non_blocking=True)
+            free_ev[sl].record(copy_stream)
+            flush.fill_(float(i))  # evict L2 while the next step runs
+
+    for i in range(args.warmup):
+        e2e_step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        e2e_step(args.warmup + i)
+    torch.cuda.synchronize()
+    e2e_ms = [(time.perf_counter() - t0) * 1e3]
+    assert bool((outs[0].status == 0).all()) and bool((outs[1].status == 0).all())
     e2e_t = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
@@ -296,7 +323,9 @@ def run_ours(args):
             "config": {"workload": desc, "episodes_per_gpu": B, "global_batch": B * world,
                        "mode": args.mode, "epsilon": EPSILON, "policy": f"hidden 32, K 2, {args.mp_mode}",
                        "parallelism": f"episode-dp{world}",
-                       "l2": "flushed between timed steps (256 MiB write)"},
+                       "l2": "flushed between timed steps (256 MiB write); e2e: steps "
+                             "pipelined (D2H on a side stream, double-buffered outputs), "
+                             "256 MiB flush on the side stream every step"},
             "e2e": {"value": e2e_value, "unit": UNIT,
                     "h2d_bytes_per_step": int(host_params.numel() * 8),
                     "d2h_bytes_per_step": int(B * n * 4 + B * 8)},

@@ -510,6 +510,16 @@ static int launch_gnn_tc(DevPolicy &P, cudaStream_t st, bool sel_head = true) {
             return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         return cudaSuccess;
     };
+    if (sel_head && !P.forest && P.rows <= kSmallEncodeRows) {
+        int64_t smem = 8LL * sel_smem_doubles(H);
+        for (int k = 0; k < P.K; ++k)
+            smem = std::max<int64_t>(smem, 8LL * node_smem_doubles(H, k, k == P.K - 1));
+        const void *kern = (const void *)gnn_small_kernel<H, BWD>;
+        FP_CUDA_RET(set_smem(kern, smem));
+        gnn_small_kernel<H, BWD><<<P.n_enc, threads, smem, st>>>(P);
+        FP_CUDA_RET(cudaGetLastError());
+        return FP_OK;
+    }
     {
         const int64_t smem = 8LL * (2 * (2 * H / 8) * 32);
         const void *kern = (const void *)gnn_proj0_kernel<H>;
@@ -538,6 +548,10 @@ static int launch_gnn_tc(DevPolicy &P, cudaStream_t st, bool sel_head = true) {
         FP_CUDA_RET(cudaGetLastError());
     }
     if (!sel_head) return FP_OK;
+    if (!P.forest) {
+        gnn_pathsum_kernel<H><<<std::max(1, std::min((P.n + 7) / 8, sms * 8)), 256, 0, st>>>(P);
+        FP_CUDA_RET(cudaGetLastError());
+    }
     if (P.forest)
         for (int r = 0; r < P.jump_rounds; ++r) {
             const int64_t total = (int64_t)P.n * H;
@@ -692,6 +706,8 @@ int fp_policy_create(const fp_problem *p, const fp_policy_desc *desc, fp_policy 
             o_nx[w] = take((size_t)n * 4);
             for (int q = 0; q < 2; ++q) { o_PS[w][q] = take(nh); o_PJ[w][q] = take((size_t)n * 4); }
         }
+    else
+        for (int w = 0; w < 2; ++w) o_PS[w][0] = take(nh);  // explicit-list path sums
     size_t o_H[2][kMaxRounds + 1], o_P[2][kMaxRounds], o_Q[2][kMaxRounds], o_U[2][kMaxRounds],
         o_AG[2][kMaxRounds];
     for (int e = 0; e < n_enc; ++e) {
@@ -775,6 +791,8 @@ int fp_policy_create(const fp_problem *p, const fp_policy_desc *desc, fp_policy 
                 P.PJ[w][q] = (int *)(b + o_PJ[w][q]);
             }
         }
+    else
+        for (int w = 0; w < 2; ++w) P.PS[w][0] = (double *)(b + o_PS[w][0]);
     for (int e = 0; e < n_enc; ++e) {
         P.H[e][0] = (double *)(b + o_H[e][0]);
         for (int k = 0; k < K; ++k) {

@@ -77,11 +77,11 @@ __device__ __forceinline__ void zero_acc(double (&acc)[NT][2]) {
 // Aggregation (HBM-bound gather / segment reduce)
 // ---------------------------------------------------------------------------
 template <int H>
-__global__ void __launch_bounds__(256) gnn_agg_kernel(DevPolicy P, int k) {
+__device__ __forceinline__ void gnn_agg_body(const DevPolicy &P, int k, int e_, int bx_, int gx_, double *gsm) {
     constexpr int HL = H / 2;                   // lanes per destination (double2 each)
     constexpr int VPW = HL >= 32 ? 1 : 32 / HL; // destinations per warp
     static_assert(H % 2 == 0 && H <= 64, "H must be even and <= 64");
-    const int e = blockIdx.y;
+    const int e = e_;
     const int lane = lane_id();
     const int sub = HL >= 32 ? 0 : lane / HL;
     const int l = HL >= 32 ? lane : lane % HL;
@@ -96,8 +96,8 @@ __global__ void __launch_bounds__(256) gnn_agg_kernel(DevPolicy P, int k) {
     double2 *agg = (double2 *)P.AG[e][k];
     const double s = P.slope;
     const int warps = blockDim.x >> 5;
-    const int gw = blockIdx.x * warps + (threadIdx.x >> 5);
-    for (int vb = gw * VPW; vb < rows; vb += gridDim.x * warps * VPW) {
+    const int gw = bx_ * warps + (threadIdx.x >> 5);
+    for (int vb = gw * VPW; vb < rows; vb += gx_ * warps * VPW) {
         const int r = vb + sub;  // row = episode * n + vertex
         if (r >= rows || (HL < 32 && lane >= VPW * HL)) continue;
         const int v = r % n, base = r - v;
@@ -129,14 +129,19 @@ __global__ void __launch_bounds__(256) gnn_agg_kernel(DevPolicy P, int k) {
     }
 }
 
+template <int H>
+__global__ void __launch_bounds__(256) gnn_agg_kernel(DevPolicy P, int k) {
+    extern __shared__ __align__(16) double gsm[];
+    gnn_agg_body<H>(P, k, blockIdx.y, blockIdx.x, gridDim.x, gsm);
+}
+
 // ---------------------------------------------------------------------------
 // Round-0 projections: [P0 | Q0] = H0 (n x 7) @ [psi.w rows 0..6 | rows 7..13]
 // ---------------------------------------------------------------------------
 template <int H>
-__global__ void __launch_bounds__(256) gnn_proj0_kernel(DevPolicy P) {
+__device__ __forceinline__ void gnn_proj0_body(const DevPolicy &P, int e_, int bx_, int gx_, double *gsm) {
     constexpr int NT2 = 2 * H / 8;
-    extern __shared__ __align__(16) double gsm[];
-    const int e = blockIdx.y, lane = lane_id(), warp = threadIdx.x >> 5;
+    const int e = e_, lane = lane_id(), warp = threadIdx.x >> 5;
     const int warps = blockDim.x >> 5, n = P.n;
     const double *psw = P.W(gnn_role(e, 0, 0));
     double *Bf = gsm;
@@ -147,7 +152,7 @@ __global__ void __launch_bounds__(256) gnn_proj0_kernel(DevPolicy P) {
     double *H0 = P.H[e][0];
     const int r = lane >> 2, c = lane & 3;
     const int rows = P.rows;
-    for (int tile = blockIdx.x * warps + warp; tile * 8 < rows; tile += gridDim.x * warps) {
+    for (int tile = bx_ * warps + warp; tile * 8 < rows; tile += gx_ * warps) {
         const int v = tile * 8 + r;  // row
         double acc[NT2][2];
         zero_acc(acc);
@@ -182,6 +187,12 @@ __global__ void __launch_bounds__(256) gnn_proj0_kernel(DevPolicy P) {
     }
 }
 
+template <int H>
+__global__ void __launch_bounds__(256) gnn_proj0_kernel(DevPolicy P) {
+    extern __shared__ __align__(16) double gsm[];
+    gnn_proj0_body<H>(P, blockIdx.y, blockIdx.x, gridDim.x, gsm);
+}
+
 // A fragment of k-step kt taken from a D fragment held in registers (the
 // previous GEMM's output, columns 8nt + 2c' + i on lane 4r + c'): lane (r, c)
 // needs column 4kt + c, which lives on lane 4r + 2(kt&1) + c/2 as element c&1
@@ -212,13 +223,12 @@ __host__ __device__ inline int node_smem_doubles(int H, int k, bool last) {
 // staging of activations, so the only shared memory is the weights.
 // ---------------------------------------------------------------------------
 template <int H, bool K0, bool BWD>
-__global__ void __launch_bounds__(256, 2) gnn_node_kernel(DevPolicy P, int k, int last) {
+__device__ __forceinline__ void gnn_node_body(const DevPolicy &P, int k, int last, int e_, int bx_, int gx_, double *gsm) {
     constexpr int NT = H / 8;
     constexpr int DK = K0 ? 7 : H;
     constexpr int K1 = DK + H;
     constexpr int KT1 = (K1 + 3) / 4;
-    extern __shared__ __align__(16) double gsm[];
-    const int e = blockIdx.y, lane = lane_id(), warp = threadIdx.x >> 5;
+    const int e = e_, lane = lane_id(), warp = threadIdx.x >> 5;
     const int warps = blockDim.x >> 5, n = P.n;
     const double s = P.slope;
     const bool feeds_sel = e == 0;
@@ -261,7 +271,7 @@ __global__ void __launch_bounds__(256, 2) gnn_node_kernel(DevPolicy P, int k, in
     const double *agg = P.AG[e][k];
     const int r = lane >> 2, c = lane & 3, c2 = c * 2;
     const int rows = P.rows;
-    for (int tile = blockIdx.x * warps + warp; tile * 8 < rows; tile += gridDim.x * warps) {
+    for (int tile = bx_ * warps + warp; tile * 8 < rows; tile += gx_ * warps) {
         const int v = tile * 8 + r;  // row (= vertex unless batched)
         const bool vok = v < rows;
         // ---- phi: A = [H_k | agg] (8 x K1) from global, fragments in registers ----
@@ -384,6 +394,61 @@ __global__ void __launch_bounds__(256, 2) gnn_node_kernel(DevPolicy P, int k, in
     }
 }
 
+template <int H, bool K0, bool BWD>
+__global__ void __launch_bounds__(256, 2) gnn_node_kernel(DevPolicy P, int k, int last) {
+    extern __shared__ __align__(16) double gsm[];
+    gnn_node_body<H, K0, BWD>(P, k, last, blockIdx.y, blockIdx.x, gridDim.x, gsm);
+}
+
+// ---------------------------------------------------------------------------
+// Explicit path lists (compact graphs): Sb[v] / St[v] = sum of H_sel over the
+// b / t path of v, in path order (the reference's sum), one warp per vertex,
+// lane = column, four independent row loads in flight.  The SEL head then
+// reads them like the forest form's pointer-jumped sums.
+// ---------------------------------------------------------------------------
+template <int H>
+__device__ __forceinline__ void gnn_pathsum_body(const DevPolicy &P, int bx_, int gx_) {
+    constexpr int HPL = (H + 31) / 32;
+    const int lane = lane_id(), warps = blockDim.x >> 5;
+    const double *Hs = P.H[0][P.K];
+    for (int v = bx_ * warps + (threadIdx.x >> 5); v < P.n; v += gx_ * warps) {
+#pragma unroll
+        for (int w = 0; w < 2; ++w) {
+            const int *pp = w == 0 ? P.bp_ptr : P.tp_ptr;
+            const int *pi = w == 0 ? P.bp_idx : P.tp_idx;
+            const int q0 = pp[v], q1 = pp[v + 1];
+            double acc[HPL];
+#pragma unroll
+            for (int t = 0; t < HPL; ++t) acc[t] = 0.0;
+            for (int q = q0; q < q1; q += 4) {
+                int u[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) u[i] = q + i < q1 ? pi[q + i] : -1;
+#pragma unroll
+                for (int t = 0; t < HPL; ++t) {
+                    const int j = lane + 32 * t;
+                    double x[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) x[i] = u[i] >= 0 && j < H ? Hs[(size_t)u[i] * H + j] : 0.0;
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        if (u[i] >= 0) acc[t] += x[i];
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < HPL; ++t) {
+                const int j = lane + 32 * t;
+                if (j < H) P.PS[w][0][(size_t)v * H + j] = acc[t];
+            }
+        }
+    }
+}
+
+template <int H>
+__global__ void __launch_bounds__(256) gnn_pathsum_kernel(DevPolicy P) {
+    gnn_pathsum_body<H>(P, blockIdx.x, gridDim.x);
+}
+
 // ---------------------------------------------------------------------------
 // SEL head (DMMA): s[v] = leaky([H | Sb | St | Zs] @ head1.w + b1) . head2.w + b2
 // A fragments straight from global (path sums from the pointer-jumping
@@ -392,14 +457,13 @@ __global__ void __launch_bounds__(256, 2) gnn_node_kernel(DevPolicy P, int k, in
 __host__ __device__ inline int sel_smem_doubles(int H) { return (4 * H / 4) * (H / 8) * 32; }
 
 template <int H, bool BWD>
-__global__ void __launch_bounds__(256, 2) gnn_sel_kernel(DevPolicy P) {
+__device__ __forceinline__ void gnn_sel_body(const DevPolicy &P, int e_, int bx_, int gx_, double *gsm) {
     constexpr int NT = H / 8;
     constexpr int KT = H;  // K = 4H
-    extern __shared__ __align__(16) double gsm[];
     const int lane = lane_id(), warp = threadIdx.x >> 5;
     const int warps = blockDim.x >> 5, n = P.n;
     const double s = P.slope;
-    if (blockIdx.x == 0 && warp == 0) {
+    if (bx_ == 0 && warp == 0) {
         // M = Wy @ W1c (5 x h), c = by @ W1c + b1  (PLC, policy.py:218-222)
         const double *yw = P.W(PR_PLC_Y_W), *yb = P.W(PR_PLC_Y_B), *w1 = P.W(PR_PLC_H1_W),
                      *b1 = P.W(PR_PLC_H1_B);
@@ -421,10 +485,11 @@ __global__ void __launch_bounds__(256, 2) gnn_sel_kernel(DevPolicy P) {
     __syncthreads();
     const double *Hs = P.H[0][P.K];
     const int rb = P.jump_rounds;
-    const double *Sb = P.forest && rb > 0 ? P.PS[0][(rb - 1) & 1] : Hs;
-    const double *St = P.forest && rb > 0 ? P.PS[1][(rb - 1) & 1] : Hs;
+    // path sums: pointer-jumped (forest) or gnn_pathsum (explicit lists)
+    const double *Sb = P.forest ? (rb > 0 ? P.PS[0][(rb - 1) & 1] : Hs) : P.PS[0][0];
+    const double *St = P.forest ? (rb > 0 ? P.PS[1][(rb - 1) & 1] : Hs) : P.PS[1][0];
     const int r = lane >> 2, c = lane & 3, c2 = c * 2;
-    for (int tile = blockIdx.x * warps + warp; tile * 8 < n; tile += gridDim.x * warps) {
+    for (int tile = bx_ * warps + warp; tile * 8 < n; tile += gx_ * warps) {
         const int v = tile * 8 + r;
         const bool vok = v < n;
         double acc[NT][2];
@@ -436,12 +501,7 @@ __global__ void __launch_bounds__(256, 2) gnn_sel_kernel(DevPolicy P) {
             if (vok) {
                 if (b == 0) x = Hs[(size_t)v * H + j];
                 else if (b == 3) x = P.Zs[(size_t)v * H + j];
-                else if (P.forest) x = (b == 1 ? Sb : St)[(size_t)v * H + j];
-                else {
-                    const int *pp = b == 1 ? P.bp_ptr : P.tp_ptr;
-                    const int *pi = b == 1 ? P.bp_idx : P.tp_idx;
-                    for (int q = pp[v]; q < pp[v + 1]; ++q) x += Hs[(size_t)pi[q] * H + j];
-                }
+                else x = (b == 1 ? Sb : St)[(size_t)v * H + j];
                 if constexpr (BWD) P.emb[(size_t)v * 4 * H + cc] = x;
             }
 #pragma unroll
@@ -461,6 +521,42 @@ __global__ void __launch_bounds__(256, 2) gnn_sel_kernel(DevPolicy P) {
         part += __shfl_xor_sync(FP_FULL_MASK, part, 1);
         part += __shfl_xor_sync(FP_FULL_MASK, part, 2);
         if (c == 0 && vok) P.s[v] = part + b2[0];
+    }
+}
+
+template <int H, bool BWD>
+__global__ void __launch_bounds__(256, 2) gnn_sel_kernel(DevPolicy P) {
+    extern __shared__ __align__(16) double gsm[];
+    gnn_sel_body<H, BWD>(P, blockIdx.y, blockIdx.x, gridDim.x, gsm);
+}
+
+// ---------------------------------------------------------------------------
+// Small graphs: the whole encode in ONE launch, one block per encoder
+// (proj0 -> K x (aggregation, node MLPs) -> SEL head on block 0), phases
+// separated by block barriers.  Same device bodies as the multi-block
+// kernels (bit-identical results); for a few hundred rows the six separate
+// launches were latency- and launch-bound.
+// ---------------------------------------------------------------------------
+constexpr int kSmallEncodeRows = 64;  // one 8-row tile per warp
+
+template <int H, bool BWD>
+__global__ void __launch_bounds__(256, 1) gnn_small_kernel(DevPolicy P) {
+    extern __shared__ __align__(16) double gsm[];
+    const int e = blockIdx.x;
+    gnn_proj0_body<H>(P, e, 0, 1, gsm);
+    __syncthreads();
+    for (int k = 0; k < P.K; ++k) {
+        gnn_agg_body<H>(P, k, e, 0, 1, gsm);
+        __syncthreads();
+        const int last = k == P.K - 1;
+        if (k == 0) gnn_node_body<H, true, BWD>(P, k, last, e, 0, 1, gsm);
+        else gnn_node_body<H, false, BWD>(P, k, last, e, 0, 1, gsm);
+        __syncthreads();
+    }
+    if (e == 0) {
+        gnn_pathsum_body<H>(P, 0, 1);
+        __syncthreads();
+        gnn_sel_body<H, BWD>(P, 0, 0, 1, gsm);
     }
 }
 

@@ -327,19 +327,29 @@ class PolicyContext:
             ft = torch.as_tensor(np.asarray(forced, dtype=np.int32).reshape(B, n, 2),
                                  device=dev) if not isinstance(forced, torch.Tensor) else forced
             ft = ft.to(dtype=torch.int32).contiguous()
-        args = N.FpRolloutArgs(
-            B, N.MODE[mode], float(epsilon), int(seed) & ((1 << 64) - 1),
-            int(episode_base) & 0xFFFFFFFF, _STRATEGY_CODE[strategy], int(simulate),
-            *[N.ptr(t).value for t in (ft, out.assign, out.step_vd, out.step_lp, out.step_ent,
-                                       out.step_argmax, out.step_ncand, out.makespan,
-                                       out.status, out.grad_rows, out.grad_ep, out.trace)],
-            out.trace.shape[1] // 16 if out.trace is not None else 0,
-            N.ptr(out.trace_len).value,
-            (N.FLAG_WIDE if wide else 0) | (N.FLAG_TIE_RANDOM if tie_random else 0) |
-            (N.FLAG_PER_STEP if self.per_step else 0))
-        ws = self.workspace(B, wide=wide, grad=out.grad_rows is not None)
-        args.workspace = N.ptr(ws).value
-        args.workspace_bytes = 0 if ws is None else ws.numel()
+        flags = ((N.FLAG_WIDE if wide else 0) | (N.FLAG_TIE_RANDOM if tie_random else 0) |
+                 (N.FLAG_PER_STEP if self.per_step else 0))
+        # the argument block is cached on the output batch (its pointers are
+        # fixed); per call only the scalars and the forced-action pointer change
+        key = (B, mode, simulate, strategy, flags)
+        args = getattr(out, "_args", None)
+        if args is None or out._args_key != key:
+            args = N.FpRolloutArgs(
+                B, N.MODE[mode], 0.0, 0, 0, _STRATEGY_CODE[strategy], int(simulate),
+                *[N.ptr(t).value for t in (None, out.assign, out.step_vd, out.step_lp,
+                                           out.step_ent, out.step_argmax, out.step_ncand,
+                                           out.makespan, out.status, out.grad_rows,
+                                           out.grad_ep, out.trace)],
+                out.trace.shape[1] // 16 if out.trace is not None else 0,
+                N.ptr(out.trace_len).value, flags)
+            ws = self.workspace(B, wide=wide, grad=out.grad_rows is not None)
+            args.workspace = N.ptr(ws).value
+            args.workspace_bytes = 0 if ws is None else ws.numel()
+            out._args, out._args_key, out._ws = args, key, ws
+        args.epsilon = float(epsilon)
+        args.seed = int(seed) & ((1 << 64) - 1)
+        args.episode_base = int(episode_base) & 0xFFFFFFFF
+        args.forced = N.ptr(ft).value
         N.check(N.lib().fp_rollout_batch(self.sim.handle, self.handle, ctypes.byref(args),
                                          N.stream_ptr(stream)))
         if self.per_step:
