@@ -790,7 +790,8 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
         const double ed = lane < D ? exp(lg - lmx) : 0.0;
         const double ecum = warp_scan_pow2<LOGD>(ed);
         const double etot = __shfl_sync(FP_FULL_MASK, ecum, D - 1);
-        const double pd = lane < D ? ed / etot : -1.0;
+        double pd = -1.0;  // only the log-prob / argmax consumers need p
+        if ((want_lp || want_amax || mode == FP_MODE_GREEDY) && lane < D) pd = ed / etot;
         int amax = -1;
         if (want_amax || mode == FP_MODE_GREEDY) {
             double am = pd;

@@ -66,3 +66,48 @@ def test_library_exports_every_declared_symbol():
     for sym in sorted(declared):
         assert hasattr(lib, sym), sym
     assert set(_native.EXPORTED) <= declared
+
+
+def test_feature_forests_reproduce_path_lists():
+    """The next-pointer forests the large-graph encoder consumes give the
+    reference's explicit b/t paths (features.py:88-95) and their lengths."""
+    for g in (builders.build_llama_block(), builders.sparse_dag(1500, seed=2)):
+        f = static_features(g, 4.0)
+        for which, paths, nxt in (("b", f.b_paths, f.b_next), ("t", f.t_paths, f.t_next)):
+            for v in range(0, len(g), 7):
+                walk = [v]
+                while nxt[walk[-1]] >= 0:
+                    walk.append(int(nxt[walk[-1]]))
+                assert tuple(walk) == paths[v]
+            assert f.path_lengths(which).tolist() == [len(p) for p in paths]
+
+
+def test_relabel_keeps_the_dag():
+    g = builders.sparse_dag(500, seed=1)
+    r = builders.relabel(g, seed=3)
+    assert G.validate(r) == []
+    assert len(r) == len(g) and len(r.edges) == len(g.edges)
+    # same multiset of (flops, bytes) and same degree sequence
+    assert sorted((v.flops, v.output_bytes) for v in r.vertices) == \
+        sorted((v.flops, v.output_bytes) for v in g.vertices)
+    assert sorted(len(r.preds(v)) for v in range(len(r))) == \
+        sorted(len(g.preds(v)) for v in range(len(g)))
+    # longest paths are relabelling-invariant
+    assert np.isclose(static_features(r, 4.0).t_level.max(), static_features(g, 4.0).t_level.max())
+
+
+def test_policy_config_modes():
+    from paper_2505_23131_b200.policy import PolicyConfig
+    assert PolicyConfig(mp_mode="per_step").mp_mode == "per_step"
+    with pytest.raises(ValueError):
+        PolicyConfig(mp_mode="sometimes")
+
+
+def test_layout_flags_are_distinct_bits():
+    from paper_2505_23131_b200 import _native as N
+    header = (ROOT / "include" / "flowplace_b200.h").read_text()
+    flags = {k: int(v) for k, v in re.findall(r"#define (FP_FLAG_\w+) (\d+)", header)}
+    assert flags == {"FP_FLAG_WIDE": N.FLAG_WIDE, "FP_FLAG_TIE_RANDOM": N.FLAG_TIE_RANDOM,
+                     "FP_FLAG_PER_STEP": N.FLAG_PER_STEP}
+    vals = list(flags.values())
+    assert all(v & (v - 1) == 0 for v in vals) and len(set(vals)) == len(vals)
