@@ -20,7 +20,7 @@ constexpr int kMaxTreeLevels = 6; // 32-ary candidate tree: n <= 32^6
 struct EpLayout {
     // ---- n-sized group (nb) ----
     int ce, cc, dsl, dse, tstart, tend, cand, npl, clist, order;
-    int rdy, missing, assign, bits;
+    int rdy, missing, cons, assign, bits;
     int tm, tz, tc, tt;  // candidate tree nodes (wide rollout): max, scaled sum, count, teacher max
     // ---- small group (sb) ----
     int xd, xn, stats, rsum, flag, ring, simres;
@@ -120,6 +120,7 @@ __host__ __device__ inline EpLayout make_layout(int n, int W, int R, int SM, boo
     L.skey = take_s(8 * P, 8);
     L.rdy = take_n(4LL * n, 4);
     L.missing = take_n(4LL * n, 4);
+    L.cons = take_n(4LL * n, 4);
     L.bits = take_n(4LL * R * L.BW, 4);
     L.cnt = take_s(4 * R, 4);
     L.pv = take_s(4 * P, 4);

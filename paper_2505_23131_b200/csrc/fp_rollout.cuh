@@ -296,14 +296,17 @@ __device__ __forceinline__ bool sel_chain(const DevProblem &PR, const DevPolicy 
 // words) -- quadratic at 10k-100k ops.  Here the candidate set is a 32-ary
 // tree over vertex ids whose node j at level l summarises leaves
 // [j*32^l, (j+1)*32^l): m = max SEL logit of its candidates, z = sum of
-// exp(s - m) over them, c = candidate count (t = max t-level for the
-// critical-path teacher).  A warp updates one node per level with one
-// coalesced 32-child load, a REDUX max and a butterfly sum, so insert /
-// remove / sample / argmax are O(log32 n) warp steps.  Sampling descends by
-// the cumulative weight in ascending-id order, i.e. the reference's
-// searchsorted(cumsum(p), u * sum(p), 'right') (policy.py:313-316), and the
-// uniform branch descends by count to the idx-th candidate in ascending
-// order; the entropy (only when requested) is one pass over the candidates.
+// exp(s - m) over them (each node keeps its own max: SEL logits grow with
+// the b/t path sums and span thousands of nats on 100k-op graphs, so no
+// global shift keeps every sum in range), c = candidate count, t = max
+// t-level (critical-path teacher).  A warp refreshes a node with one
+// coalesced 32-child load, a REDUX max, one exp per lane and a butterfly sum;
+// the ancestors touched by one step (the placed vertex and its newly ready
+// successors) are refreshed once each, level by level.  Sampling descends
+// by cumulative weight in ascending-id order -- the reference's
+// searchsorted(cumsum(p), u * sum(p), 'right') (policy.py:313-316) -- and
+// the uniform branch by count to the idx-th candidate in ascending order;
+// the entropy (only when requested) is one pass over the candidates.
 // ---------------------------------------------------------------------------
 struct TreeRef {
     double *tm, *tz, *tt;
@@ -339,8 +342,7 @@ struct TreeRef {
         int c;
         child(l, j, m, z, t, c);
         const double M = warp_max_redux(m);
-        const double zz = c > 0 ? z * exp(m - M) : 0.0;
-        const double Z = warp_sum(zz);
+        const double Z = warp_sum(c > 0 ? z * exp(m - M) : 0.0);
         const int C = __reduce_add_sync(FP_FULL_MASK, c);
         const double T = teacher ? warp_max_redux(t) : -INFINITY;
         if (lane_id() == 0) {
@@ -351,12 +353,27 @@ struct TreeRef {
         __syncwarp();
     }
 
-    // leaf v changed: refresh its ancestors bottom-up
-    __device__ __forceinline__ void update(int v) const {
-        for (int l = 1; l <= L->tl_n; ++l) recompute(l, v >> (5 * l));
+    // leaves held by the lanes (-1: none) changed: refresh every distinct
+    // ancestor once, bottom-up
+    __device__ __forceinline__ void update_many(int leaf) const {
+        for (int l = 1; l <= L->tl_n; ++l) {
+            const int id = leaf >= 0 ? leaf >> (5 * l) : -1;
+            const unsigned peers = __match_any_sync(FP_FULL_MASK, id);
+            unsigned todo = __ballot_sync(FP_FULL_MASK, id >= 0 && lane_id() == __ffs(peers) - 1);
+            while (todo) {
+                const int src = __ffs(todo) - 1;
+                todo &= todo - 1;
+                recompute(l, __shfl_sync(FP_FULL_MASK, id, src));
+            }
+        }
     }
 
     __device__ __forceinline__ int root() const { return L->tl_off[L->tl_n]; }
+
+    __device__ __forceinline__ void rebuild() const {
+        for (int l = 1; l <= L->tl_n; ++l)
+            for (int j = 0; j < L->tl_cnt[l]; ++j) recompute(l, j);
+    }
 
     // first leaf whose inclusive cumulative weight exceeds target (root units)
     __device__ __forceinline__ int descend_weight(double target) const {
@@ -373,7 +390,7 @@ struct TreeRef {
             const int sel = hit ? __ffs(hit) - 1 : 31 - __clz(nonempty);
             const double prev = __shfl_sync(FP_FULL_MASK, cum - w, sel);
             const double ms = __shfl_sync(FP_FULL_MASK, m, sel);
-            target = (target - prev) * exp(Mn - ms);
+            target = (target - prev) * exp(Mn - ms);  // into the child's units
             Mn = ms;
             j = (j << 5) + sel;
         }
@@ -455,10 +472,11 @@ __device__ __forceinline__ void sel_chain_wide(const DevProblem &PR, const DevPo
         if (np == 0) atomicOr(&cand[v >> 5], 1u << (v & 31));
     }
     __syncwarp();
-    for (int l = 1; l <= L.tl_n; ++l)
-        for (int j = 0; j < L.tl_cnt[l]; ++j) T.recompute(l, j);
+    T.rebuild();
 
     const int rt = T.root();
+    FP_PHASE_DECL;
+    FP_PHASE_BEGIN(pw);
     double dc1 = 0.0, dc2 = 0.0;  // draw cache (step_draw)
     const bool tie_rand = mode == FP_MODE_TEACHER && (A.flags & FP_FLAG_TIE_RANDOM);
     for (int step = 0; step < n; ++step) {
@@ -470,7 +488,7 @@ __device__ __forceinline__ void sel_chain_wide(const DevProblem &PR, const DevPo
             ring_publish(ring, dead, step, -1);
             return;
         }
-        const double Mr = T.tm[rt], Zr = T.tz[rt];
+        const double Mr = T.tm[rt], Zr = T.tz[rt];  // p = exp(s - Mr) / Zr
         int v = -1;
         if (mode == FP_MODE_FORCED) {
             const int fv = frow[2 * step];
@@ -530,6 +548,7 @@ __device__ __forceinline__ void sel_chain_wide(const DevProblem &PR, const DevPo
             ring_publish(ring, dead, step, -2);
             return;
         }
+        FP_PHASE_END(pw, 5);
         if (!ring_publish(ring, dead, step, v)) return;
         if (want_lp) {
             const double ek = eps / (double)k;
@@ -562,25 +581,35 @@ __device__ __forceinline__ void sel_chain_wide(const DevProblem &PR, const DevPo
             atomicAnd(&cand[v >> 5], ~(1u << (v & 31)));
         }
         __syncwarp();
-        T.update(v);
-        // successors whose last predecessor was just placed become candidates
-        for (int j0 = sp[v]; j0 < sp[v + 1]; j0 += 32) {
-            const int j = j0 + lane;
-            int w = -1;
-            if (j < sp[v + 1]) {
-                w = si[j];
-                if (--npl[w] == 0) atomicOr(&cand[w >> 5], 1u << (w & 31));
-                else w = -1;
-            }
-            __syncwarp();
-            unsigned ready = __ballot_sync(FP_FULL_MASK, w >= 0);
-            while (ready) {
-                const int src = __ffs(ready) - 1;
-                ready &= ready - 1;
-                T.update(__shfl_sync(FP_FULL_MASK, w, src));
+        FP_PHASE_END(pw, 6);
+        // successors whose last predecessor was just placed become candidates;
+        // the changed leaves (v on lane 0 in the first round, then the new
+        // candidates) refresh their ancestors once each
+        {
+            const int end_j = sp[v + 1];
+            int base_j = sp[v];
+            for (bool first = true;; first = false) {
+                const int off = first ? 1 : 0;
+                const int j = base_j + lane - off;
+                int changed = -1;
+                if (first && lane == 0) {
+                    changed = v;
+                } else if (j < end_j) {
+                    const int w = si[j];
+                    if (--npl[w] == 0) {
+                        atomicOr(&cand[w >> 5], 1u << (w & 31));
+                        changed = w;
+                    }
+                }
+                __syncwarp();
+                T.update_many(changed);
+                base_j += 32 - off;
+                if (base_j >= end_j) break;
             }
         }
+        FP_PHASE_END(pw, 7);
     }
+    FP_PHASE_FLUSH(0);
 }
 
 // ---------------------------------------------------------------------------

@@ -125,6 +125,7 @@ __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *nb, 
     const int lane = lane_id();
     const int n = P.n, d = P.d, R = P.R, SM = P.SM, BW = L.BW;
     uint32_t *rdy = (uint32_t *)(nb + L.rdy);
+    uint32_t *cons = (uint32_t *)(nb + L.cons);
     int *missing = (int *)(nb + L.missing);
     const uint8_t *assign = nb + L.assign;
     uint32_t *bits = (uint32_t *)(nb + L.bits);
@@ -150,6 +151,11 @@ __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *nb, 
     for (int v = lane; v < n; v += 32) {
         const bool e = ent[v];
         rdy[v] = e ? dmask : 0u;
+        if constexpr (!OVL) {  // consumer devices (_simcore.pyx:84-97), all placed
+            uint32_t c = 0;
+            for (int j = sp[v]; j < sp[v + 1]; ++j) c |= 1u << assign[si[j]];
+            cons[v] = c;
+        }
         int miss = 0;
         for (int j = P.pred_ptr[v]; j < P.pred_ptr[v + 1]; ++j) miss += !ent[P.pred_idx[j]];
         missing[v] = miss;
@@ -345,9 +351,14 @@ __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *nb, 
                     dev = r;
                     atomicOr(&rdy[v], 1u << r);
                     ++done_exec;
-                    // consumer devices of v (_simcore.pyx:84-97), known once placed
+                    // consumer devices of v (_simcore.pyx:84-97); overlapped: only
+                    // known now that every successor is placed
                     uint32_t m = 0u;
-                    for (int j = sp[v]; j < sp[v + 1]; ++j) m |= 1u << assign[si[j]];
+                    if constexpr (OVL) {
+                        for (int j = sp[v]; j < sp[v + 1]; ++j) m |= 1u << assign[si[j]];
+                    } else {
+                        m = cons[v];
+                    }
                     m &= ~(1u << r);
                     const int pos = rpos[v];
                     while (m) {

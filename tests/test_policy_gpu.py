@@ -299,3 +299,22 @@ def test_dmma_encoder_matches_fused_encoder(which, torch_cuda):
         x, y = a.read_table(name), b.read_table(name)
         np.testing.assert_allclose(x, y, rtol=1e-12, atol=1e-13 * max(1.0, np.abs(y).max()),
                                    err_msg=f"{which}:{name}")
+
+
+def test_wide_tree_underflow_fallback(torch_cuda):
+    """Logits spread over thousands of nats: candidate weights exp(s - max s)
+    underflow to zero and the wide kernel takes its max-shifted slow pass;
+    actions and log-probs still match the compact kernel."""
+    g, cl = builders.build_llama_block(), ClusterSpec.uniform(8, 1e9, 1e7)
+    pc = PolicyConfig()
+    params = init_policy_params(pc, seed=4)
+    params["sel.head2.w"].data = params["sel.head2.w"].data * 4000.0
+    ctx = PolicyContext(g, cl, pc)
+    ctx.prepare(params)
+    s = ctx.read_table("sel_logit")
+    assert s.max() - s.min() > 1000.0
+    a = _rollout_np(ctx.rollout_batch(params, 32, 0.2, 5, trace_steps=True))
+    b = _rollout_np(ctx.rollout_batch(params, 32, 0.2, 5, trace_steps=True, wide=True))
+    assert (a["status"] == 0).all() and (b["status"] == 0).all()
+    assert np.array_equal(a["step_vd"], b["step_vd"]) and np.array_equal(a["makespan"], b["makespan"])
+    np.testing.assert_allclose(b["step_lp"], a["step_lp"], rtol=1e-9, atol=1e-12)

@@ -22,7 +22,7 @@ from paper_2505_23131_b200.params import init_policy_params  # noqa: E402
 from paper_2505_23131_b200.policy import PolicyConfig, PolicyContext  # noqa: E402
 
 NAMES = {0: "sel.compact", 1: "sel.softmax", 2: "sel.decide+publish", 3: "sel.lp/ent",
-         4: "sel.cand-update", 10: "plc.wait-order", 11: "plc.features", 12: "plc.stats+xn",
+         4: "sel.cand-update", 5: "sel.tree-decide", 6: "sel.publish+lp", 7: "sel.tree-update", 10: "plc.wait-order", 11: "plc.features", 12: "plc.stats+xn",
          13: "plc.preact+reduce", 14: "plc.softmax", 15: "plc.decide", 16: "plc.lp/grad",
          17: "plc.commit", 21: "sim.start", 23: "sim.tmin", 24: "sim.complete"}
 
@@ -43,6 +43,7 @@ for i in range(3):
     ctx.rollout_batch(flat, a.batch, EPSILON, 100 + i, out=out)
 torch.cuda.synchronize()
 lib.fp_phase_read(cyc, cnt, 1)
+lib.fp_phase_read_wide(cyc, cnt, 1)
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 ev[0].record()
 ctx.rollout_batch(flat, a.batch, EPSILON, 999, out=out, prepare=False)
@@ -50,6 +51,12 @@ ev[1].record()
 torch.cuda.synchronize()
 ms = ev[0].elapsed_time(ev[1])
 lib.fp_phase_read(cyc, cnt, 1)
+cyc2 = (ctypes.c_ulonglong * 64)()
+cnt2 = (ctypes.c_ulonglong * 64)()
+lib.fp_phase_read_wide(cyc2, cnt2, 1)
+for i in range(64):  # wide-kernel counters live in their own translation unit
+    cyc[i] += cyc2[i]
+    cnt[i] += cnt2[i]
 print(f"{a.workload}: rollout+sim launch {ms:.3f} ms (instrumented)")
 tot = {"sel": 0, "plc": 0, "sim": 0}
 for i in sorted(NAMES):
