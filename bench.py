@@ -297,8 +297,7 @@ def run_ours(args):
             alg += B * n * 4 * h * 8  # REINFORCE rows written
         per_step = args.mp_mode == "per_step"
         K = pc.k_rounds
-        jumps = ctx.jump_rounds() if hasattr(ctx, "jump_rounds") else 0
-        prep_launches = 2 * K + 2 + jumps  # proj0, K x (aggregation, node), [jumps], SEL head
+        prep_launches = ctx.encode_launches()
         if per_step:
             # per step: 2 encoders x K rounds of aggregation over B*n rows (the
             # HBM-bound part) -- node MLP traffic not counted

@@ -33,13 +33,11 @@ struct PsState {
     int *order;      // [B*n] placement order
     double *tstart, *tend;   // [B*n] timeline
     double *avail, *aflops;  // [B][32]
-    int *cid;        // [B*n] candidate list scratch
-    double *cs;      // [B*n] candidate logits scratch
     int *stat;       // [B] FP_EP_* (non-zero: episode stopped)
 };
 
 struct PsLayout {
-    int64_t dev, npl, cand, order, tstart, tend, avail, aflops, cid, cs, stat;
+    int64_t dev, npl, cand, order, tstart, tend, avail, aflops, stat;
     int64_t H[2][kMaxRounds + 1], Pm[2][kMaxRounds], Qm[2][kMaxRounds], AG[2][kMaxRounds];
     int64_t Zs, A, G;
     int64_t bytes;
@@ -58,7 +56,7 @@ static PsLayout ps_layout(int n, int B, int h, int K, int n_enc, int W) {
     L.dev = take(4 * R); L.npl = take(4 * R); L.cand = take(4LL * B * W); L.order = take(4 * R);
     L.tstart = take(8 * R); L.tend = take(8 * R);
     L.avail = take(8LL * B * 32); L.aflops = take(8LL * B * 32);
-    L.cid = take(4 * R); L.cs = take(8 * R); L.stat = take(4LL * B);
+    L.stat = take(4LL * B);
     for (int e = 0; e < n_enc; ++e) {
         L.H[e][0] = take(8 * R * 7);
         for (int k = 0; k < K; ++k) {
@@ -516,7 +514,7 @@ int per_step_rollout(const fp_problem *p, const fp_policy *pol, const fp_rollout
     S.dev = (int *)(w + L.dev); S.npl = (int *)(w + L.npl); S.cand = (uint32_t *)(w + L.cand);
     S.order = (int *)(w + L.order); S.tstart = (double *)(w + L.tstart);
     S.tend = (double *)(w + L.tend); S.avail = (double *)(w + L.avail);
-    S.aflops = (double *)(w + L.aflops); S.cid = (int *)(w + L.cid); S.cs = (double *)(w + L.cs);
+    S.aflops = (double *)(w + L.aflops);
     S.stat = (int *)(w + L.stat);
     DevPolicy PB = PO;  // weights + graph constants shared; activations over B*n rows
     PB.rows = n * B;

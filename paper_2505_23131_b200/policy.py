@@ -255,6 +255,17 @@ class PolicyContext:
             self._lib.fp_policy_destroy(h)
             self.handle = None
 
+    def encode_launches(self) -> int:
+        """Kernel launches of one prepare: a single fused launch for graphs of
+        <= 64 ops; else proj0 + K x (aggregation, node MLPs) + path sums (or
+        the pointer-jumping rounds) + SEL head (fp_encode.cu)."""
+        K = self.config.k_rounds
+        if self.config.hidden in (8, 16, 32, 64):
+            if len(self.graph) <= 64 and not self.forest:
+                return 1
+            return 2 * K + 2 + (self.jump_rounds() if self.forest else 1)
+        return K + 1  # fused per-vertex encoder
+
     def jump_rounds(self) -> int:
         """Pointer-jumping launches per prepare (forest-form paths only)."""
         if not self.forest:

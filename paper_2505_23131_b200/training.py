@@ -185,8 +185,7 @@ class BatchedTrainer:
         # encode (K+1) + rollout + reduce (2) + alpha/baseline (torch ops: not ours)
         # + backward (head 2 + outer 2 + small 1 + per (enc, round) 3 (+copy)) + sgd
         per_round = n_enc * pc.k_rounds * 4 - n_enc
-        # encode: proj0 + K x (aggregation, node MLP) + SEL head
-        return (2 * pc.k_rounds + 2) + 1 + 2 + 5 + per_round + 1
+        return self.ctx.encode_launches() + 1 + 2 + 5 + per_round + 1
 
     def step(self, seed: int, out=None, kernel_events=None, record=False):
         """One update over B local episodes.  Returns host stats when
