@@ -207,7 +207,10 @@ class BatchedTrainer:
                           simulate=self.executor is None, strategy=self.config.strategy)
         if kernel_events is not None:
             kernel_events[1].record()
-        if self.executor is not None:
+        if self.executor is not None and hasattr(self.executor, "batch"):
+            # Stage III with a batched executor: the whole batch in one call
+            out.makespan = self.executor.batch(ctx, out.assign)
+        elif self.executor is not None:
             # Stage III: rewards from an external executor (host callable)
             assign = out.assign.cpu().numpy()
             mk = [float(self.executor(ctx.graph, Assignment(tuple(int(x) for x in a))))
@@ -296,6 +299,14 @@ def system_rl_stage(graph, cluster, executor, config, pconfig, params, context=N
         except Exception as exc:  # noqa: BLE001 — reference wraps every failure
             raise RuntimeError(f"executor failed: {exc}") from exc
 
+    if hasattr(executor, "batch"):  # a batched executor scores the whole batch at once
+        def safe_batch(ctx, assign):
+            try:
+                return executor.batch(ctx, assign)
+            except Exception as exc:  # noqa: BLE001
+                raise RuntimeError(f"executor failed: {exc}") from exc
+        safe.batch = safe_batch
+
     return _stage("system_rl", graph, cluster, config, pconfig, params, context, batch_size,
                   executor=safe, **kw)
 
@@ -315,8 +326,41 @@ class SimulatorExecutor:
 
     def __call__(self, graph: DataflowGraph, assignment) -> float:
         seed = self.base_seed + next(self._calls)
-        mk = exec_time_batch(graph, [list(assignment)], self.cluster, self.strategy, seed=seed)
-        return float(mk[0])
+        prob = self._problem(graph)
+        import torch
+        a = torch.tensor([list(assignment)], dtype=torch.int32, device="cuda")
+        jit = prob.jitter_table(seed)
+        jt = torch.from_numpy(jit).cuda() if jit is not None else None
+        out = prob.simulate(a, self.strategy, jitter=jt)
+        if int(out["status"][0]) != 0:
+            raise RuntimeError("simulation deadlocked")
+        return float(out["makespan"][0])
+
+    def _problem(self, graph: DataflowGraph):
+        from .simulate import SimProblem
+
+        prob = getattr(self, "_prob", None)
+        if prob is None or prob.graph is not graph:
+            self._prob = prob = SimProblem(graph, self.cluster)
+        return prob
+
+    def batch(self, ctx, assign):
+        """Makespans of a device batch of assignments [B, n] in one launch:
+        episode i gets the i-th next seed of the call stream, exactly as B
+        successive calls would (per-task jitter factors from the reference's
+        host libm recipe, one table per episode)."""
+        import torch
+
+        prob = self._problem(ctx.graph)
+        B = assign.shape[0]
+        seeds = [self.base_seed + next(self._calls) for _ in range(B)]
+        jt = None
+        if self.cluster.jitter_sigma > 0:
+            jt = torch.from_numpy(np.stack([prob.jitter_table(sd) for sd in seeds])).cuda()
+        out = prob.simulate(assign, self.strategy, jitter=jt)
+        if bool((out["status"] != 0).any()):
+            raise RuntimeError("simulation deadlocked")
+        return out["makespan"]
 
 
 SIDECAR_SUFFIX = ".sidecar.json"

@@ -124,3 +124,21 @@ def test_sim_rl_stage_improves_on_fixture(torch_cuda):
     assert res.best_makespan <= rand.mean()
     assert res.best_makespan <= 1.10 * oracle
     assert exec_time(g, res.best_assignment, cl)[0] == res.best_makespan
+
+
+def test_system_rl_batched_executor_matches_per_call():
+    """Stage III (training.py:235-248) with the jittered simulator executor:
+    the batched path (one simulation launch per update, per-episode seeds in
+    call order) gives the same rewards and updates as per-episode calls."""
+    from paper_2505_23131_b200.training import SimulatorExecutor, TrainConfig, system_rl_stage
+    g, cl = builders.build_chainmm(64, 2), ClusterSpec.uniform(4, 1e6, 1e5)
+    pc = PolicyConfig(hidden=16, k_rounds=1)
+    cfg = TrainConfig(episodes=8, seed=0)
+    batched = SimulatorExecutor(cl, jitter_sigma=0.1, base_seed=5)
+    per_call = SimulatorExecutor(cl, jitter_sigma=0.1, base_seed=5)
+    r1 = system_rl_stage(g, cl, batched, cfg, pc, init_policy_params(pc, 0), batch_size=4)
+    r2 = system_rl_stage(g, cl, lambda gg, a: per_call(gg, a), cfg, pc,
+                         init_policy_params(pc, 0), batch_size=4)
+    m1 = [row["makespan_ms"] for row in r1.curve]
+    m2 = [row["makespan_ms"] for row in r2.curve]
+    assert m1 == m2 and len(m1) == 8
