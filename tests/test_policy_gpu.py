@@ -318,3 +318,37 @@ def test_wide_tree_underflow_fallback(torch_cuda):
     assert (a["status"] == 0).all() and (b["status"] == 0).all()
     assert np.array_equal(a["step_vd"], b["step_vd"]) and np.array_equal(a["makespan"], b["makespan"])
     np.testing.assert_allclose(b["step_lp"], a["step_lp"], rtol=1e-9, atol=1e-12)
+
+
+@pytest.mark.parametrize("wide", [False, True])
+def test_multi_slot_cluster_rollouts_match_oracle(wide, torch_cuda):
+    """Clusters with several exec / transfer slots per resource take the
+    shared-memory in-flight pool (not the single-slot register path) in the
+    overlapped (compact) and wide simulators; sampled episodes and their
+    makespans still match the oracle."""
+    rng = np.random.default_rng(3)
+    d = 4
+    bw = rng.uniform(1e4, 1e5, size=(d, d))
+    cl = ClusterSpec(d, tuple(rng.uniform(5e5, 2e6, size=d)), tuple(map(tuple, bw)),
+                     (2, 1, 3, 2), tuple(tuple(int(x) for x in r)
+                                         for r in rng.integers(1, 3, size=(d, d))))
+    g = builders.build_chainmm(64, 2)
+    pc = PolicyConfig(hidden=16, k_rounds=2)
+    params = init_policy_params(pc, seed=6)
+    ctx = PolicyContext(g, cl, pc)
+    B, seed = 24, 9
+    rb = ctx.rollout_batch(params, B, 0.3, seed, trace_steps=True, wide=wide, sim_trace=True)
+    assert (rb.status.cpu().numpy() == 0).all()
+    vd, mk = rb.step_vd.cpu().numpy(), rb.makespan.cpu().numpy()
+    assign = rb.assign.cpu().numpy()
+    from paper_2505_23131_b200.simulate import decode_events
+    tr, tl = rb.trace.cpu().numpy(), rb.trace_len.cpu().numpy()
+    octx = _oracle_ctx(ctx)
+    P = OP.leaves(params, need=False)
+    for b in (0, 11, 23):
+        ro = OP.rollout(P, octx, 0.3, mode="uniform", seed=seed, episode=b)
+        assert [(int(x), int(y)) for x, y in vd[b]] == [(s["vertex"], s["device"])
+                                                        for s in ro["steps"]]
+        omk, oev = osim.exec_time(g, assign[b], cl)
+        assert mk[b] == omk
+        assert decode_events(tr[b], int(tl[b])) == oev
