@@ -352,3 +352,37 @@ def test_multi_slot_cluster_rollouts_match_oracle(wide, torch_cuda):
         omk, oev = osim.exec_time(g, assign[b], cl)
         assert mk[b] == omk
         assert decode_events(tr[b], int(tl[b])) == oev
+
+
+@pytest.mark.parametrize("d", [3, 6, 12])
+def test_odd_device_counts_match_oracle(d, torch_cuda):
+    """Device counts that are not powers of two (true division in the
+    standardisation, padded device lanes in the PLC reductions)."""
+    g = builders.build_ffnn(8, 4, 16, 4, 2)
+    cl = ClusterSpec.uniform(d, 1e6, 1e5)
+    pc = PolicyConfig(hidden=16, k_rounds=2)
+    params = init_policy_params(pc, seed=8)
+    ctx = PolicyContext(g, cl, pc)
+    B, seed = 16, 21
+    rb = ctx.rollout_batch(params, B, 0.2, seed, trace_steps=True)
+    assert (rb.status.cpu().numpy() == 0).all()
+    vd, lp, mk = rb.step_vd.cpu().numpy(), rb.step_lp.cpu().numpy(), rb.makespan.cpu().numpy()
+    octx = _oracle_ctx(ctx)
+    P = OP.leaves(params, need=False)
+    for b in (0, 15):
+        ro = OP.rollout(P, octx, 0.2, mode="uniform", seed=seed, episode=b)
+        assert [(int(x), int(y)) for x, y in vd[b]] == [(s["vertex"], s["device"])
+                                                        for s in ro["steps"]]
+        for t, s in enumerate(ro["steps"]):
+            assert _close(lp[b, t, 1], s["plc_logprob"])
+        omk, _ = osim.exec_time(g, rb.assign.cpu().numpy()[b], cl)
+        assert mk[b] == omk
+    # per_step on the same odd cluster
+    pc2 = PolicyConfig(hidden=16, k_rounds=1, mp_mode="per_step")
+    ctx2 = PolicyContext(g, cl, pc2)
+    p2 = init_policy_params(pc2, seed=8)
+    rb2 = ctx2.rollout_batch(p2, 4, 0.2, seed, trace_steps=True)
+    ro = OP.rollout(OP.leaves(p2, need=False), _oracle_ctx(ctx2), 0.2, mode="uniform", seed=seed,
+                    episode=1, per_step=True)
+    assert [(int(x), int(y)) for x, y in rb2.step_vd.cpu().numpy()[1]] == \
+        [(s["vertex"], s["device"]) for s in ro["steps"]]
