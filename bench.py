@@ -336,6 +336,11 @@ def run_ours(args):
                          "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "kernel_ms": kms, "alg_bytes_per_launch": alg,
+                         "note": ("B x n batched encodes per step; aggregation bytes over the "
+                                  "whole rollout" if per_step else
+                                  "latency-bound: each episode is a dependent chain of n "
+                                  "decisions + the overlapped simulation (DESIGN.md section 4); "
+                                  "GNN kernels' rooflines in profiles/r1_ncu_*"),
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
         }
         if clk:
