@@ -104,6 +104,7 @@ ps_step_kernel(DevProblem PR, DevPolicy PO, DevPolicy PB, fp_rollout_args A, PsS
     __shared__ double cs[1024];
     __shared__ int cid[1024];
     __shared__ int k_sm;
+    __shared__ double sd_part[kPsWarps - 1][MAXD * HPL <= 16 ? MAXD : 1][MAXD * HPL <= 16 ? 32 * HPL : 1];
     const int lane = lane_id(), warp = threadIdx.x >> 5;
     const int ep = blockIdx.x;
     if (ep >= A.B || S.stat[ep] != FP_EP_OK) return;  // block-uniform
@@ -187,8 +188,58 @@ ps_step_kernel(DevProblem PR, DevPolicy PO, DevPolicy PB, fp_rollout_args A, PsS
         part = warp_sum(part);
         if (lane == 0) cs[i] = part + b2;
     }
+    // h_d partial sums: h_d = sum of this step's G rows over the vertices
+    // placed on d (before this step) -- independent of this step's choices,
+    // so every warp takes a contiguous quarter of the placement order
+    constexpr bool SPLIT = MAXD * HPL <= 16;
+    double Sd[MAXD][HPL];
+#pragma unroll
+    for (int d = 0; d < MAXD; ++d)
+#pragma unroll
+        for (int t = 0; t < HPL; ++t) Sd[d][t] = 0.0;
+    {
+        const int nw = SPLIT ? kPsWarps : 1;
+        const int chunk = (step + nw - 1) / nw;
+        const int i_lo = SPLIT ? warp * chunk : 0, i_hi = SPLIT ? min(step, i_lo + chunk) : step;
+        if (SPLIT || warp == 0)
+            for (int i0 = i_lo; i0 < i_hi; i0 += 32) {
+                // 32 placed vertices at a time: lane i loads (u, d_u), then the G
+                // rows are summed in placement order (independent loads in flight)
+                const int cnt = min(32, i_hi - i0);
+                const int my_u = lane < cnt ? S.order[base + i0 + lane] : 0;
+                const int my_d = lane < cnt ? S.dev[base + my_u] : -1;
+#pragma unroll 4
+                for (int i = 0; i < cnt; ++i) {
+                    const int u = __shfl_sync(FP_FULL_MASK, my_u, i);
+                    const int du = __shfl_sync(FP_FULL_MASK, my_d, i);
+#pragma unroll
+                    for (int t = 0; t < HPL; ++t) {
+                        const int j = lane + 32 * t;
+                        const double g = j < h ? PB.G[(base + u) * h + j] : 0.0;
+#pragma unroll
+                        for (int d = 0; d < MAXD; ++d)
+                            if (d == du) Sd[d][t] += g;
+                    }
+                }
+            }
+        if constexpr (SPLIT) {
+            if (warp != 0)
+#pragma unroll
+                for (int d = 0; d < MAXD; ++d)
+#pragma unroll
+                    for (int t = 0; t < HPL; ++t)
+                        sd_part[warp - 1][d][lane + 32 * t] = Sd[d][t];
+        }
+    }
     __syncthreads();
     if (warp != 0) return;
+    if constexpr (SPLIT)  // fixed order: warp 0's quarter, then warps 1, 2, 3
+#pragma unroll
+        for (int w = 0; w < kPsWarps - 1; ++w)
+#pragma unroll
+            for (int d = 0; d < MAXD; ++d)
+#pragma unroll
+                for (int t = 0; t < HPL; ++t) Sd[d][t] += sd_part[w][d][lane + 32 * t];
     // masked softmax over the candidates in ascending-id order (policy.py:204)
     double mx = -INFINITY;
     for (int i = lane; i < k; i += 32) mx = fmax(mx, cs[i]);
@@ -332,32 +383,6 @@ ps_step_kernel(DevProblem PR, DevPolicy PO, DevPolicy PB, fp_rollout_args A, PsS
         xn[i] = __dmul_rn(__dsub_rn(xd[i], stats[c]), stats[5 + c]);
     }
     __syncwarp();
-    // h_d = sum of this step's G rows over the vertices placed on d
-    double Sd[MAXD][HPL];
-#pragma unroll
-    for (int d = 0; d < MAXD; ++d)
-#pragma unroll
-        for (int t = 0; t < HPL; ++t) Sd[d][t] = 0.0;
-    for (int i0 = 0; i0 < step; i0 += 32) {
-        // 32 placed vertices at a time: lane i loads (u, d_u), then the G rows
-        // are summed in placement order (independent row loads in flight)
-        const int cnt = min(32, step - i0);
-        const int my_u = lane < cnt ? S.order[base + i0 + lane] : 0;
-        const int my_d = lane < cnt ? S.dev[base + my_u] : -1;
-#pragma unroll 4
-        for (int i = 0; i < cnt; ++i) {
-            const int u = __shfl_sync(FP_FULL_MASK, my_u, i);
-            const int du = __shfl_sync(FP_FULL_MASK, my_d, i);
-#pragma unroll
-            for (int t = 0; t < HPL; ++t) {
-                const int j = lane + 32 * t;
-                const double g = j < h ? PB.G[(base + u) * h + j] : 0.0;
-#pragma unroll
-                for (int d = 0; d < MAXD; ++d)
-                    if (d == du) Sd[d][t] += g;
-            }
-        }
-    }
     const double *w2p = PO.W(PR_PLC_H2_W);
     const double b2p = PO.W(PR_PLC_H2_B)[0];
     double part[MAXD];
