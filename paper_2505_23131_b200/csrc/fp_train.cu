@@ -287,23 +287,47 @@ struct OuterJob {
     int ldx, xoff, K, ldy, rows, h;
 };
 
-__global__ void outer_kernel(const OuterJob *jobs) {
+// Weight gradients as row contractions out[i][j] = sum_r X[r][xoff+i] * Y[r][j]
+// (X == NULL: a bias, X = 1).  One block per output row i: the 8 warps take
+// contiguous row chunks (lane = column), and the chunk partials are summed in
+// warp order -- deterministic, and the rows no longer form one long
+// dependent chain per output element.
+constexpr int kOuterWarps = 8;
+
+__global__ void __launch_bounds__(kOuterWarps * 32) outer_kernel(const OuterJob *jobs) {
+    __shared__ double part[kOuterWarps][64];
     const OuterJob J = jobs[blockIdx.y];
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= J.K * J.h) return;
-    const int i = idx / J.h, j = idx - i * J.h;
-    double acc = 0.0;
-    for (int r = 0; r < J.rows; ++r) {
+    const int i = blockIdx.x;
+    if (i >= J.K) return;  // block-uniform
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int chunk = (J.rows + kOuterWarps - 1) / kOuterWarps;
+    const int r0 = warp * chunk, r1 = min(J.rows, r0 + chunk);
+    double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll 4
+    for (int r = r0; r < r1; ++r) {
         const double x = J.X ? J.X[(size_t)r * J.ldx + J.xoff + i] : 1.0;
-        acc = fma(x, J.Y[(size_t)r * J.ldy + j], acc);
+        const double *y = J.Y + (size_t)r * J.ldy;
+        if (lane < J.h) acc0 = fma(x, y[lane], acc0);
+        if (lane + 32 < J.h) acc1 = fma(x, y[lane + 32], acc1);
     }
-    J.out[(size_t)i * J.h + j] = acc;
+    part[warp][lane] = acc0;
+    part[warp][lane + 32] = acc1;
+    __syncthreads();
+    if (warp == 0) {
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+        for (int w = 0; w < kOuterWarps; ++w) { a0 += part[w][lane]; a1 += part[w][lane + 32]; }
+        if (lane < J.h) J.out[(size_t)i * J.h + lane] = a0;
+        if (lane + 32 < J.h) J.out[(size_t)i * J.h + lane + 32] = a1;
+    }
 }
 
 // PLC small terms + SEL head2 (single block): dWy = dM @ W1c^T, dby = dc @ W1c^T,
 // db1 = dc, dw2/db2 from the reduction, SEL w2 / b2.
-__global__ void small_bwd_kernel(DevPolicy P, double *grad) {
+__global__ void __launch_bounds__(256) small_bwd_kernel(DevPolicy P, double *grad) {
+    __shared__ double part[8][65];  // [warp][column | sum of ds]
     const int h = P.h, n = P.n;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const double *dc = P.dsmall, *dM = P.dsmall + h, *dw2 = P.dsmall + 6 * h;
     const double db2 = P.dsmall[7 * h];
     const double *w1p = P.W(PR_PLC_H1_W);
@@ -318,16 +342,32 @@ __global__ void small_bwd_kernel(DevPolicy P, double *grad) {
     for (int j = threadIdx.x; j < h; j += blockDim.x) {
         grad[P.off[PR_PLC_H1_B] + j] = dc[j];
         grad[P.off[PR_PLC_H2_W] + j] = dw2[j];
-        // SEL head2: dw2[j] = sum_v ds_v * leaky(hidpre[v][j])
-        double acc = 0.0;
-        for (int v = 0; v < n; ++v) acc = fma(P.ds[v], lk_t(P.hidpre[(size_t)v * h + j], P.slope), acc);
-        grad[P.off[PR_SEL_H2_W] + j] = acc;
     }
-    if (threadIdx.x == 0) {
-        grad[P.off[PR_PLC_H2_B]] = db2;
-        double acc = 0.0;
-        for (int v = 0; v < n; ++v) acc += P.ds[v];
-        grad[P.off[PR_SEL_H2_B]] = acc;
+    // SEL head2: dw2[j] = sum_v ds_v * leaky(hidpre[v][j]), db2 = sum_v ds_v: the
+    // 8 warps take contiguous vertex chunks (lane = column), then the chunk
+    // partials are summed in warp order (deterministic)
+    const int chunk = (n + 7) / 8, v0 = warp * chunk, v1 = min(n, v0 + chunk);
+    double a0 = 0.0, a1 = 0.0, sd = 0.0;
+    for (int v = v0; v < v1; ++v) {
+        const double dsv = P.ds[v];
+        if (lane < h) a0 = fma(dsv, lk_t(P.hidpre[(size_t)v * h + lane], P.slope), a0);
+        if (lane + 32 < h) a1 = fma(dsv, lk_t(P.hidpre[(size_t)v * h + lane + 32], P.slope), a1);
+        sd += dsv;
+    }
+    part[warp][lane] = a0;
+    part[warp][lane + 32] = a1;
+    if (lane == 0) part[warp][64] = sd;
+    __syncthreads();
+    if (warp == 0) {
+        double b0 = 0.0, b1 = 0.0, bs = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) { b0 += part[w][lane]; b1 += part[w][lane + 32]; bs += part[w][64]; }
+        if (lane < h) grad[P.off[PR_SEL_H2_W] + lane] = b0;
+        if (lane + 32 < h) grad[P.off[PR_SEL_H2_W] + lane + 32] = b1;
+        if (lane == 0) {
+            grad[P.off[PR_PLC_H2_B]] = db2;
+            grad[P.off[PR_SEL_H2_B]] = bs;
+        }
     }
 }
 
@@ -425,9 +465,9 @@ static int build_jobs(fp_policy *pol, double *grad) {
 static void launch_outer(fp_train_state *ts, int stage, cudaStream_t st) {
     const auto &b = ts->batches[stage];
     int maxk = 0;
-    for (auto &j : b) maxk = std::max(maxk, j.K * j.h);
-    dim3 grid((maxk + 127) / 128, (unsigned)b.size());
-    outer_kernel<<<grid, 128, 0, st>>>(ts->jobs_dev + ts->stage_offset[stage]);
+    for (auto &j : b) maxk = std::max(maxk, j.K);
+    dim3 grid(maxk, (unsigned)b.size());
+    outer_kernel<<<grid, kOuterWarps * 32, 0, st>>>(ts->jobs_dev + ts->stage_offset[stage]);
 }
 
 }  // namespace fp
@@ -471,7 +511,7 @@ int fp_policy_backward(fp_policy *pol, double *grad, void *stream) {
     head_bwd_kernel<<<g4, 128, 0, st>>>(P);
     path_gather_kernel<<<g4, 128, 0, st>>>(P);
     launch_outer(ts, 0, st);  // dc
-    small_bwd_kernel<<<1, 128, 0, st>>>(P, grad);
+    small_bwd_kernel<<<1, 256, 0, st>>>(P, grad);
     launch_outer(ts, 1, st);  // head weight gradients
     int stage = 2;
     for (int e = 0; e < P.n_enc; ++e)
