@@ -60,7 +60,7 @@ struct PlcLog {  // log2(MAXD)
 // ---------------------------------------------------------------------------
 // SEL warp
 // ---------------------------------------------------------------------------
-template <bool GRAD>
+template <bool GRAD, bool LEAN = false>
 __device__ __forceinline__ bool sel_chain(const DevProblem &PR, const DevPolicy &PO,
                                           const fp_rollout_args &A, uint8_t *base /* nb == sb */,
                                           const EpLayout &L, const double *s_sm, int ep,
@@ -78,7 +78,7 @@ __device__ __forceinline__ bool sel_chain(const DevProblem &PR, const DevPolicy 
     const double eps = A.epsilon, ome = 1.0 - eps;
     const uint32_t k0 = (uint32_t)A.seed, k1 = (uint32_t)(A.seed >> 32);
     const uint32_t ctr_ep = A.episode_base + (uint32_t)ep;
-    const int mode = A.mode;
+    const int mode = LEAN ? FP_MODE_SAMPLE : A.mode;  // LEAN: sampling-only build
     const int32_t *frow = mode == FP_MODE_FORCED ? A.forced + (size_t)ep * n * 2 : nullptr;
     const int *__restrict__ pp = PR.pred_ptr;
     const int *__restrict__ sp = PR.succ_ptr;
@@ -615,7 +615,7 @@ __device__ __forceinline__ void sel_chain_wide(const DevProblem &PR, const DevPo
 // ---------------------------------------------------------------------------
 // PLC warp
 // ---------------------------------------------------------------------------
-template <int MAXD, int HPL, bool GRAD, bool WIDE = false>
+template <int MAXD, int HPL, bool GRAD, bool WIDE = false, bool LEAN = false>
 __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &PO,
                                          const fp_rollout_args &A, uint8_t *nb, uint8_t *sb,
                                          const EpLayout &L, int ep, bool want_lp,
@@ -636,7 +636,7 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
     const double eps = A.epsilon, ome = 1.0 - eps, slope = PO.slope;
     const uint32_t k0 = (uint32_t)A.seed, k1 = (uint32_t)(A.seed >> 32);
     const uint32_t ctr_ep = A.episode_base + (uint32_t)ep;
-    const int mode = A.mode;
+    const int mode = LEAN ? FP_MODE_SAMPLE : A.mode;
     const int32_t *frow = mode == FP_MODE_FORCED ? A.forced + (size_t)ep * n * 2 : nullptr;
     const double *__restrict__ Atab = PO.A;
     const double *__restrict__ Gtab = PO.G;
@@ -963,7 +963,10 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
     return status;
 }
 
-template <int MAXD, int HPL, bool GRAD, int EPB, bool SM1>
+// LEAN: the sampling-only instantiation (no forced / teacher / greedy modes,
+// no per-step outputs, no traces) -- a smaller kernel for the throughput path
+// (fewer instruction-fetch stalls with SEL, PLC and simulator code resident).
+template <int MAXD, int HPL, bool GRAD, int EPB, bool SM1, bool LEAN = false>
 __global__ void __launch_bounds__(EPB * 64, 8 / EPB)
 rollout_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
     extern __shared__ __align__(16) uint8_t smem[];
@@ -986,14 +989,14 @@ rollout_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
     }
     __syncthreads();
     if (ep >= A.B) return;
-    const bool want_lp = GRAD || A.step_lp != nullptr || A.step_ent != nullptr;
-    const bool want_amax = A.step_argmax != nullptr;
+    const bool want_lp = !LEAN && (GRAD || A.step_lp != nullptr || A.step_ent != nullptr);
+    const bool want_amax = !LEAN && A.step_argmax != nullptr;
     double *simres = (double *)(base + L.simres);  // makespan, status
     int status = FP_EP_OK;
     if (!is_plc) {
         // SEL warp: the vertex order, then -- while the PLC warp is still
         // placing -- the simulation, chasing the placement frontier
-        const bool ok = sel_chain<GRAD>(PR, PO, A, base, L, s_sm, ep, want_lp, want_amax);
+        const bool ok = sel_chain<GRAD, LEAN>(PR, PO, A, base, L, s_sm, ep, want_lp, want_amax);
         if (ok && A.simulate) {
             const volatile int *order = (const volatile int *)(base + L.order);
             int *pos = (int *)(base + L.clist);     // SEL scratch, free now
@@ -1016,7 +1019,8 @@ rollout_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
             __syncwarp();
             SimOut o = sim_episode<RPL, false, SM1, true>(
                 PR, base, base, L, A.strategy, nullptr,
-                A.trace ? A.trace + (size_t)ep * A.trace_cap : nullptr, A.trace_cap, nullptr,
+                (!LEAN && A.trace) ? A.trace + (size_t)ep * A.trace_cap : nullptr, A.trace_cap,
+                nullptr,
                 SimSync{flag, flag + 1, maxsucc, iw});
             if (lane == 0) {
                 simres[0] = o.makespan;
@@ -1025,7 +1029,8 @@ rollout_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
             }
         }
     } else {
-        status = plc_chain<MAXD, HPL, GRAD>(PR, PO, A, base, base, L, ep, want_lp, want_amax);
+        status = plc_chain<MAXD, HPL, GRAD, false, LEAN>(PR, PO, A, base, base, L, ep, want_lp,
+                                                         want_amax);
         if (status != FP_EP_OK && lane == 0) flag[1] = 1;  // release a waiting simulator
         const uint8_t *dev = base + L.assign;
         for (int v = lane; v < n; v += 32)
@@ -1055,7 +1060,11 @@ int launch_rollout(const fp_problem *p, const fp_policy *pol, const fp_rollout_a
         set_error("episode state exceeds shared memory for this graph size");
         return FP_ERR_UNSUPPORTED;
     }
-    auto kern = PR.SM == 1 ? rollout_kernel<MAXD, HPL, GRAD, EPB, true>
+    const bool lean = !GRAD && a.mode == FP_MODE_SAMPLE && !a.step_vd && !a.step_lp &&
+                      !a.step_ent && !a.step_argmax && !a.step_ncand && !a.trace &&
+                      !(a.flags & FP_FLAG_TIE_RANDOM);
+    auto kern = PR.SM == 1 ? (lean ? rollout_kernel<MAXD, HPL, GRAD, EPB, true, !GRAD>
+                                   : rollout_kernel<MAXD, HPL, GRAD, EPB, true>)
                            : rollout_kernel<MAXD, HPL, GRAD, EPB, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
