@@ -84,8 +84,10 @@ __device__ __forceinline__ bool sel_chain(const DevProblem &PR, const DevPolicy 
     const int *__restrict__ sp = PR.succ_ptr;
     const int *__restrict__ si = PR.succ_idx;
 
+#pragma unroll 1
     for (int w = lane; w < W; w += 32) cand[w] = 0u;
     __syncwarp();
+#pragma unroll 1
     for (int v = lane; v < n; v += 32) {
         const int np = pp[v + 1] - pp[v];
         npl[v] = np;
@@ -155,6 +157,7 @@ __device__ __forceinline__ bool sel_chain(const DevProblem &PR, const DevPolicy 
             }
         } else {
             double mx = -INFINITY;
+#pragma unroll 1
             for (int i = lane; i < k; i += 32) mx = fmax(mx, s_sm[clist[i]]);
             mx = warp_max_redux(mx);
             double carry = 0.0;
@@ -650,6 +653,7 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
     double *rsl = (double *)(sb + L.rsum);    // [D][h] running lp sums (grad)
     double *rse = rsl + D * h;                // [D][h] running entropy sums
 
+#pragma unroll 1
     for (int v = lane; v < n; v += 32) { tstart[v] = 0.0; tend[v] = 0.0; dev[v] = 0xFF; }
     double avail = 0.0, aflops = 0.0;  // lane d < D
     double Mr[5][HPL], cr[HPL], w2r[HPL], Sd[MAXD][HPL];
@@ -1001,15 +1005,19 @@ rollout_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
             const volatile int *order = (const volatile int *)(base + L.order);
             int *pos = (int *)(base + L.clist);     // SEL scratch, free now
             int *maxsucc = (int *)(base + L.npl);
+#pragma unroll 1
             for (int i = lane; i < n; i += 32) pos[order[i]] = i;
             __syncwarp();
             int iw = -1;
+#pragma unroll 1
             for (int v = lane; v < n; v += 32) {
                 int m = -1;
+#pragma unroll 1
                 for (int j = PR.succ_ptr[v]; j < PR.succ_ptr[v + 1]; ++j) m = max(m, pos[PR.succ_idx[j]]);
                 maxsucc[v] = m;
                 if (!PR.is_entry[v]) {
                     bool all_entry = true;
+#pragma unroll 1
                     for (int j = PR.pred_ptr[v]; j < PR.pred_ptr[v + 1]; ++j)
                         all_entry &= PR.is_entry[PR.pred_idx[j]] != 0;
                     if (all_entry) iw = max(iw, pos[v]);

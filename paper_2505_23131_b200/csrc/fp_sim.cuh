@@ -147,19 +147,23 @@ __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *nb, 
     const double *__restrict__ edur = P.edur;
     const double *__restrict__ tdur = P.tdur;
 
-    // ---- init (_simcore.pyx:71-105) ----
+    // ---- init (_simcore.pyx:71-105); cold loops kept rolled (code size) ----
+#pragma unroll 1
     for (int v = lane; v < n; v += 32) {
         const bool e = ent[v];
         rdy[v] = e ? dmask : 0u;
         if constexpr (!OVL) {  // consumer devices (_simcore.pyx:84-97), all placed
             uint32_t c = 0;
+#pragma unroll 1
             for (int j = sp[v]; j < sp[v + 1]; ++j) c |= 1u << assign[si[j]];
             cons[v] = c;
         }
         int miss = 0;
+#pragma unroll 1
         for (int j = P.pred_ptr[v]; j < P.pred_ptr[v + 1]; ++j) miss += !ent[P.pred_idx[j]];
         missing[v] = miss;
     }
+#pragma unroll 1
     for (int i = lane; i < R * BW; i += 32) bits[i] = 0u;
     // SM1: every resource has at most one slot (the reference's default
     // cluster), so each resource's in-flight task lives in its owning lane's
@@ -168,6 +172,13 @@ __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *nb, 
     int fr[RPL];
     int ipv[SM1 ? RPL : 1];
     double iend[SM1 ? RPL : 1];
+    int rsrc[RPL], rdst[RPL];  // link r >= d: (src, dst) = divmod(r - d, d), once per episode
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) {
+        const int r = lane + 32 * q;
+        rsrc[q] = r < d ? r : (r - d) / d;
+        rdst[q] = r < d ? r : (r - d) - rsrc[q] * d;
+    }
 #pragma unroll
     for (int q = 0; q < RPL; ++q) {
         const int r = lane + 32 * q;
@@ -233,8 +244,8 @@ __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *nb, 
                             dur = edur[v * d + r];
                             if (jit) dur = __dmul_rn(dur, jit[v * d + r]);
                         } else {
-                            const int ta = (r - d) / d;
-                            kind = 1; tb = (r - d) - ta * d;
+                            const int ta = rsrc[q];
+                            kind = 1; tb = rdst[q];
                             dur = tdur[(v * d + ta) * d + tb];
                             if (jit) dur = __dmul_rn(dur, jit[n * d + (v * d + ta) * d + tb]);
                         }
@@ -369,7 +380,7 @@ __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *nb, 
                         atomicAdd(&cnt[rr], 1);
                     }
                 } else {
-                    dev = (r - d) % d;
+                    dev = rdst[q];
                     atomicOr(&rdy[v], 1u << dev);
                 }
                 for (int j = sp[v]; j < sp[v + 1]; ++j) {
