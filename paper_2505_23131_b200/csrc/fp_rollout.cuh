@@ -161,6 +161,7 @@ __device__ __forceinline__ bool sel_chain(const DevProblem &PR, const DevPolicy 
             for (int i = lane; i < k; i += 32) mx = fmax(mx, s_sm[clist[i]]);
             mx = warp_max_redux(mx);
             double carry = 0.0;
+#pragma unroll 1
             for (int b0 = 0; b0 < k; b0 += 32) {
                 const int i = b0 + lane;
                 const double e = i < k ? exp(s_sm[clist[i]] - mx) : 0.0;
@@ -277,6 +278,7 @@ __device__ __forceinline__ bool sel_chain(const DevProblem &PR, const DevPolicy 
             cand[v >> 5] &= ~(1u << (v & 31));
         }
         __syncwarp();
+#pragma unroll 1
         for (int j = sp[v] + lane; j < sp[v + 1]; j += 32) {
             const int w = si[j];
             if (atomicSub(&npl[w], 1) == 1) atomicOr(&cand[w >> 5], 1u << (w & 31));
@@ -714,6 +716,7 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
             double f1 = 0.0, f2 = 0.0, f3 = 0.0;
             bool any_local = false;
             const int p0 = pp[v], p1 = pp[v + 1];
+#pragma unroll 1
             for (int j = p0; j < p1; ++j) {
                 const int p = pi[j];
                 const int dp = dev[p];
@@ -988,6 +991,7 @@ rollout_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
     volatile int *flag = (volatile int *)(base + L.flag);  // [0] placed, [1] PLC abort
     if (!is_plc) {
         volatile int *order = (volatile int *)(base + L.order);
+#pragma unroll 1
         for (int t = lane; t < n; t += 32) order[t] = -3;  // hand-off sentinel
         if (lane == 0) { flag[0] = 0; flag[1] = 0; }
     }
@@ -1041,6 +1045,7 @@ rollout_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
                                                          want_amax);
         if (status != FP_EP_OK && lane == 0) flag[1] = 1;  // release a waiting simulator
         const uint8_t *dev = base + L.assign;
+#pragma unroll 1
         for (int v = lane; v < n; v += 32)
             A.assign[(size_t)ep * n + v] = dev[v] == 0xFF ? -1 : dev[v];
     }

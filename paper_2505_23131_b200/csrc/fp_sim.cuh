@@ -366,6 +366,7 @@ __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *nb, 
                     // known now that every successor is placed
                     uint32_t m = 0u;
                     if constexpr (OVL) {
+#pragma unroll 1
                         for (int j = sp[v]; j < sp[v + 1]; ++j) m |= 1u << assign[si[j]];
                     } else {
                         m = cons[v];
@@ -383,6 +384,7 @@ __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *nb, 
                     dev = rdst[q];
                     atomicOr(&rdy[v], 1u << dev);
                 }
+#pragma unroll 1
                 for (int j = sp[v]; j < sp[v + 1]; ++j) {
                     const int w = si[j];
                     if (assign[w] == dev && atomicSub(&missing[w], 1) == 1) {
