@@ -447,6 +447,7 @@ __device__ __forceinline__ bool ring_publish(volatile int *ring, volatile int *d
     return __shfl_sync(FP_FULL_MASK, ok, 0) != 0;
 }
 
+template <bool LEAN = false>
 __device__ __forceinline__ void sel_chain_wide(const DevProblem &PR, const DevPolicy &PO,
                                                const fp_rollout_args &A, uint8_t *nb,
                                                uint8_t *sb, const EpLayout &L, int ep,
@@ -460,7 +461,7 @@ __device__ __forceinline__ void sel_chain_wide(const DevProblem &PR, const DevPo
     const double eps = A.epsilon, ome = 1.0 - eps;
     const uint32_t k0 = (uint32_t)A.seed, k1 = (uint32_t)(A.seed >> 32);
     const uint32_t ctr_ep = A.episode_base + (uint32_t)ep;
-    const int mode = A.mode;
+    const int mode = LEAN ? FP_MODE_SAMPLE : A.mode;
     const int32_t *frow = mode == FP_MODE_FORCED ? A.forced + (size_t)ep * n * 2 : nullptr;
     const int *__restrict__ pp = PR.pred_ptr;
     const int *__restrict__ sp = PR.succ_ptr;
@@ -1093,7 +1094,7 @@ int launch_rollout(const fp_problem *p, const fp_policy *pol, const fp_rollout_a
 // n-sized state in the HBM workspace slice of this block, small scratch and
 // the hand-off ring in shared memory.  After the PLC chain the same warp
 // scores the assignment with the hierarchical-bitset simulator.
-template <int MAXD, int HPL, bool SM1>
+template <int MAXD, int HPL, bool SM1, bool LEAN = false>
 __global__ void __launch_bounds__(64, 8)
 rollout_wide_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
     extern __shared__ __align__(16) uint8_t smem[];
@@ -1103,8 +1104,8 @@ rollout_wide_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) 
     const int n = PR.n;
     uint8_t *sb = smem;
     uint8_t *nb = (uint8_t *)A.workspace + (size_t)blockIdx.x * L.gbytes;
-    const bool want_lp = A.step_lp != nullptr || A.step_ent != nullptr;
-    const bool want_amax = A.step_argmax != nullptr;
+    const bool want_lp = !LEAN && (A.step_lp != nullptr || A.step_ent != nullptr);
+    const bool want_amax = !LEAN && A.step_argmax != nullptr;
     for (int ep = blockIdx.x; ep < A.B; ep += gridDim.x) {
         if (!is_plc) {
             volatile int *ring = (volatile int *)(sb + L.ring);
@@ -1113,10 +1114,10 @@ rollout_wide_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) 
         }
         __syncthreads();
         if (!is_plc) {
-            sel_chain_wide(PR, PO, A, nb, sb, L, ep, want_lp, want_amax);
+            sel_chain_wide<LEAN>(PR, PO, A, nb, sb, L, ep, want_lp, want_amax);
         } else {
-            int status = plc_chain<MAXD, HPL, false, true>(PR, PO, A, nb, sb, L, ep, want_lp,
-                                                           want_amax);
+            int status = plc_chain<MAXD, HPL, false, true, LEAN>(PR, PO, A, nb, sb, L, ep,
+                                                                 want_lp, want_amax);
             const uint8_t *dev = nb + L.assign;
             for (int v = lane; v < n; v += 32)
                 A.assign[(size_t)ep * n + v] = dev[v] == 0xFF ? -1 : dev[v];
@@ -1125,7 +1126,8 @@ rollout_wide_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) 
                 __syncwarp();
                 SimOut o = sim_episode<RPL, true, SM1>(
                     PR, nb, sb, L, A.strategy, nullptr,
-                    A.trace ? A.trace + (size_t)ep * A.trace_cap : nullptr, A.trace_cap, nullptr);
+                    (!LEAN && A.trace) ? A.trace + (size_t)ep * A.trace_cap : nullptr,
+                    A.trace_cap, nullptr);
                 status = o.status;
                 mk = o.makespan;
                 if (lane == 0 && A.trace_len) A.trace_len[ep] = o.n_events;
@@ -1149,7 +1151,11 @@ int launch_rollout_wide(const fp_problem *p, const fp_policy *pol,
         set_error("episode scratch exceeds shared memory (too many devices / slots)");
         return FP_ERR_UNSUPPORTED;
     }
-    auto kern = PR.SM == 1 ? rollout_wide_kernel<MAXD, HPL, true> : rollout_wide_kernel<MAXD, HPL, false>;
+    const bool lean = a.mode == FP_MODE_SAMPLE && !a.step_vd && !a.step_lp && !a.step_ent &&
+                      !a.step_argmax && !a.step_ncand && !a.trace && !(a.flags & FP_FLAG_TIE_RANDOM);
+    auto kern = PR.SM == 1 ? (lean ? rollout_wide_kernel<MAXD, HPL, true, true>
+                                   : rollout_wide_kernel<MAXD, HPL, true>)
+                           : rollout_wide_kernel<MAXD, HPL, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FP_ERR_CUDA; }
