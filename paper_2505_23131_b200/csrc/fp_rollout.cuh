@@ -998,7 +998,7 @@ rollout_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
     }
     __syncthreads();
     if (ep >= A.B) return;
-    const bool want_lp = !LEAN && (GRAD || A.step_lp != nullptr || A.step_ent != nullptr);
+    const bool want_lp = GRAD || (!LEAN && (A.step_lp != nullptr || A.step_ent != nullptr));
     const bool want_amax = !LEAN && A.step_argmax != nullptr;
     double *simres = (double *)(base + L.simres);  // makespan, status
     int status = FP_EP_OK;
@@ -1074,10 +1074,10 @@ int launch_rollout(const fp_problem *p, const fp_policy *pol, const fp_rollout_a
         set_error("episode state exceeds shared memory for this graph size");
         return FP_ERR_UNSUPPORTED;
     }
-    const bool lean = !GRAD && a.mode == FP_MODE_SAMPLE && !a.step_vd && !a.step_lp &&
-                      !a.step_ent && !a.step_argmax && !a.step_ncand && !a.trace &&
+    const bool lean = a.mode == FP_MODE_SAMPLE && !a.step_vd && !a.step_lp && !a.step_ent &&
+                      !a.step_argmax && !a.step_ncand && !a.trace &&
                       !(a.flags & FP_FLAG_TIE_RANDOM);
-    auto kern = PR.SM == 1 ? (lean ? rollout_kernel<MAXD, HPL, GRAD, EPB, true, !GRAD>
+    auto kern = PR.SM == 1 ? (lean ? rollout_kernel<MAXD, HPL, GRAD, EPB, true, true>
                                    : rollout_kernel<MAXD, HPL, GRAD, EPB, true>)
                            : rollout_kernel<MAXD, HPL, GRAD, EPB, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
