@@ -179,3 +179,20 @@ def test_wide_workspace_contract(torch_cuda):
                               ctypes.c_int32(0), None, None, None, ctypes.c_int64(0),
                               ctypes.c_int32(0), None)
     assert rc == N.FP_ERR_INVALID and b"workspace" in N.lib().fp_last_error()
+
+
+def test_run_packed_drop_in_large_graph(torch_cuda):
+    """The Cython-ABI drop-in (fp_run_packed, _simcore.pyx:39-45) on a graph
+    beyond shared memory (the call sizes and frees its own workspace):
+    bit-identical event stream to the C oracle, and exec_time agrees."""
+    from paper_2505_23131_b200 import simulate as S
+    g = builders.sparse_dag(4000, seed=5)
+    cl = ClusterSpec.uniform(8, rate=1e9, bandwidth=1e7)
+    feats = static_features(g, cl.comm_factor)
+    a = np.random.default_rng(2).integers(0, 8, size=len(g)).astype(np.int32)
+    packed = osim.pack(g, a, cl, feats, "depth_first", 0)
+    omk, oev = osim.run_packed(*packed)
+    mk, ev = S.run_packed(*packed)
+    assert mk == omk and ev == oev
+    mk2, sched = S.exec_time(g, a, cl, "depth_first", 0, feats)
+    assert mk2 == omk and len(sched.events) == len(oev)
