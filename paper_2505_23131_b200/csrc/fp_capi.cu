@@ -45,7 +45,9 @@ struct Arena {
 // warp's shared-memory slice, one wave.  Wide path (state beyond shared
 // memory): a persistent grid, each resident warp owning one HBM workspace
 // slice of L.gbytes and looping over episodes.
-template <int RPL, int WARPS, bool WIDE, bool SM1>
+// LEAN: no trace / jitter / blocked-frontier outputs (the makespan-only path:
+// batched scoring, brute force) -- smaller code, fewer instruction fetch stalls.
+template <int RPL, int WARPS, bool WIDE, bool SM1, bool LEAN = false>
 __global__ void __launch_bounds__(WARPS * 32)
 sim_batch_kernel(DevProblem P, EpLayout L, const int32_t *__restrict__ assign, int B,
                  int strategy, const double *__restrict__ jit, long long jit_stride,
@@ -62,10 +64,10 @@ sim_batch_kernel(DevProblem P, EpLayout L, const int32_t *__restrict__ assign, i
         const int32_t *row = assign + (size_t)ep * P.n;
         for (int v = lane_id(); v < P.n; v += 32) as[v] = (uint8_t)row[v];
         __syncwarp();
-        SimOut o = sim_episode<RPL, WIDE, SM1>(P, nb, sb, L, strategy,
-                                          jit ? jit + (size_t)ep * jit_stride : nullptr,
-                                          trace ? trace + (size_t)ep * trace_cap : nullptr,
-                                          trace_cap, blocked ? blocked + (size_t)ep * P.n : nullptr);
+        SimOut o = sim_episode<RPL, WIDE, SM1>(
+            P, nb, sb, L, strategy, (!LEAN && jit) ? jit + (size_t)ep * jit_stride : nullptr,
+            (!LEAN && trace) ? trace + (size_t)ep * trace_cap : nullptr, trace_cap,
+            (!LEAN && blocked) ? blocked + (size_t)ep * P.n : nullptr);
         if (lane_id() == 0) {
             makespan[ep] = o.makespan;
             status[ep] = o.status;
@@ -109,10 +111,14 @@ static int launch_sim_t(const fp_problem *p, const int32_t *assign, int B, int s
         return FP_ERR_UNSUPPORTED;
     }
     const bool sm1 = p->dev.SM == 1;
-    const void *kern = wide ? (sm1 ? (const void *)sim_batch_kernel<RPL, WARPS, true, true>
-                                   : (const void *)sim_batch_kernel<RPL, WARPS, true, false>)
-                            : (sm1 ? (const void *)sim_batch_kernel<RPL, WARPS, false, true>
-                                   : (const void *)sim_batch_kernel<RPL, WARPS, false, false>);
+    const bool lean = sm1 && !jit && !trace && !blocked;
+    const void *kern =
+        wide ? (sm1 ? (lean ? (const void *)sim_batch_kernel<RPL, WARPS, true, true, true>
+                            : (const void *)sim_batch_kernel<RPL, WARPS, true, true>)
+                    : (const void *)sim_batch_kernel<RPL, WARPS, true, false>)
+             : (sm1 ? (lean ? (const void *)sim_batch_kernel<RPL, WARPS, false, true, true>
+                            : (const void *)sim_batch_kernel<RPL, WARPS, false, true>)
+                    : (const void *)sim_batch_kernel<RPL, WARPS, false, false>);
     FP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t need_blocks = (B + WARPS - 1) / WARPS;
     const int grid = wide ? persistent_blocks(kern, WARPS * 32, smem, need_blocks)
