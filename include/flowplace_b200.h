@@ -128,6 +128,16 @@ int fp_run_packed(int32_t n, int32_t d, const int32_t *pred_indptr, const int32_
                   int64_t seed, double *makespan, fp_event *events, int64_t events_cap,
                   int64_t *n_events, uint8_t *blocked);
 
+/* Static per-vertex features (flowplace/features.py:51-96) on the host in
+ * native code, bit-identical to the reference's sweep: matrix [n][5] =
+ * (flops, sum of incoming comm costs, comm cost x out-degree, t-level,
+ * b-level), and the first-maximum argmax neighbours b_next / t_next (-1 at a
+ * path's end).  Host pointers.  FP_ERR_INVALID if the graph has a cycle. */
+int fp_static_features(int32_t n, const int32_t *pred_indptr, const int32_t *pred_indices,
+                       const int32_t *succ_indptr, const int32_t *succ_indices,
+                       const double *flops, const double *obytes, double comm_factor,
+                       double *matrix, int32_t *b_next, int32_t *t_next);
+
 /* Host libm jitter tables (the exact reference factors), layout as above. */
 int fp_jitter_tables(int32_t n, int32_t d, double sigma, int64_t seed, double *out);
 

@@ -82,6 +82,33 @@ def test_feature_forests_reproduce_path_lists():
             assert f.path_lengths(which).tolist() == [len(p) for p in paths]
 
 
+def test_native_static_features_bit_exact():
+    """fp_static_features (native host sweep used from NATIVE_MIN_N ops on)
+    reproduces the Python mirror of features.py:51-96 bit for bit, next
+    forests included, and refuses a cycle."""
+    from paper_2505_23131_b200 import _native as N
+    graphs = (builders.build_llama_block(), builders.build_ffnn(8, 4, 16, 4, 2),
+              builders.sparse_dag(5000, seed=4), builders.relabel(builders.sparse_dag(3000, seed=5), 9))
+    for g in graphs:
+        for cf in (4.0, 3.7):
+            a = static_features(g, cf, native=False)
+            b = static_features(g, cf, native=True)
+            assert a.matrix.tobytes() == b.matrix.tobytes()
+            assert a.b_next.tolist() == b.b_next.tolist()
+            assert a.t_next.tolist() == b.t_next.tolist()
+    # 0 -> 1 -> 2 -> 1 (cycle)
+    ip = np.array([0, 0, 2, 3], np.int32)
+    pi = np.array([0, 2, 1], np.int32)
+    si_p = np.array([0, 1, 2, 3], np.int32)
+    si = np.array([1, 2, 1], np.int32)
+    z = np.ones(3)
+    out = np.zeros((3, 5)); nx = np.zeros(3, np.int32); tx = np.zeros(3, np.int32)
+    with pytest.raises(N.NativeError, match="not a DAG"):
+        N.check(N.lib().fp_static_features(ctypes.c_int32(3), N.ptr(ip), N.ptr(pi), N.ptr(si_p),
+                                           N.ptr(si), N.ptr(z), N.ptr(z), ctypes.c_double(4.0),
+                                           N.ptr(out), N.ptr(nx), N.ptr(tx)))
+
+
 def test_relabel_keeps_the_dag():
     g = builders.sparse_dag(500, seed=1)
     r = builders.relabel(g, seed=3)
