@@ -144,6 +144,33 @@ class Clocks:
 
 
 # --------------------------------------------------------------------------- GPU
+def _episode_rates(g, assign: np.ndarray, episodes_per_s: float) -> dict:
+    """Decisions/s and simulated WC events/s from the last timed
+    batch: an episode makes n SEL+PLC decisions and its simulation runs one
+    exec per non-entry vertex plus one transfer per (vertex, other consumer
+    device) -- 2 events (beg, end) per task."""
+    c = g.csr()
+    n = len(g)
+    src = np.repeat(np.arange(n), np.diff(c["succ_indptr"]))
+    dst = c["succ_indices"].astype(np.int64)
+    B = assign.shape[0]
+    a = assign.astype(np.int64)
+    cons = np.zeros((B, n), dtype=np.int64)
+    for e in range(len(src)):  # device bitmask of each vertex's consumers
+        cons[:, src[e]] |= np.left_shift(1, a[:, dst[e]])
+    cons &= ~np.left_shift(1, a)
+    nonentry = c["is_entry"] == 0
+    bits = np.zeros_like(cons)
+    x = cons.copy()
+    while x.any():
+        bits += x & 1
+        x >>= 1
+    tasks = int(nonentry.sum()) + bits[:, nonentry].sum(axis=1)
+    return {"decisions_per_s": episodes_per_s * n,
+            "sim_tasks_per_episode": float(tasks.mean()),
+            "sim_events_per_s": episodes_per_s * 2 * float(tasks.mean())}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -343,6 +370,7 @@ def run_ours(args):
                                   "GNN kernels' rooflines in profiles/r1_ncu_*"),
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
         }
+        line["rates"] = _episode_rates(g, out.assign.cpu().numpy(), value)
         if clk:
             line["clocks"] = clk.summary(local)
         if world == 1 and not args.no_cpu:
