@@ -178,9 +178,17 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # FP_BENCH_DIST_BACKEND=gloo (+ ranks sharing a GPU) exercises the
+    # multi-rank code path on a one-GPU box; the driver's runs use NCCL
+    backend = os.environ.get("FP_BENCH_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_2505_23131_b200.params import init_policy_params
     from paper_2505_23131_b200.policy import PolicyConfig, PolicyContext
 
