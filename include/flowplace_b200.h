@@ -241,7 +241,8 @@ int fp_policy_table(const fp_policy *pol, int32_t which, const double **ptr, int
 /* Device workspace fp_rollout_batch needs for B episodes (0 on the compact
  * shared-memory path; graphs beyond it run the wide path, whose per-episode
  * n-sized state lives in this caller-owned HBM scratch).  grad = 1 for a
- * rollout that writes REINFORCE rows (compact path only). */
+ * rollout that writes REINFORCE rows (compact path only): its per-decision
+ * records (B*n*(56*d + 8) + 4*B bytes) also live in the workspace. */
 int fp_rollout_workspace_size(const fp_problem *p, const fp_policy *pol, int32_t B,
                               int32_t flags, int32_t grad, int64_t *bytes);
 /* Batched SEL/PLC episodes (+ fused WC simulation) — one warp per episode. */

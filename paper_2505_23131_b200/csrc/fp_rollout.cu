@@ -20,8 +20,8 @@ FP_ROLLOUT_CONFIGS(FP_DECL)
 
 static bool rollout_compact_fits(const fp_problem *p, const fp_policy *pol, bool grad) {
     const DevProblem &PR = p->dev;
-    const EpLayout L = make_layout(PR.n, PR.W, PR.R, PR.SM, true,
-                                   grad ? 2 * PR.d * pol->dev.h : 0);
+    (void)pol; (void)grad;  // REINFORCE records live in the workspace, not shared memory
+    const EpLayout L = make_layout(PR.n, PR.W, PR.R, PR.SM, true, 0);
     // the compact SEL chain keeps the candidate bitset in one word per lane
     return PR.n <= 1024 && fp_align(8 * PR.n, 16) + (int64_t)L.bytes <= 227 * 1024;
 }
@@ -52,7 +52,10 @@ static int dispatch_grad(const fp_problem *p, const fp_policy *pol, const fp_rol
         }
         return launch_rollout_wide<MAXD, HPL>(p, pol, a, ws_needed, st);
     }
-    if (ws_needed) { *ws_needed = 0; return FP_OK; }
+    if (ws_needed) {
+        *ws_needed = grad ? grad_rec_bytes(a.B, p->dev.n, p->dev.d) : 0;
+        return FP_OK;
+    }
     return grad ? launch_rollout<MAXD, HPL, true>(p, pol, a, st)
                 : launch_rollout<MAXD, HPL, false>(p, pol, a, st);
 }

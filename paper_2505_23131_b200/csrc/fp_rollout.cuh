@@ -51,6 +51,15 @@ __host__ __device__ inline int64_t grad_ep_stride(int n, int h, int d) {
     return ((2LL * n + 12LL * h + 2 + 2LL * d * h) + 3) / 4 * 4;
 }
 
+// REINFORCE decision records (compact GRAD rollouts): per (episode, step) the
+// normalised device features xn[5d] and the head-2 adjoints gl[d], ge[d]
+// (7d doubles), then per (episode, step) the (vertex, device) pair, then a
+// per-episode "PLC chain completed" flag.  The PLC warp only records; the
+// gradient arithmetic runs afterwards in plc_grad_kernel, off the chain.
+__host__ __device__ inline int64_t grad_rec_bytes(int B, int n, int d) {
+    return (int64_t)B * n * 7 * d * 8 + (int64_t)B * n * 8 + (int64_t)B * 4;
+}
+
 template <int MAXD>
 struct PlcLog {  // log2(MAXD)
     static constexpr int v = MAXD <= 1 ? 0 : MAXD <= 2 ? 1 : MAXD <= 4 ? 2 : MAXD <= 8 ? 3 :
@@ -653,15 +662,13 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
     const double *__restrict__ tdur = PR.tdur;
     const double *__restrict__ edur = PR.edur;
     const double b2p = PO.W(PR_PLC_H2_B)[0];
-    double *rsl = (double *)(sb + L.rsum);    // [D][h] running lp sums (grad)
-    double *rse = rsl + D * h;                // [D][h] running entropy sums
+    double *rec_x = GRAD ? (double *)A.workspace : nullptr;  // decision records (GRAD)
+    int2 *rec_vd = GRAD ? (int2 *)(rec_x + (size_t)A.B * n * 7 * D) : nullptr;
 
 #pragma unroll 1
     for (int v = lane; v < n; v += 32) { tstart[v] = 0.0; tend[v] = 0.0; dev[v] = 0xFF; }
     double avail = 0.0, aflops = 0.0;  // lane d < D
     double Mr[5][HPL], cr[HPL], w2r[HPL], Sd[MAXD][HPL];
-    double dMl[GRAD ? 5 : 1][HPL], dMe[GRAD ? 5 : 1][HPL], dwl[HPL], dwe[HPL];
-    double db2l = 0.0, db2e = 0.0;
     {
         const double *w2p = PO.W(PR_PLC_H2_W);
 #pragma unroll
@@ -672,16 +679,9 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
             for (int c = 0; c < 5; ++c) Mr[c][t] = ok ? PO.M[c * h + j] : 0.0;
             cr[t] = ok ? PO.c[j] : 0.0;
             w2r[t] = ok ? w2p[j] : 0.0;
-            dwl[t] = dwe[t] = 0.0;
 #pragma unroll
             for (int d = 0; d < MAXD; ++d) Sd[d][t] = 0.0;
-            if constexpr (GRAD) {
-#pragma unroll
-                for (int c = 0; c < 5; ++c) dMl[c][t] = dMe[c][t] = 0.0;
-            }
         }
-        if constexpr (GRAD)
-            for (int i = lane; i < 2 * D * h; i += 32) rsl[i] = 0.0;
     }
     __syncwarp();
     int status = FP_EP_OK;
@@ -883,45 +883,10 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
                 const double gl = lane < D ? ome * pj / __dadd_rn(mj, 1e-30) *
                                                  ((lane == jdx ? 1.0 : 0.0) - pd) : 0.0;
                 const double ge = lane < D ? pd * (q - qpd) : 0.0;
-                double arl[HPL], are[HPL];
-#pragma unroll
-                for (int t = 0; t < HPL; ++t) arl[t] = are[t] = 0.0;
-#pragma unroll
-                for (int d = 0; d < MAXD; ++d) {
-                    if (d >= D) continue;
-                    const double gld = __shfl_sync(FP_FULL_MASK, gl, d);
-                    const double ged = __shfl_sync(FP_FULL_MASK, ge, d);
-                    if (lane == 0) { db2l += gld; db2e += ged; }
-                    const double x0 = xn[d * 5], x1 = xn[d * 5 + 1], x2 = xn[d * 5 + 2],
-                                 x3 = xn[d * 5 + 3], x4 = xn[d * 5 + 4];
-#pragma unroll
-                    for (int t = 0; t < HPL; ++t) {
-                        const double dl = gld * w2r[t] * lkd(pre[d][t], slope);
-                        const double de = ged * w2r[t] * lkd(pre[d][t], slope);
-                        const double lv = lk(pre[d][t], slope);
-                        dwl[t] = fma(gld, lv, dwl[t]);
-                        dwe[t] = fma(ged, lv, dwe[t]);
-                        arl[t] += dl;
-                        are[t] += de;
-                        const int j = lane + 32 * t;
-                        if (j < h) { rsl[d * h + j] += dl; rse[d * h + j] += de; }
-                        dMl[0][t] = fma(x0, dl, dMl[0][t]); dMe[0][t] = fma(x0, de, dMe[0][t]);
-                        dMl[1][t] = fma(x1, dl, dMl[1][t]); dMe[1][t] = fma(x1, de, dMe[1][t]);
-                        dMl[2][t] = fma(x2, dl, dMl[2][t]); dMe[2][t] = fma(x2, de, dMe[2][t]);
-                        dMl[3][t] = fma(x3, dl, dMl[3][t]); dMe[3][t] = fma(x3, de, dMe[3][t]);
-                        dMl[4][t] = fma(x4, dl, dMl[4][t]); dMe[4][t] = fma(x4, de, dMe[4][t]);
-                    }
-                }
-                double *row = A.grad_rows + ((size_t)ep * n + v) * 4 * h;
-#pragma unroll
-                for (int t = 0; t < HPL; ++t) {
-                    const int j = lane + 32 * t;
-                    if (j >= h) continue;
-                    row[j] = arl[t];
-                    row[h + j] = are[t];
-                    row[2 * h + j] = rsl[jdx * h + j];
-                    row[3 * h + j] = rse[jdx * h + j];
-                }
+                double *rec = rec_x + ((size_t)ep * n + step) * (7 * D);
+                for (int i = lane; i < 5 * D; i += 32) rec[i] = xn[i];
+                if (lane < D) { rec[5 * D + lane] = gl; rec[6 * D + lane] = ge; }
+                if (lane == 0) rec_vd[(size_t)ep * n + step] = make_int2(v, jdx);
             }
         }
         FP_PHASE_END(pp_, 16);
@@ -951,23 +916,8 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
         FP_PHASE_END(pp_, 17);
     }
     FP_PHASE_FLUSH(0);
-    if constexpr (GRAD) if (status == FP_EP_OK) {
-        double *q = A.grad_ep + (size_t)ep * grad_ep_stride(n, h, D) + 2 * n;
-#pragma unroll
-        for (int t = 0; t < HPL; ++t) {
-            const int j = lane + 32 * t;
-            if (j >= h) continue;
-#pragma unroll
-            for (int c = 0; c < 5; ++c) { q[c * h + j] = dMl[c][t]; q[5 * h + c * h + j] = dMe[c][t]; }
-            q[10 * h + j] = dwl[t];
-            q[11 * h + j] = dwe[t];
-            for (int d = 0; d < D; ++d) {
-                q[12 * h + 2 + d * h + j] = rsl[d * h + j];
-                q[12 * h + 2 + D * h + d * h + j] = rse[d * h + j];
-            }
-        }
-        if (lane == 0) { q[12 * h] = db2l; q[12 * h + 1] = db2e; }
-    }
+    if constexpr (GRAD)
+        if (lane == 0) ((int *)(rec_vd + (size_t)A.B * n))[ep] = status == FP_EP_OK;
     return status;
 }
 
@@ -1062,14 +1012,177 @@ rollout_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
     }
 }
 
+// Deferred REINFORCE pass of the PLC head: the PLC warp records each
+// decision (xn, gl, ge, v, jdx) and this kernel -- off the latency-bound
+// placement chain, one warp per episode -- walks the records in placement
+// order with the PLC's arithmetic: it rebuilds the per-device sums S_d and the
+// pre-activations from (A, G, M, c) and xn, and produces the per-vertex rows
+// (d logit / d S-row terms, running per-device sums at placement) and the
+// per-episode sums (dM, dw2, db2, total per-device sums) that fp_pg_reduce and
+// the backward consume.  The next step's record is staged in shared memory
+// while the current one is reduced.
+constexpr int kGradWarps = 4;
+
+template <int MAXD, int HPL>
+__global__ void __launch_bounds__(kGradWarps * 32)
+plc_grad_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A) {
+    __shared__ double stage[kGradWarps][2][7 * MAXD];
+    const int lane = lane_id();
+    const int wi = threadIdx.x >> 5;
+    const int ep = blockIdx.x * kGradWarps + wi;
+    if (ep >= A.B) return;
+    const int n = PR.n, D = PR.d, h = PO.h;
+    const int RD = 7 * D;
+    const double slope = PO.slope;
+    const double *recd = (const double *)A.workspace + (size_t)ep * n * RD;
+    const int2 *recv = (const int2 *)((const double *)A.workspace + (size_t)A.B * n * RD) +
+                       (size_t)ep * n;
+    const int ok = ((const int *)((const int2 *)((const double *)A.workspace +
+                                                 (size_t)A.B * n * RD) + (size_t)A.B * n))[ep];
+    double *q = A.grad_ep + (size_t)ep * grad_ep_stride(n, h, D) + 2 * n;
+    double *rows = A.grad_rows + (size_t)ep * n * 4 * h;
+    if (!ok) {  // failed chain: zero rows / sums (finite under a zero advantage)
+        for (int i = lane; i < n * 4 * h; i += 32) rows[i] = 0.0;
+        for (int i = lane; i < 12 * h + 2 + 2 * D * h; i += 32) q[i] = 0.0;
+        return;
+    }
+    const double *__restrict__ Atab = PO.A;
+    const double *__restrict__ Gtab = PO.G;
+    double Mr[5][HPL], cr[HPL], w2r[HPL], Sd[MAXD][HPL], rsl[MAXD][HPL], rse[MAXD][HPL];
+    double dMl[5][HPL], dMe[5][HPL], dwl[HPL], dwe[HPL];
+    double db2l = 0.0, db2e = 0.0;
+    {
+        const double *w2p = PO.W(PR_PLC_H2_W);
+#pragma unroll
+        for (int t = 0; t < HPL; ++t) {
+            const int j = lane + 32 * t;
+            const bool in = j < h;
+#pragma unroll
+            for (int c = 0; c < 5; ++c) {
+                Mr[c][t] = in ? PO.M[c * h + j] : 0.0;
+                dMl[c][t] = dMe[c][t] = 0.0;
+            }
+            cr[t] = in ? PO.c[j] : 0.0;
+            w2r[t] = in ? w2p[j] : 0.0;
+            dwl[t] = dwe[t] = 0.0;
+#pragma unroll
+            for (int d = 0; d < MAXD; ++d) Sd[d][t] = rsl[d][t] = rse[d][t] = 0.0;
+        }
+    }
+    double *st0 = stage[wi][0];
+    for (int i = lane; i < RD; i += 32) st0[i] = recd[i];
+    int2 vj = recv[0];
+    __syncwarp();
+#pragma unroll 1
+    for (int step = 0; step < n; ++step) {
+        const double *x = stage[wi][step & 1];
+        const int v = vj.x, jdx = vj.y;
+        // stage the next record while this one is reduced
+        double nx[(7 * MAXD + 31) / 32];
+        int2 nvj = vj;
+        if (step + 1 < n) {
+            const double *nr = recd + (size_t)(step + 1) * RD;
+#pragma unroll
+            for (int k = 0; k < (7 * MAXD + 31) / 32; ++k) {
+                const int i = lane + 32 * k;
+                nx[k] = i < RD ? nr[i] : 0.0;
+            }
+            nvj = recv[step + 1];
+        }
+        double Av[HPL], Gv[HPL], arl[HPL], are[HPL];
+#pragma unroll
+        for (int t = 0; t < HPL; ++t) {
+            const int j = lane + 32 * t;
+            Av[t] = j < h ? Atab[(size_t)v * h + j] : 0.0;
+            Gv[t] = j < h ? Gtab[(size_t)v * h + j] : 0.0;
+            arl[t] = are[t] = 0.0;
+        }
+#pragma unroll
+        for (int d = 0; d < MAXD; ++d) {
+            if (d >= D) continue;
+            const double x0 = x[d * 5], x1 = x[d * 5 + 1], x2 = x[d * 5 + 2], x3 = x[d * 5 + 3],
+                         x4 = x[d * 5 + 4];
+            const double gld = x[5 * D + d], ged = x[6 * D + d];
+            if (lane == 0) { db2l += gld; db2e += ged; }
+#pragma unroll
+            for (int t = 0; t < HPL; ++t) {
+                double a = Av[t] + Sd[d][t] + cr[t];
+                a = fma(x0, Mr[0][t], a);
+                a = fma(x1, Mr[1][t], a);
+                a = fma(x2, Mr[2][t], a);
+                a = fma(x3, Mr[3][t], a);
+                a = fma(x4, Mr[4][t], a);
+                const double dl = gld * w2r[t] * lkd(a, slope);
+                const double de = ged * w2r[t] * lkd(a, slope);
+                const double lv = lk(a, slope);
+                dwl[t] = fma(gld, lv, dwl[t]);
+                dwe[t] = fma(ged, lv, dwe[t]);
+                arl[t] += dl;
+                are[t] += de;
+                rsl[d][t] += dl;
+                rse[d][t] += de;
+                dMl[0][t] = fma(x0, dl, dMl[0][t]); dMe[0][t] = fma(x0, de, dMe[0][t]);
+                dMl[1][t] = fma(x1, dl, dMl[1][t]); dMe[1][t] = fma(x1, de, dMe[1][t]);
+                dMl[2][t] = fma(x2, dl, dMl[2][t]); dMe[2][t] = fma(x2, de, dMe[2][t]);
+                dMl[3][t] = fma(x3, dl, dMl[3][t]); dMe[3][t] = fma(x3, de, dMe[3][t]);
+                dMl[4][t] = fma(x4, dl, dMl[4][t]); dMe[4][t] = fma(x4, de, dMe[4][t]);
+            }
+        }
+        double *row = rows + (size_t)v * 4 * h;
+#pragma unroll
+        for (int t = 0; t < HPL; ++t) {
+            const int j = lane + 32 * t;
+            double sl = 0.0, se = 0.0;
+#pragma unroll
+            for (int d = 0; d < MAXD; ++d)
+                if (d == jdx) { sl = rsl[d][t]; se = rse[d][t]; Sd[d][t] += Gv[t]; }
+            if (j < h) {
+                row[j] = arl[t];
+                row[h + j] = are[t];
+                row[2 * h + j] = sl;
+                row[3 * h + j] = se;
+            }
+        }
+        if (step + 1 < n) {
+            double *ns = stage[wi][(step + 1) & 1];
+#pragma unroll
+            for (int k = 0; k < (7 * MAXD + 31) / 32; ++k) {
+                const int i = lane + 32 * k;
+                if (i < RD) ns[i] = nx[k];
+            }
+            vj = nvj;
+        }
+        __syncwarp();
+    }
+#pragma unroll
+    for (int t = 0; t < HPL; ++t) {
+        const int j = lane + 32 * t;
+        if (j >= h) continue;
+#pragma unroll
+        for (int c = 0; c < 5; ++c) { q[c * h + j] = dMl[c][t]; q[5 * h + c * h + j] = dMe[c][t]; }
+        q[10 * h + j] = dwl[t];
+        q[11 * h + j] = dwe[t];
+#pragma unroll
+        for (int d = 0; d < MAXD; ++d) {
+            if (d >= D) continue;
+            q[12 * h + 2 + d * h + j] = rsl[d][t];
+            q[12 * h + 2 + D * h + d * h + j] = rse[d][t];
+        }
+    }
+    if (lane == 0) { q[12 * h] = db2l; q[12 * h + 1] = db2e; }
+}
+
 template <int MAXD, int HPL, bool GRAD>
 int launch_rollout(const fp_problem *p, const fp_policy *pol, const fp_rollout_args &a,
                           cudaStream_t st) {
     constexpr int EPB = 1;
     const DevProblem &PR = p->dev;
-    const EpLayout L = make_layout(PR.n, PR.W, PR.R, PR.SM, true,
-                                   GRAD ? 2 * PR.d * pol->dev.h : 0);
+    const EpLayout L = make_layout(PR.n, PR.W, PR.R, PR.SM, true, 0);
     const int64_t smem = fp_align(8 * PR.n, 16) + (int64_t)L.bytes * EPB;
+    if (GRAD && (!a.workspace || a.workspace_bytes < grad_rec_bytes(a.B, PR.n, PR.d))) {
+        set_error("REINFORCE rollout needs fp_rollout_workspace_size bytes of workspace");
+        return FP_ERR_INVALID;
+    }
     if (smem > 227 * 1024) {
         set_error("episode state exceeds shared memory for this graph size");
         return FP_ERR_UNSUPPORTED;
@@ -1085,6 +1198,9 @@ int launch_rollout(const fp_problem *p, const fp_policy *pol, const fp_rollout_a
     if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FP_ERR_CUDA; }
     const int grid = (a.B + EPB - 1) / EPB;
     kern<<<grid, EPB * 64, smem, st>>>(PR, pol->dev, a, L);
+    if constexpr (GRAD)
+        plc_grad_kernel<MAXD, HPL><<<(a.B + kGradWarps - 1) / kGradWarps, kGradWarps * 32, 0,
+                                     st>>>(PR, pol->dev, a);
     e = cudaGetLastError();
     if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FP_ERR_CUDA; }
     return FP_OK;

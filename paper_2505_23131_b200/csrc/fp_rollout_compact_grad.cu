@@ -8,3 +8,19 @@ namespace fp {
                                                     const fp_rollout_args &, cudaStream_t);
 FP_INST(4, 1) FP_INST(8, 1) FP_INST(16, 1) FP_INST(32, 1) FP_INST(8, 2) FP_INST(16, 2) FP_INST(32, 2)
 }  // namespace fp
+
+using namespace fp;
+extern "C" {
+#ifdef FP_PHASE_PROFILE
+int fp_phase_read_grad(unsigned long long *cycles, unsigned long long *counts, int reset) {
+    cudaMemcpyFromSymbol(cycles, g_phase_cycles, sizeof(unsigned long long) * 64);
+    cudaMemcpyFromSymbol(counts, g_phase_count, sizeof(unsigned long long) * 64);
+    if (reset) {
+        unsigned long long z[64] = {0};
+        cudaMemcpyToSymbol(g_phase_cycles, z, sizeof(z));
+        cudaMemcpyToSymbol(g_phase_count, z, sizeof(z));
+    }
+    return FP_OK;
+}
+#endif
+}

@@ -44,6 +44,7 @@ for i in range(3):
 torch.cuda.synchronize()
 lib.fp_phase_read(cyc, cnt, 1)
 lib.fp_phase_read_wide(cyc, cnt, 1)
+lib.fp_phase_read_grad(cyc, cnt, 1)
 ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
 ev[0].record()
 ctx.rollout_batch(flat, a.batch, EPSILON, 999, out=out, prepare=False)
@@ -53,10 +54,11 @@ ms = ev[0].elapsed_time(ev[1])
 lib.fp_phase_read(cyc, cnt, 1)
 cyc2 = (ctypes.c_ulonglong * 64)()
 cnt2 = (ctypes.c_ulonglong * 64)()
-lib.fp_phase_read_wide(cyc2, cnt2, 1)
-for i in range(64):  # wide-kernel counters live in their own translation unit
-    cyc[i] += cyc2[i]
-    cnt[i] += cnt2[i]
+for rd in (lib.fp_phase_read_wide, lib.fp_phase_read_grad):
+    rd(cyc2, cnt2, 1)
+    for i in range(64):  # wide / grad kernels' counters live in their own TUs
+        cyc[i] += cyc2[i]
+        cnt[i] += cnt2[i]
 print(f"{a.workload}: rollout+sim launch {ms:.3f} ms (instrumented)")
 tot = {"sel": 0, "plc": 0, "sim": 0}
 for i in sorted(NAMES):
