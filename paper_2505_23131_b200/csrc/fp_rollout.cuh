@@ -1019,8 +1019,10 @@ rollout_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
 // pre-activations from (A, G, M, c) and xn, and produces the per-vertex rows
 // (d logit / d S-row terms, running per-device sums at placement) and the
 // per-episode sums (dM, dw2, db2, total per-device sums) that fp_pg_reduce and
-// the backward consume.  The next step's record is staged in shared memory
-// while the current one is reduced.
+// the backward consume.  The next step's record, vertex rows and (vertex,
+// device) pair are fetched while the current step is reduced (measured: a
+// block of 4 warps per episode splitting the devices, with one barrier per
+// step, was slower -- 500 vs 302 us at Llama-layer x 1024).
 constexpr int kGradWarps = 4;
 
 template <int MAXD, int HPL>
@@ -1072,14 +1074,23 @@ plc_grad_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A) {
     double *st0 = stage[wi][0];
     for (int i = lane; i < RD; i += 32) st0[i] = recd[i];
     int2 vj = recv[0];
+    int2 vj1 = n > 1 ? recv[1] : vj;
+    double Av[HPL], Gv[HPL];
+#pragma unroll
+    for (int t = 0; t < HPL; ++t) {
+        const int j = lane + 32 * t;
+        Av[t] = j < h ? Atab[(size_t)vj.x * h + j] : 0.0;
+        Gv[t] = j < h ? Gtab[(size_t)vj.x * h + j] : 0.0;
+    }
     __syncwarp();
 #pragma unroll 1
     for (int step = 0; step < n; ++step) {
         const double *x = stage[wi][step & 1];
         const int v = vj.x, jdx = vj.y;
-        // stage the next record while this one is reduced
-        double nx[(7 * MAXD + 31) / 32];
-        int2 nvj = vj;
+        // fetch the next record, vertex rows and (vertex, device) pair while
+        // this step is reduced
+        double nx[(7 * MAXD + 31) / 32], nA[HPL], nG[HPL];
+        int2 vj2 = vj1;
         if (step + 1 < n) {
             const double *nr = recd + (size_t)(step + 1) * RD;
 #pragma unroll
@@ -1087,16 +1098,17 @@ plc_grad_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A) {
                 const int i = lane + 32 * k;
                 nx[k] = i < RD ? nr[i] : 0.0;
             }
-            nvj = recv[step + 1];
-        }
-        double Av[HPL], Gv[HPL], arl[HPL], are[HPL];
 #pragma unroll
-        for (int t = 0; t < HPL; ++t) {
-            const int j = lane + 32 * t;
-            Av[t] = j < h ? Atab[(size_t)v * h + j] : 0.0;
-            Gv[t] = j < h ? Gtab[(size_t)v * h + j] : 0.0;
-            arl[t] = are[t] = 0.0;
+            for (int t = 0; t < HPL; ++t) {
+                const int j = lane + 32 * t;
+                nA[t] = j < h ? Atab[(size_t)vj1.x * h + j] : 0.0;
+                nG[t] = j < h ? Gtab[(size_t)vj1.x * h + j] : 0.0;
+            }
+            if (step + 2 < n) vj2 = recv[step + 2];
         }
+        double arl[HPL], are[HPL];
+#pragma unroll
+        for (int t = 0; t < HPL; ++t) arl[t] = are[t] = 0.0;
 #pragma unroll
         for (int d = 0; d < MAXD; ++d) {
             if (d >= D) continue;
@@ -1150,7 +1162,10 @@ plc_grad_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A) {
                 const int i = lane + 32 * k;
                 if (i < RD) ns[i] = nx[k];
             }
-            vj = nvj;
+#pragma unroll
+            for (int t = 0; t < HPL; ++t) { Av[t] = nA[t]; Gv[t] = nG[t]; }
+            vj = vj1;
+            vj1 = vj2;
         }
         __syncwarp();
     }
