@@ -244,7 +244,36 @@ __device__ __forceinline__ bool sel_chain(const DevProblem &PR, const DevPolicy 
         // store replacing the -3 sentinel is the whole hand-off)
         if (lane == 0) order[step] = v;
         FP_PHASE_END(ps, 2);
-        if (want_lp) {
+        if (want_lp && fast) {
+            // candidate i on lane i: p, mix, log(mix) once per lane; the
+            // chosen candidate's terms by shuffle (the sums below are the
+            // slow path's, same reduction tree)
+            const double ek = eps / (double)k;
+            double p = 0.0, mix = 0.0, lm = 0.0, q = 0.0;
+            if (lane < k) {
+                p = e0 / tot;
+                mix = __dadd_rn(__dmul_rn(p, ome), ek);
+                lm = log(__dadd_rn(mix, 1e-30));
+                if constexpr (GRAD) q = -ome * (lm + mix / __dadd_rn(mix, 1e-30));
+            }
+            const double ent = -warp_sum(lane < k ? mix * lm : 0.0);
+            const double lp = __shfl_sync(FP_FULL_MASK, lm, idx);
+            if constexpr (GRAD) {
+                const double pidx = __shfl_sync(FP_FULL_MASK, p, idx);
+                const double midx = __shfl_sync(FP_FULL_MASK, mix, idx);
+                const double qp = warp_sum(lane < k ? q * p : 0.0);
+                const double c1 = ome * pidx / __dadd_rn(midx, 1e-30);
+                if (lane < k) {
+                    dsl[myv] += c1 * ((lane == idx ? 1.0 : 0.0) - p);
+                    dse[myv] += p * (q - qp);
+                }
+            }
+            if (lane == 0) {
+                const size_t o = (size_t)ep * n + step;
+                if (A.step_lp) A.step_lp[2 * o] = lp;
+                if (A.step_ent) A.step_ent[2 * o] = ent;
+            }
+        } else if (want_lp) {
             const double ek = eps / (double)k;
             double entp = 0.0, lp = 0.0, pidx = 0.0, midx = 0.0, qp = 0.0;
             for (int i = lane; i < k; i += 32) {
