@@ -950,6 +950,19 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
     return status;
 }
 
+// Which warp of an episode's (SEL, PLC) pair runs the PLC chain, by hardware
+// warp slot (%warpid; scheduler = slot % 4, see rollout_kernel).  All threads
+// of the block call it (one barrier); slots: 2 x (pairs in the block).
+__device__ __forceinline__ bool plc_role(unsigned *slots, int warp) {
+    unsigned ws;
+    asm volatile("mov.u32 %0, %%warpid;" : "=r"(ws));
+    if (lane_id() == 0) slots[warp] = ws;
+    __syncthreads();
+    const unsigned s0 = slots[warp & ~1], s1 = slots[warp | 1];
+    const bool p0 = (s0 & 1u) == ((s0 >> 2) & 1u), p1 = (s1 & 1u) == ((s1 >> 2) & 1u);
+    return p0 != p1 ? ((warp & 1) ? p1 : p0) : (warp & 1) != 0;
+}
+
 // LEAN: the sampling-only instantiation (no forced / teacher / greedy modes,
 // no per-step outputs, no traces) -- a smaller kernel for the throughput path
 // (fewer instruction-fetch stalls with SEL, PLC and simulator code resident).
@@ -961,7 +974,13 @@ rollout_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
     const int lane = lane_id();
     const int warp = threadIdx.x >> 5;
     const int slot = warp >> 1;  // episode slot in the block
-    const bool is_plc = warp & 1;
+    // Role by hardware warp slot (%warpid; scheduler = slot % 4): blocks of
+    // two warps take slot pairs (2b, 2b + 1), so "odd warp = PLC" would put
+    // every latency-critical PLC warp on schedulers 1 and 3.  Choosing the
+    // PLC warp by (slot & 1) == ((slot >> 2) & 1) spreads them over all four;
+    // any other slot pattern falls back to warp 1 (both warps decide alike).
+    __shared__ unsigned hw_slot[2 * EPB];
+    const bool is_plc = plc_role(hw_slot, warp);
     const int ep = blockIdx.x * EPB + slot;
     const int n = PR.n;
     // block-shared SEL logits (every episode of the batch uses one snapshot)
@@ -1260,7 +1279,8 @@ rollout_wide_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) 
     extern __shared__ __align__(16) uint8_t smem[];
     constexpr int RPL = (MAXD + MAXD * MAXD + 31) / 32;
     const int lane = lane_id();
-    const bool is_plc = (threadIdx.x >> 5) & 1;
+    __shared__ unsigned hw_slot[2];
+    const bool is_plc = plc_role(hw_slot, threadIdx.x >> 5);  // spread over schedulers
     const int n = PR.n;
     uint8_t *sb = smem;
     uint8_t *nb = (uint8_t *)A.workspace + (size_t)blockIdx.x * L.gbytes;
