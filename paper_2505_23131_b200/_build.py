@@ -56,7 +56,7 @@ def build(force: bool = False, verbose: bool = False, profile: bool = False) -> 
     if verbose:
         flags += ["-Xptxas", "-v"]
     if profile:
-        flags += ["-DFP_PHASE_PROFILE"]
+        flags += ["-DFP_PHASE_PROFILE", "-DFP_SMALL_TIMING"]
     # one nvcc per translation unit, all in parallel
     procs = []
     for src in sources():

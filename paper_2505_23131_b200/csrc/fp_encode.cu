@@ -511,7 +511,9 @@ static int launch_gnn_tc(DevPolicy &P, cudaStream_t st, bool sel_head = true) {
         return cudaSuccess;
     };
     if (sel_head && !P.forest && P.rows <= kSmallEncodeRows) {
-        int64_t smem = 8LL * sel_smem_doubles(H);
+        // + shared-memory H_sel copy, path sums and SEL path lists (block 0)
+        int64_t smem = 8LL * (sel_smem_doubles(H) + 3LL * P.n * H) +
+                       4LL * (2 * (P.n + 1) + P.n_bpath + P.n_tpath);
         for (int k = 0; k < P.K; ++k)
             smem = std::max<int64_t>(smem, 8LL * node_smem_doubles(H, k, k == P.K - 1));
         const void *kern = (const void *)gnn_small_kernel<H, BWD>;
@@ -779,6 +781,8 @@ int fp_policy_create(const fp_problem *p, const fp_policy_desc *desc, fp_policy 
     P.adj_e = (const double *)(b + o_ae);
     P.bp_ptr = (const int *)(b + o_bp); P.bp_idx = (const int *)(b + o_bi);
     P.tp_ptr = (const int *)(b + o_tp); P.tp_idx = (const int *)(b + o_ti);
+    P.n_bpath = forest ? 0 : (int)Lb;
+    P.n_tpath = forest ? 0 : (int)Lt;
     P.ibp_ptr = (const int *)(b + o_ibp); P.ibp_idx = (const int *)(b + o_ibi);
     P.itp_ptr = (const int *)(b + o_itp); P.itp_idx = (const int *)(b + o_iti);
     P.forest = forest ? 1 : 0;

@@ -407,15 +407,19 @@ __global__ void __launch_bounds__(256, 2) gnn_node_kernel(DevPolicy P, int k, in
 // reads them like the forest form's pointer-jumped sums.
 // ---------------------------------------------------------------------------
 template <int H>
-__device__ __forceinline__ void gnn_pathsum_body(const DevPolicy &P, int bx_, int gx_) {
+__device__ __forceinline__ void gnn_pathsum_body(const DevPolicy &P, int bx_, int gx_,
+                                                 const double *Hs_copy = nullptr,
+                                                 const int *const *paths = nullptr,
+                                                 double *const *ps_out = nullptr) {
     constexpr int HPL = (H + 31) / 32;
     const int lane = lane_id(), warps = blockDim.x >> 5;
-    const double *Hs = P.H[0][P.K];
+    const double *Hs = Hs_copy ? Hs_copy : P.H[0][P.K];
     for (int v = bx_ * warps + (threadIdx.x >> 5); v < P.n; v += gx_ * warps) {
 #pragma unroll
         for (int w = 0; w < 2; ++w) {
-            const int *pp = w == 0 ? P.bp_ptr : P.tp_ptr;
-            const int *pi = w == 0 ? P.bp_idx : P.tp_idx;
+            // (paths: shared-memory copies of bp_ptr, bp_idx, tp_ptr, tp_idx)
+            const int *pp = paths ? paths[2 * w] : w == 0 ? P.bp_ptr : P.tp_ptr;
+            const int *pi = paths ? paths[2 * w + 1] : w == 0 ? P.bp_idx : P.tp_idx;
             const int q0 = pp[v], q1 = pp[v + 1];
             double acc[HPL];
 #pragma unroll
@@ -438,7 +442,7 @@ __device__ __forceinline__ void gnn_pathsum_body(const DevPolicy &P, int bx_, in
 #pragma unroll
             for (int t = 0; t < HPL; ++t) {
                 const int j = lane + 32 * t;
-                if (j < H) P.PS[w][0][(size_t)v * H + j] = acc[t];
+                if (j < H) (ps_out ? ps_out[w] : P.PS[w][0])[(size_t)v * H + j] = acc[t];
             }
         }
     }
@@ -456,38 +460,49 @@ __global__ void __launch_bounds__(256) gnn_pathsum_kernel(DevPolicy P) {
 // ---------------------------------------------------------------------------
 __host__ __device__ inline int sel_smem_doubles(int H) { return (4 * H / 4) * (H / 8) * 32; }
 
+// PLC constants M = Wy @ W1c (5 x h), c = by @ W1c + b1 (policy.py:218-222), one
+// warp: lane = column, the six dot products interleaved (independent chains)
+template <int H>
+__device__ __forceinline__ void gnn_plc_consts_body(const DevPolicy &P) {
+    const int lane = lane_id();
+    const double *yw = P.W(PR_PLC_Y_W), *yb = P.W(PR_PLC_Y_B), *w1 = P.W(PR_PLC_H1_W),
+                 *b1 = P.W(PR_PLC_H1_B);
+    for (int j = lane; j < H; j += 32) {
+        double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll 4
+        for (int i = 0; i < H; ++i) {
+            const double w = w1[(2 * H + i) * H + j];
+#pragma unroll
+            for (int rr = 0; rr < 5; ++rr) acc[rr] = fma(yw[rr * H + i], w, acc[rr]);
+            acc[5] = fma(yb[i], w, acc[5]);
+        }
+#pragma unroll
+        for (int rr = 0; rr < 5; ++rr) P.M[rr * H + j] = acc[rr];
+        P.c[j] = acc[5] + b1[j];
+    }
+}
+
 template <int H, bool BWD>
-__device__ __forceinline__ void gnn_sel_body(const DevPolicy &P, int e_, int bx_, int gx_, double *gsm) {
+__device__ __forceinline__ void gnn_sel_body(const DevPolicy &P, int e_, int bx_, int gx_, double *gsm,
+                                             const double *Hs_copy = nullptr, bool consts = true,
+                                             const double *Sb_copy = nullptr,
+                                             const double *St_copy = nullptr) {
     constexpr int NT = H / 8;
     constexpr int KT = H;  // K = 4H
     const int lane = lane_id(), warp = threadIdx.x >> 5;
     const int warps = blockDim.x >> 5, n = P.n;
     const double s = P.slope;
-    if (bx_ == 0 && warp == 0) {
-        // M = Wy @ W1c (5 x h), c = by @ W1c + b1  (PLC, policy.py:218-222)
-        const double *yw = P.W(PR_PLC_Y_W), *yb = P.W(PR_PLC_Y_B), *w1 = P.W(PR_PLC_H1_W),
-                     *b1 = P.W(PR_PLC_H1_B);
-        for (int j = lane; j < H; j += 32) {
-            for (int rr = 0; rr < 5; ++rr) {
-                double acc = 0.0;
-                for (int i = 0; i < H; ++i) acc = fma(yw[rr * H + i], w1[(2 * H + i) * H + j], acc);
-                P.M[rr * H + j] = acc;
-            }
-            double acc = 0.0;
-            for (int i = 0; i < H; ++i) acc = fma(yb[i], w1[(2 * H + i) * H + j], acc);
-            P.c[j] = acc + b1[j];
-        }
-    }
+    if (consts && bx_ == 0 && warp == 0) gnn_plc_consts_body<H>(P);
     const double *w1 = P.W(PR_SEL_H1_W), *b1 = P.W(PR_SEL_H1_B), *w2 = P.W(PR_SEL_H2_W),
                  *b2 = P.W(PR_SEL_H2_B);
     double *Fw = gsm;
     stage_frag(Fw, 4 * H, KT, NT, [&](int kk, int j) { return w1[kk * H + j]; });
     __syncthreads();
-    const double *Hs = P.H[0][P.K];
+    const double *Hs = Hs_copy ? Hs_copy : P.H[0][P.K];
     const int rb = P.jump_rounds;
     // path sums: pointer-jumped (forest) or gnn_pathsum (explicit lists)
-    const double *Sb = P.forest ? (rb > 0 ? P.PS[0][(rb - 1) & 1] : Hs) : P.PS[0][0];
-    const double *St = P.forest ? (rb > 0 ? P.PS[1][(rb - 1) & 1] : Hs) : P.PS[1][0];
+    const double *Sb = Sb_copy ? Sb_copy : P.forest ? (rb > 0 ? P.PS[0][(rb - 1) & 1] : Hs) : P.PS[0][0];
+    const double *St = St_copy ? St_copy : P.forest ? (rb > 0 ? P.PS[1][(rb - 1) & 1] : Hs) : P.PS[1][0];
     const int r = lane >> 2, c = lane & 3, c2 = c * 2;
     for (int tile = bx_ * warps + warp; tile * 8 < n; tile += gx_ * warps) {
         const int v = tile * 8 + r;
@@ -543,21 +558,63 @@ template <int H, bool BWD>
 __global__ void __launch_bounds__(256, 1) gnn_small_kernel(DevPolicy P) {
     extern __shared__ __align__(16) double gsm[];
     const int e = blockIdx.x;
+#ifdef FP_SMALL_TIMING
+    long long tt[12]; int nt_ = 0;
+#define TT() do { __syncthreads(); tt[nt_++] = clock64(); } while (0)
+#else
+#define TT() do {} while (0)
+#endif
+    TT();
     gnn_proj0_body<H>(P, e, 0, 1, gsm);
     __syncthreads();
+    TT();
     for (int k = 0; k < P.K; ++k) {
         gnn_agg_body<H>(P, k, e, 0, 1, gsm);
         __syncthreads();
+        TT();
         const int last = k == P.K - 1;
         if (k == 0) gnn_node_body<H, true, BWD>(P, k, last, e, 0, 1, gsm);
         else gnn_node_body<H, false, BWD>(P, k, last, e, 0, 1, gsm);
         __syncthreads();
+        TT();
     }
+#ifdef FP_SMALL_TIMING
+    if (e == 1 && threadIdx.x == 0) {
+        printf("blk1: proj0 %lld agg0 %lld node0 %lld agg1 %lld node1 %lld\n", tt[1] - tt[0], tt[2] - tt[1], tt[3] - tt[2], tt[4] - tt[3], tt[5] - tt[4]);
+    }
+#endif
+    if (e == 1) gnn_plc_consts_body<H>(P);  // off the SEL block's critical path
     if (e == 0) {
-        gnn_pathsum_body<H>(P, 0, 1);
+        // the path sums walk H_sel row by row (dependent index -> row loads):
+        // from shared-memory copies of H_sel and the path lists instead of
+        // L2 round trips
+        double *hs = gsm + sel_smem_doubles(H);
+        const double *Hs = P.H[0][P.K];
+        for (int i = threadIdx.x; i < P.n * H; i += blockDim.x) hs[i] = Hs[i];
+        double *ps[2] = {hs + P.n * H, hs + 2 * P.n * H};  // path sums stay on chip
+        int *ip = (int *)(hs + 3 * P.n * H);
+        const int nb = P.bp_ptr[P.n], ntp = P.tp_ptr[P.n];
+        const int *paths[4] = {ip, ip + P.n + 1, ip + P.n + 1 + nb, ip + 2 * (P.n + 1) + nb};
+        for (int i = threadIdx.x; i <= P.n; i += blockDim.x) {
+            ((int *)paths[0])[i] = P.bp_ptr[i];
+            ((int *)paths[2])[i] = P.tp_ptr[i];
+        }
+        for (int i = threadIdx.x; i < nb; i += blockDim.x) ((int *)paths[1])[i] = P.bp_idx[i];
+        for (int i = threadIdx.x; i < ntp; i += blockDim.x) ((int *)paths[3])[i] = P.tp_idx[i];
         __syncthreads();
-        gnn_sel_body<H, BWD>(P, 0, 0, 1, gsm);
+        TT();
+        gnn_pathsum_body<H>(P, 0, 1, hs, paths, ps);
+        __syncthreads();
+        TT();
+        gnn_sel_body<H, BWD>(P, 0, 0, 1, gsm, hs, P.n_enc == 1, ps[0], ps[1]);
+        TT();
+#ifdef FP_SMALL_TIMING
+        if (threadIdx.x == 0) {
+            printf("blk0: proj0 %lld agg0 %lld node0 %lld agg1 %lld node1 %lld copy %lld pathsum %lld sel %lld\n", tt[1] - tt[0], tt[2] - tt[1], tt[3] - tt[2], tt[4] - tt[3], tt[5] - tt[4], tt[6] - tt[5], tt[7] - tt[6], tt[8] - tt[7]);
+        }
+#endif
     }
+#undef TT
 }
 
 }  // namespace fp

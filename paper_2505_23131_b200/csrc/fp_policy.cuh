@@ -57,6 +57,7 @@ struct DevPolicy {
     const int *adj_ptr, *adj_nbr;  // messages INTO v: source vertices, message order
     const double *adj_e;           // standardized edge cost per message
     const int *bp_ptr, *bp_idx, *tp_ptr, *tp_idx;     // SEL b/t paths
+    int n_bpath, n_tpath;                             // their total lengths
     const int *ibp_ptr, *ibp_idx, *itp_ptr, *itp_idx; // inverse paths (u -> v with u in path(v))
     // forest form (large graphs): next pointers + pointer-jumping buffers
     int forest, jump_rounds;
