@@ -1,4 +1,5 @@
-// Dependent-chain latencies on this GPU (cycles): DFMA, DADD, FFMA, SHFL
+// Dependent-chain latencies on this GPU (cycles per loop trip, ~19 of which are the loop itself):
+// build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/micro/lat tools/micro/lat.cu
 // (32-bit and a double as 2x32), LDS, exp(double), log(double), sqrt_rn,
 // rcp_rn, fp64 divide.  One warp, clock64 around 256-long chains.
 #include <cstdio>
