@@ -1,7 +1,8 @@
-// Dependent-chain latencies on this GPU (cycles per loop trip, ~19 of which are the loop itself):
+// Dependent-chain latencies on this GPU, in cycles per loop trip (about 19 of
+// which are the loop itself): DFMA, DADD, FFMA, SHFL (32-bit and a double),
+// LDS, exp / log / sqrt_rn / rcp / div_rn (fp64), fmax, REDUX.  One warp,
+// clock64 around 256-long chains.  Measured on B200.
 // build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/micro/lat tools/micro/lat.cu
-// (32-bit and a double as 2x32), LDS, exp(double), log(double), sqrt_rn,
-// rcp_rn, fp64 divide.  One warp, clock64 around 256-long chains.
 #include <cstdio>
 #include <cuda_runtime.h>
 #define N 256
