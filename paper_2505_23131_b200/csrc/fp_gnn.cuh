@@ -42,12 +42,29 @@ __host__ __device__ constexpr int tile_stride(int K) { return ((K + 11) / 16) * 
 
 // Stage a K x N matrix B(k, n) into fragment order [KT][NT][32]:
 // lane l of (kt, nt) holds B(kt*4 + l%4, nt*8 + l/4); rows >= K are zero.
+// Eight loads are issued before their shared-memory stores (the stores could
+// alias the generic source pointer, so a load-store loop would pay one full
+// global round trip per element).
 template <typename F>
 __device__ __forceinline__ void stage_frag(double *dst, int K, int KT, int NT, F B) {
-    for (int i = threadIdx.x; i < KT * NT * 32; i += blockDim.x) {
-        const int l = i & 31, nt = (i >> 5) % NT, kt = (i >> 5) / NT;
-        const int k = kt * 4 + (l & 3), nn = nt * 8 + (l >> 2);
-        dst[i] = k < K ? B(k, nn) : 0.0;
+    constexpr int U = 8;
+    const int total = KT * NT * 32, step = blockDim.x;
+    for (int i0 = threadIdx.x; i0 < total; i0 += U * step) {
+        double v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = i0 + u * step;
+            double x = 0.0;
+            if (i < total) {
+                const int l = i & 31, nt = (i >> 5) % NT, kt = (i >> 5) / NT;
+                const int k = kt * 4 + (l & 3), nn = nt * 8 + (l >> 2);
+                if (k < K) x = B(k, nn);
+            }
+            v[u] = x;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (i0 + u * step < total) dst[i0 + u * step] = v[u];
     }
 }
 
@@ -509,18 +526,30 @@ __device__ __forceinline__ void gnn_sel_body(const DevPolicy &P, int e_, int bx_
         const bool vok = v < n;
         double acc[NT][2];
         zero_acc(acc);
-#pragma unroll 8
-        for (int kt = 0; kt < KT; ++kt) {
-            const int cc = kt * 4 + c, b = cc / H, j = cc - b * H;
-            double x = 0.0;
-            if (vok) {
-                if (b == 0) x = Hs[(size_t)v * H + j];
-                else if (b == 3) x = P.Zs[(size_t)v * H + j];
-                else x = (b == 1 ? Sb : St)[(size_t)v * H + j];
-                if constexpr (BWD) P.emb[(size_t)v * 4 * H + cc] = x;
+        // 8 k-steps of A loads in flight before their (possibly aliasing)
+        // embedding-row stores and the MMAs
+        for (int kt0 = 0; kt0 < KT; kt0 += 8) {
+            double xs[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int cc = (kt0 + u) * 4 + c, b = cc / H, j = cc - b * H;
+                double x = 0.0;
+                if (vok && kt0 + u < KT) {
+                    if (b == 0) x = Hs[(size_t)v * H + j];
+                    else if (b == 3) x = P.Zs[(size_t)v * H + j];
+                    else x = (b == 1 ? Sb : St)[(size_t)v * H + j];
+                }
+                xs[u] = x;
             }
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt) dmma(acc[nt], x, Fw[(kt * NT + nt) * 32 + lane]);
+            for (int u = 0; u < 8; ++u) {
+                const int kt = kt0 + u;
+                if (kt >= KT) break;
+                if constexpr (BWD)
+                    if (vok) P.emb[(size_t)v * 4 * H + kt * 4 + c] = xs[u];
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) dmma(acc[nt], xs[u], Fw[(kt * NT + nt) * 32 + lane]);
+            }
         }
         double part = 0.0;
 #pragma unroll
