@@ -105,7 +105,8 @@ NATIVE_MIN_N = 4096
 def static_features(graph: DataflowGraph, comm_factor: float = DEFAULT_COMM_FACTOR,
                     native: bool | None = None) -> StaticGraphFeatures:
     n = len(graph)
-    if native if native is not None else n >= NATIVE_MIN_N:
+    use_native = n >= NATIVE_MIN_N if native is None else native
+    if use_native:
         return _static_features_native(graph, comm_factor)
     order = topo_order(graph)
     mat = np.zeros((n, 5), dtype=np.float64)
