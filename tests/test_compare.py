@@ -87,3 +87,21 @@ def test_compare_engines_end_to_end():
     assert -1.0 <= doc["pearson"] <= 1.0 and -1.0 <= doc["spearman"] <= 1.0
     with pytest.raises(ValueError, match="unknown engine"):
         compare(g, cl, engines=("nope",))
+
+
+@pytest.mark.gpu
+def test_compare_clean_run_uses_the_clusters_own_jitter():
+    """cli.py:339: the clean column is exec_time on the cluster as given (its
+    own jitter_sigma, seed 0); the noisy ones use --jitter-sigma."""
+    from paper_2505_23131_b200.compare import compare_assignments
+    from paper_2505_23131_b200.simulate import exec_time
+    g = builders.build_ffnn(8, 4, 16, 4, 2)
+    cl = ClusterSpec.from_dict({**ClusterSpec.uniform(8, rate=1e6, bandwidth=1e5).to_dict(),
+                                "jitter_sigma": 0.05})
+    pairs = [(f"r{k}", list(random_assign(g, 8, seed=k))) for k in range(3)]
+    doc = compare_assignments(g, cl, pairs, trials=2, jitter_sigma=0.3, seed=9)
+    for (name, a), row in zip(pairs, doc["rows"]):
+        assert row["clean_ms"] == exec_time(g, a, cl, seed=0)[0]
+        jc = ClusterSpec.from_dict({**cl.to_dict(), "jitter_sigma": 0.3})
+        assert row["noisy_mean_ms"] == float(np.mean([exec_time(g, a, jc, seed=9 + t)[0]
+                                                      for t in range(2)]))
