@@ -740,6 +740,11 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
             Av[t] = j < h ? Atab[(size_t)v * h + j] : 0.0;
             Gv[t] = j < h ? Gtab[(size_t)v * h + j] : 0.0;
         }
+        // the commit's operands, loaded now (off the decision -> commit chain):
+        // lane d holds v's duration on device d
+        const double fl_v = flops[v];
+        const bool ent_v = ent[v] != 0;
+        const double edur_v = lane < D ? edur[v * D + lane] : 0.0;
         // ---- device features, lane = device (policy.py:240-246) ----
         double f4 = 0.0;
         if (lane < D) {
@@ -921,9 +926,9 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
         FP_PHASE_END(pp_, 16);
         // ---- commit (timeline.py:47-58) ----
         if (lane == jdx) {
-            aflops = __dadd_rn(aflops, flops[v]);
-            if (!ent[v]) {
-                const double en = __dadd_rn(f4, edur[v * D + jdx]);
+            aflops = __dadd_rn(aflops, fl_v);
+            if (!ent_v) {
+                const double en = __dadd_rn(f4, edur_v);
                 tstart[v] = f4;
                 tend[v] = en;
                 avail = en;
