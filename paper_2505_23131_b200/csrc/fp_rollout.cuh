@@ -751,18 +751,34 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
             double f1 = 0.0, f2 = 0.0, f3 = 0.0;
             bool any_local = false;
             const int p0 = pp[v], p1 = pp[v + 1];
+            // two predecessors per trip: both load chains (index -> device ->
+            // transfer time) in flight together, folded in predecessor order
 #pragma unroll 1
-            for (int j = p0; j < p1; ++j) {
-                const int p = pi[j];
-                const int dp = dev[p];
+            for (int j = p0; j < p1; j += 2) {
+                const bool two = j + 1 < p1;
+                const int pa = pi[j], pb = two ? pi[j + 1] : pa;
+                const int da = dev[pa], db = dev[pb];
+                const bool ea = ent[pa] != 0, eb = ent[pb] != 0;
+                const double ta = tend[pa], tb = tend[pb];
+                const double ra = tdur[(pa * D + da) * D + lane], rb = tdur[(pb * D + db) * D + lane];
+                const double fa = flops[pa], fb = flops[pb];
+                const double sa = tstart[pa], sbb = tstart[pb];
                 // arrival = end + transfer (0.0 on the same device), timeline.py:30-35
-                const double arr =
-                    ent[p] ? 0.0 : __dadd_rn(tend[p], tdur[(p * D + dp) * D + lane]);
-                f3 = j == p0 ? arr : fmax(f3, arr);
-                if (dp == lane) {
-                    f1 = __dadd_rn(f1, flops[p]);
-                    f2 = any_local ? fmin(f2, tstart[p]) : tstart[p];
+                const double arra = ea ? 0.0 : __dadd_rn(ta, ra);
+                f3 = j == p0 ? arra : fmax(f3, arra);
+                if (da == lane) {
+                    f1 = __dadd_rn(f1, fa);
+                    f2 = any_local ? fmin(f2, sa) : sa;
                     any_local = true;
+                }
+                if (two) {
+                    const double arrb = eb ? 0.0 : __dadd_rn(tb, rb);
+                    f3 = fmax(f3, arrb);
+                    if (db == lane) {
+                        f1 = __dadd_rn(f1, fb);
+                        f2 = any_local ? fmin(f2, sbb) : sbb;
+                        any_local = true;
+                    }
                 }
             }
             f4 = fmax(avail, f3);
