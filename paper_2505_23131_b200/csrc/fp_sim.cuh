@@ -366,8 +366,12 @@ __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *nb, 
                     // known now that every successor is placed
                     uint32_t m = 0u;
                     if constexpr (OVL) {
+                        const int j1 = sp[v + 1];
 #pragma unroll 1
-                        for (int j = sp[v]; j < sp[v + 1]; ++j) m |= 1u << assign[si[j]];
+                        for (int j = sp[v]; j < j1; j += 2) {  // two successors per trip
+                            const int wa = si[j], wb = j + 1 < j1 ? si[j + 1] : wa;
+                            m |= (1u << assign[wa]) | (1u << assign[wb]);
+                        }
                     } else {
                         m = cons[v];
                     }
