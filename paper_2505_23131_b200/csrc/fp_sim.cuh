@@ -389,10 +389,18 @@ __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *nb, 
                     atomicOr(&rdy[v], 1u << dev);
                 }
 #pragma unroll 1
-                for (int j = sp[v]; j < sp[v + 1]; ++j) {
-                    const int w = si[j];
-                    if (assign[w] == dev && atomicSub(&missing[w], 1) == 1) {
-                        pend_push<HIER>(bits + dev * BW, L, rpos[w]);
+                for (int j = sp[v], j1 = sp[v + 1]; j < j1; j += 2) {
+                    // two successors per trip: index and device loads in flight
+                    // together, processed in successor order
+                    const bool two = j + 1 < j1;
+                    const int wa = si[j], wb = two ? si[j + 1] : wa;
+                    const bool ha = assign[wa] == dev, hb = two && assign[wb] == dev;
+                    if (ha && atomicSub(&missing[wa], 1) == 1) {
+                        pend_push<HIER>(bits + dev * BW, L, rpos[wa]);
+                        atomicAdd(&cnt[dev], 1);
+                    }
+                    if (hb && atomicSub(&missing[wb], 1) == 1) {
+                        pend_push<HIER>(bits + dev * BW, L, rpos[wb]);
                         atomicAdd(&cnt[dev], 1);
                     }
                 }
