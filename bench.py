@@ -11,9 +11,15 @@ BASELINE.json: FFNN graph, 8 simulated devices, 1024 episodes per GPU).
 NCCL allreduce of the gradient, SGD).  N>1: one process per GPU (torchrun),
 episodes sharded (weak scaling), time = max over ranks.
 
-``--impl reference`` times the reference algorithm's CPU implementation (the
-oracle port: numpy rollout structured like flowplace/policy.py + the C
-restatement of flowplace/_simcore.pyx) on all host cores.
+``--impl reference`` times the REFERENCE itself on all host cores: the
+``flowplace`` package built by ``oracle/build_ref.sh`` into ``oracle/_ref``
+(its Cython simulator core), one process per core looping exactly the calls
+of its trainer (``training.py:193-194``: ``PolicyContext.rollout`` +
+``exec_time``; ``--mode train`` runs ``sim_rl_stage``, i.e. adds the tape
+backward and SGD).  Without ``oracle/_ref`` it falls back to the oracle port
+(numpy rollout + the C restatement of ``_simcore.pyx``), ``kind: "port"``.
+The default workload is BASELINE config 3's per-GPU share: the Llama-block
+graph, 8 simulated devices, 1024 episodes per GPU (8192 at 8 GPUs).
 """
 
 from __future__ import annotations
@@ -62,10 +68,49 @@ def workload(name: str):
 
 
 # --------------------------------------------------------------------------- CPU
-def _cpu_worker(args):
-    """Reference-algorithm episodes on one core until the deadline."""
+REF_DIR = ROOT / "oracle" / "_ref"
+
+
+def ref_available() -> bool:
+    return (REF_DIR / "flowplace" / "policy.py").exists()
+
+
+def _ref_worker(args):
+    """The reference's own episodes on one core until the deadline:
+    PolicyContext.rollout + exec_time (training.py:193-194), or sim_rl_stage
+    chunks (rollout + reward + tape backward + SGD) in train mode."""
     wl, seed0, deadline, train, per_step = args
-    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    if str(REF_DIR) not in sys.path:
+        sys.path.insert(0, str(REF_DIR))
+    os.environ.pop("FLOWPLACE_SIM_BACKEND", None)
+    from flowplace import graph as RG
+    from flowplace import simulate as RS
+    from flowplace.cluster import ClusterSpec as RC
+    from flowplace.policy import PolicyConfig as RPC, PolicyContext as RPX, init_policy_params as rinit
+    from flowplace.training import TrainConfig as RTC, sim_rl_stage
+    from paper_2505_23131_b200.graph import graph_to_dict
+    assert RS.backend_name() == "cython", RS.backend_name()
+    g, cl, _ = workload(wl)
+    rg = RG.graph_from_dict(graph_to_dict(g))
+    rc = RC.from_dict(cl.to_dict())
+    pc = RPC(hidden=32, k_rounds=2, mp_mode="per_step" if per_step else "per_episode")
+    params = rinit(pc, seed=0)
+    ctx = RPX(rg, rc, pc)
+    done = 0
+    t0 = time.perf_counter()
+    while time.perf_counter() < deadline or done == 0:
+        if train:
+            sim_rl_stage(rg, rc, RTC(episodes=1, seed=seed0 + done), pc, params, context=ctx)
+        else:
+            a, _ = ctx.rollout(params, epsilon=EPSILON, seed=seed0 + done)
+            RS.exec_time(rg, a, rc, "fifo", seed=0, features=ctx.features)
+        done += 1
+    return done, time.perf_counter() - t0
+
+
+def _port_worker(args):
+    """Reference-algorithm episodes (the oracle port) on one core."""
+    wl, seed0, deadline, train, per_step = args
     from oracle import policy as OP
     from oracle import sim as osim
     from paper_2505_23131_b200.params import init_policy_params
@@ -89,18 +134,66 @@ def _cpu_worker(args):
     return done, time.perf_counter() - t0
 
 
+def _cpu_worker(args):
+    return (_ref_worker if ref_available() else _port_worker)(args)
+
+
+_POOL = None
+
+
+def _pool(procs: int):
+    """One worker process per core, single-threaded BLAS (spawned with the
+    env set, so numpy's BLAS never starts extra threads); reused across
+    steps."""
+    global _POOL
+    if _POOL is None:
+        for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+            os.environ[k] = "1"
+        _POOL = mp.get_context("spawn").Pool(procs)
+    return _POOL
+
+
 def cpu_throughput(wl: str, seconds: float, procs: int, train: bool = False,
                    per_step: bool = False):
+    pool = _pool(procs)
+    # every worker imports its stack first (untimed), then runs to a shared deadline
+    pool.map(_warm_worker, [(wl, per_step)] * procs)
     deadline = time.perf_counter() + seconds
-    if procs == 1:
-        res = [_cpu_worker((wl, 1000, deadline, train, per_step))]
-    else:
-        with mp.get_context("fork").Pool(procs) as pool:
-            res = pool.map(_cpu_worker, [(wl, 1000 + i, deadline, train, per_step)
-                                         for i in range(procs)])
+    res = pool.map(_cpu_worker, [(wl, 1000 + 7919 * i, deadline, train, per_step)
+                                 for i in range(procs)])
     eps = sum(r[0] for r in res)
     wall = max(r[1] for r in res)
     return eps / wall, eps, wall
+
+
+def _warm_worker(args):
+    wl, per_step = args
+    _cpu_worker((wl, 0, 0.0, False, per_step))
+    return True
+
+
+def cpu_kind() -> str:
+    return "reference" if ref_available() else "port"
+
+
+def cpu_sample_desc(eps_done: int, wall: float, procs: int, train: bool = False) -> str:
+    if ref_available():
+        what = ("flowplace reference (oracle/_ref, Cython simulator core): " +
+                ("sim_rl_stage, one episode per call (rollout + exec_time + backward + SGD)"
+                 if train else "PolicyContext.rollout + exec_time per episode"))
+    else:
+        what = "oracle port (numpy rollout + C simulator)"
+    return f"{eps_done} episodes in {wall:.1f}s across {procs} processes, {what}"
+
+
+def bench_config(args, world: int, desc: str) -> dict:
+    """The config both arms report (same keys, so the driver can pair them)."""
+    return {"workload": desc, "episodes_per_gpu": args.batch,
+            "global_batch": args.batch * world, "mode": args.mode, "epsilon": EPSILON,
+            "policy": f"hidden 32, K 2, {args.mp_mode}", "parallelism": f"episode-dp{world}",
+            "l2": "GPU arm: flushed between timed steps (256 MiB write); e2e: steps pipelined "
+                  "(D2H on a side stream, double-buffered outputs), 256 MiB flush on the side "
+                  "stream every step"}
 
 
 # --------------------------------------------------------------------------- clocks
@@ -354,12 +447,7 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (builder graph; random-init policy seed 0; Philox episodes)",
-            "config": {"workload": desc, "episodes_per_gpu": B, "global_batch": B * world,
-                       "mode": args.mode, "epsilon": EPSILON, "policy": f"hidden 32, K 2, {args.mp_mode}",
-                       "parallelism": f"episode-dp{world}",
-                       "l2": "flushed between timed steps (256 MiB write); e2e: steps "
-                             "pipelined (D2H on a side stream, double-buffered outputs), "
-                             "256 MiB flush on the side stream every step"},
+            "config": bench_config(args, world, desc),
             "e2e": {"value": e2e_value, "unit": UNIT,
                     "h2d_bytes_per_step": int(host_params.numel() * 8),
                     "d2h_bytes_per_step": int(B * n * 4 + B * 8)},
@@ -385,9 +473,8 @@ def run_ours(args):
             v, eps_done, wall = cpu_throughput(args.workload, args.cpu_seconds, os.cpu_count(),
                                                train, args.mp_mode == "per_step")
             line["cpu_baseline"] = {
-                "value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-                "sample": f"{eps_done} episodes in {wall:.1f}s across {os.cpu_count()} "
-                          f"processes (oracle numpy rollout + C simulator)"}
+                "value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": cpu_kind(),
+                "sample": cpu_sample_desc(eps_done, wall, os.cpu_count(), train)}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -395,10 +482,10 @@ def run_ours(args):
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
     procs = os.cpu_count() or 1
-    vals = []
     total_eps = 0
     wall = 0.0
     for _ in range(args.warmup):
@@ -407,7 +494,6 @@ def run_reference(args):
     for _ in range(args.steps):
         v, e, w = cpu_throughput(args.workload, args.ref_step_seconds, procs,
                                  args.mode == "train", args.mp_mode == "per_step")
-        vals.append(v)
         total_eps += e
         wall += w
     value = total_eps / wall
@@ -416,12 +502,11 @@ def run_reference(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0, "impl": "reference",
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": desc, "mode": args.mode,
-                                        "epsilon": EPSILON,
-                                        "policy": f"hidden 32, K 2, {args.mp_mode}"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port",
-                         "sample": f"{total_eps} episodes over {args.steps} steps of "
-                                   f"{args.ref_step_seconds}s on {procs} processes"},
+        "data": "synthetic (builder graph; random-init policy seed 0)",
+        "config": bench_config(args, world, desc),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": cpu_kind(),
+                         "sample": cpu_sample_desc(total_eps, wall, procs, args.mode == "train") +
+                         f"; {args.steps} steps of {args.ref_step_seconds}s"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -432,14 +517,14 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="ffnn")
+    ap.add_argument("--workload", default="llama_block")
     ap.add_argument("--batch", type=int, default=1024)
     ap.add_argument("--mode", default="rollout", choices=("rollout", "train"))
     ap.add_argument("--mp-mode", default="per_episode", choices=("per_episode", "per_step"),
                     help="message passing once per snapshot (reference default) or per step")
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--ref-step-seconds", type=float, default=5.0)
+    ap.add_argument("--ref-step-seconds", type=float, default=4.0)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -62,7 +62,22 @@ sim_batch_kernel(DevProblem P, EpLayout L, const int32_t *__restrict__ assign, i
     for (int ep = gw; ep < B; ep += gridDim.x * WARPS) {
         uint8_t *as = nb + L.assign;
         const int32_t *row = assign + (size_t)ep * P.n;
-        for (int v = lane_id(); v < P.n; v += 32) as[v] = (uint8_t)row[v];
+        // device ids index per-device arrays and 1u << dev: an id outside
+        // [0, d) fails the episode (FP_EP_BAD_ACTION) instead of running
+        bool bad = false;
+        for (int v = lane_id(); v < P.n; v += 32) {
+            const int32_t a = row[v];
+            bad |= a < 0 || a >= P.d;
+            as[v] = (uint8_t)a;
+        }
+        if (__any_sync(FP_FULL_MASK, bad)) {
+            if (lane_id() == 0) {
+                makespan[ep] = 0.0;
+                status[ep] = FP_EP_BAD_ACTION;
+                if (trace_len) trace_len[ep] = 0;
+            }
+            continue;
+        }
         __syncwarp();
         SimOut o = sim_episode<RPL, WIDE, SM1>(
             P, nb, sb, L, strategy, (!LEAN && jit) ? jit + (size_t)ep * jit_stride : nullptr,

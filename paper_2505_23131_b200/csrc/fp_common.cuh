@@ -61,6 +61,23 @@ __device__ __forceinline__ double warp_max(double v) {
     return v;
 }
 
+// CPython >= 3.12 builtin sum() over floats (bltinmodule.c): Neumaier
+// compensation, the compensation added once at the end when nonzero and
+// finite.  The reference sums predecessor FLOPs with sum()
+// (flowplace/policy.py:243), so the device feature needs the same rounding.
+struct NeuSum {
+    double s = 0.0, c = 0.0;
+    __device__ __forceinline__ void add(double x) {
+        const double t = __dadd_rn(s, x);
+        c = __dadd_rn(c, fabs(s) >= fabs(x) ? __dadd_rn(__dsub_rn(s, t), x)
+                                            : __dadd_rn(__dsub_rn(x, t), s));
+        s = t;
+    }
+    __device__ __forceinline__ double value() const {
+        return (c != 0.0 && isfinite(c)) ? __dadd_rn(s, c) : s;
+    }
+};
+
 // Order-preserving map double -> uint64 (total order for non-NaN values).
 __device__ __forceinline__ uint64_t f64_key(double x) {
     const uint64_t b = (uint64_t)__double_as_longlong(x);

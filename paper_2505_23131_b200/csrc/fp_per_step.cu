@@ -343,7 +343,8 @@ ps_step_kernel(DevProblem PR, DevPolicy PO, DevPolicy PB, fp_rollout_args A, PsS
     const uint8_t *ent = PR.is_entry;
     double f4 = 0.0;
     if (lane < D) {
-        double f1 = 0.0, f2 = 0.0, f3 = 0.0;
+        double f2 = 0.0, f3 = 0.0;
+        fp::NeuSum f1s;
         bool any_local = false;
         for (int j = pp[v]; j < pp[v + 1]; ++j) {
             const int p = pi[j];
@@ -352,14 +353,14 @@ ps_step_kernel(DevProblem PR, DevPolicy PO, DevPolicy PB, fp_rollout_args A, PsS
                 ent[p] ? 0.0 : __dadd_rn(S.tend[base + p], PR.tdur[(p * D + dp) * D + lane]);
             f3 = j == pp[v] ? arr : fmax(f3, arr);
             if (dp == lane) {
-                f1 = __dadd_rn(f1, PR.flops[p]);
+                f1s.add(PR.flops[p]);
                 f2 = any_local ? fmin(f2, S.tstart[base + p]) : S.tstart[base + p];
                 any_local = true;
             }
         }
         f4 = fmax(S.avail[ep * 32 + lane], f3);
         double *xr = xd + lane * 5;
-        xr[0] = S.aflops[ep * 32 + lane]; xr[1] = f1; xr[2] = f2; xr[3] = f3; xr[4] = f4;
+        xr[0] = S.aflops[ep * 32 + lane]; xr[1] = f1s.value(); xr[2] = f2; xr[3] = f3; xr[4] = f4;
     }
     __syncwarp();
     if (lane < 5) {

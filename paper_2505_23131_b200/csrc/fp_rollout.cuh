@@ -748,7 +748,8 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
         // ---- device features, lane = device (policy.py:240-246) ----
         double f4 = 0.0;
         if (lane < D) {
-            double f1 = 0.0, f2 = 0.0, f3 = 0.0;
+            double f2 = 0.0, f3 = 0.0;
+            fp::NeuSum f1;
             bool any_local = false;
             const int p0 = pp[v], p1 = pp[v + 1];
             // two predecessors per trip: both load chains (index -> device ->
@@ -767,7 +768,7 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
                 const double arra = ea ? 0.0 : __dadd_rn(ta, ra);
                 f3 = j == p0 ? arra : fmax(f3, arra);
                 if (da == lane) {
-                    f1 = __dadd_rn(f1, fa);
+                    f1.add(fa);
                     f2 = any_local ? fmin(f2, sa) : sa;
                     any_local = true;
                 }
@@ -775,7 +776,7 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
                     const double arrb = eb ? 0.0 : __dadd_rn(tb, rb);
                     f3 = fmax(f3, arrb);
                     if (db == lane) {
-                        f1 = __dadd_rn(f1, fb);
+                        f1.add(fb);
                         f2 = any_local ? fmin(f2, sbb) : sbb;
                         any_local = true;
                     }
@@ -783,7 +784,7 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
             }
             f4 = fmax(avail, f3);
             double *xr = xd + lane * 5;
-            xr[0] = aflops; xr[1] = f1; xr[2] = f2; xr[3] = f3; xr[4] = f4;
+            xr[0] = aflops; xr[1] = f1.value(); xr[2] = f2; xr[3] = f3; xr[4] = f4;
         }
         __syncwarp();
         FP_PHASE_END(pp_, 11);

@@ -60,6 +60,52 @@ class CriticalPathRule:
             return top[0]
         return top[int(rng.integers(len(top)))]
 
+    def place(self, v: int, timeline: "PlacementTimeline") -> int:
+        """Earliest-start device, smallest id on ties (heuristics.py:83-91).
+        The GPU teacher computes the same argmin from its device features."""
+        starts = [timeline.earliest_start(v, d) for d in range(self.cluster.device_count)]
+        return min(range(len(starts)), key=starts.__getitem__)
+
+
+class PlacementTimeline:
+    """Host model of committed placements for ``CriticalPathRule.place``
+    (reference ``timeline.py:19-58``).  The rollout kernel keeps the same
+    per-episode state on chip; this mirror serves host callers.  Inputs
+    (entry vertices) cost nothing and are ready everywhere at t = 0."""
+
+    def __init__(self, graph, cluster):
+        self.graph, self.cluster = graph, cluster
+        n, nd = len(graph), cluster.device_count
+        self.device = [-1] * n
+        self.start, self.end = [0.0] * n, [0.0] * n
+        self.device_avail, self.assigned_flops = [0.0] * nd, [0.0] * nd
+
+    def arrival_time(self, pred: int, device: int) -> float:
+        if self.graph.is_entry(pred):
+            return 0.0
+        if self.device[pred] < 0:
+            raise ValueError(f"predecessor {pred} is not assigned yet")
+        nbytes = self.graph.vertices[pred].output_bytes
+        return self.end[pred] + self.cluster.transfer_duration(nbytes, self.device[pred], device)
+
+    def inputs_ready_time(self, v: int, device: int) -> float:
+        ready = [self.arrival_time(u, device) for u in self.graph.preds(v)]
+        return max(ready) if ready else 0.0
+
+    def earliest_start(self, v: int, device: int) -> float:
+        return max(self.device_avail[device], self.inputs_ready_time(v, device))
+
+    def commit(self, v: int, device: int) -> None:
+        if self.device[v] >= 0:
+            raise ValueError(f"vertex {v} is already placed")
+        fl = self.graph.vertices[v].flops
+        self.device[v] = device
+        self.assigned_flops[device] += fl
+        if not self.graph.is_entry(v):
+            t0 = self.earliest_start(v, device)
+            self.start[v], self.end[v] = t0, t0 + self.cluster.exec_duration(fl, device)
+            self.device_avail[device] = self.end[v]
+
 
 def critical_path_assign(graph, cluster, trials: int = 50, seed: int = 0,
                          strategy: str = "fifo", features=None, return_all: bool = False):

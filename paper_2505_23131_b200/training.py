@@ -130,22 +130,28 @@ class GlobalUpdate:
 
         return self.ret_sum / self.count if self.count else torch.zeros_like(self.ret_sum)
 
-    def alpha(self, makespan, out):
-        """alpha_e = -advantage_e / B_g with advantage_e = -mk_e - baseline."""
+    def alpha(self, makespan, out, n_global: int | None = None):
+        """alpha_e = -advantage_e / B_g with advantage_e = -mk_e - baseline
+        (``n_global`` episodes in this update, B_g unless it is a short last
+        batch)."""
         import torch
 
-        return torch.add(makespan, self.baseline(), out=out).mul_(1.0 / self.Bg)
+        return torch.add(makespan, self.baseline(), out=out).mul_(1.0 / (n_global or self.Bg))
 
-    def finish(self, makespan):
-        """Append sum of local returns, allreduce, advance the baseline."""
+    def finish(self, makespan, n_global: int | None = None):
+        """Append sum of local returns, allreduce, advance the baseline.
+        ``makespan`` holds this rank's valid episodes only (may be empty)."""
         import torch
         import torch.distributed as dist
 
-        torch.sum(makespan, dim=0, keepdim=True, out=self.gbuf[-1:]).neg_()
+        if makespan.numel():
+            torch.sum(makespan, dim=0, keepdim=True, out=self.gbuf[-1:]).neg_()
+        else:
+            self.gbuf[-1:].zero_()
         if self.world > 1:
             dist.all_reduce(self.gbuf, op=dist.ReduceOp.SUM, group=self.group)
         self.ret_sum += self.gbuf[-1:]
-        self.count += self.Bg
+        self.count += n_global or self.Bg
 
 
 class BatchedTrainer:
@@ -187,59 +193,111 @@ class BatchedTrainer:
         per_round = n_enc * pc.k_rounds * 4 - n_enc
         return self.ctx.encode_launches() + 1 + 2 + 5 + per_round + 1
 
-    def step(self, seed: int, out=None, kernel_events=None, record=False):
-        """One update over B local episodes.  Returns host stats when
-        ``record`` (makespans, advantages, epsilon, lr) — that needs a sync."""
+    def local_count(self, n_global: int) -> int:
+        """Episodes of a (possibly short) update of ``n_global`` episodes that
+        fall on this rank: global index u*B_g + rank*B + b, b < B."""
+        return max(0, min(self.B, n_global - self.rank * self.B))
+
+    def step(self, seed: int, out=None, kernel_events=None, record=False,
+             n_global: int | None = None):
+        """One update over B local episodes (``n_global`` < B_g: a short last
+        batch of exactly that many episodes across the ranks; a rank with no
+        episode still joins the allreduce).  Returns host stats when
+        ``record`` (makespans, advantages, epsilon, lr, per-episode loss for
+        imitation) — that needs a sync."""
         import torch
 
         ctx = self.ctx
+        ng = self.Bg if n_global is None else int(n_global)
+        if not 0 < ng <= self.Bg:
+            raise ValueError(f"n_global must be in 1..{self.Bg}")
+        Bl = self.local_count(ng)
         ep0 = self.upd.count  # global episodes before this batch
         eps = 0.0 if self.stage == "imitation" else self.eps_sched.value(ep0)
         lr = self.lr_sched.value(ep0)
         if out is None:
-            out = self.out = self.out or ctx.alloc_batch(self.B, grad=True)
+            out = self.out = self.out or ctx.alloc_batch(
+                self.B, grad=True, trace_steps=self.stage == "imitation")
         ctx.prepare(self.flat)
         if kernel_events is not None:
             kernel_events[0].record()
         mode = "teacher" if self.stage == "imitation" else "sample"
-        ctx.rollout_batch(self.flat, self.B, eps, seed, mode=mode, grad=True, out=out,
-                          episode_base=self.rank * self.B, prepare=False,
-                          simulate=self.executor is None, strategy=self.config.strategy)
+        if Bl:
+            ctx.rollout_batch(self.flat, Bl, eps, seed, mode=mode, grad=True, out=out,
+                              episode_base=self.rank * self.B, prepare=False,
+                              simulate=self.executor is None, strategy=self.config.strategy)
         if kernel_events is not None:
             kernel_events[1].record()
-        if self.executor is not None and hasattr(self.executor, "batch"):
+        if self.executor is not None and Bl and hasattr(self.executor, "batch"):
             # Stage III with a batched executor: the whole batch in one call
-            out.makespan = self.executor.batch(ctx, out.assign)
-        elif self.executor is not None:
+            mk = self.executor.batch(ctx, out.assign[:Bl])
+        elif self.executor is not None and Bl:
             # Stage III: rewards from an external executor (host callable)
-            assign = out.assign.cpu().numpy()
-            mk = [float(self.executor(ctx.graph, Assignment(tuple(int(x) for x in a))))
-                  for a in assign]
-            out.makespan = torch.tensor(mk, dtype=torch.float64, device="cuda")
-        mk = out.makespan
-        # alpha_e = -adv_e / B_g, adv_e = -mk_e - baseline
+            assign = out.assign[:Bl].cpu().numpy()
+            mkl = [float(self.executor(ctx.graph, Assignment(tuple(int(x) for x in a))))
+                   for a in assign]
+            mk = torch.tensor(mkl, dtype=torch.float64, device="cuda")
+        else:
+            mk = out.makespan[:Bl]
+        if Bl and bool((out.status[:Bl] != 0).any()):
+            st = out.status[:Bl].cpu().numpy()
+            raise RuntimeError(f"rollout failed for {int((st != 0).sum())} of {Bl} episodes "
+                               f"(status codes {sorted(set(st.tolist()) - {0})})")
+        # alpha_e = -adv_e / n_global, adv_e = -mk_e - baseline
         if record:
             base_host = float(self.upd.baseline().item())
+        alpha = self.alpha[:Bl]
         if self.stage == "imitation":
-            self.alpha.fill_(-1.0 / self.Bg)
+            alpha.fill_(-1.0 / ng)
             beta = 0.0
         else:
-            self.upd.alpha(mk, self.alpha)
-            beta = -self.config.entropy_weight / self.Bg
-        N.check(N.lib().fp_pg_reduce(ctx.handle, N.ptr(out.grad_rows), N.ptr(out.grad_ep),
-                                     N.ptr(out.assign), N.ptr(self.alpha), ctypes.c_double(beta),
-                                     ctypes.c_int32(self.B), N.stream_ptr()))
-        N.check(N.lib().fp_policy_backward(ctx.handle, N.ptr(self.grad), N.stream_ptr()))
-        self.upd.finish(mk)
+            self.upd.alpha(mk, alpha, ng)
+            beta = -self.config.entropy_weight / ng
+        if Bl:
+            N.check(N.lib().fp_pg_reduce(ctx.handle, N.ptr(out.grad_rows), N.ptr(out.grad_ep),
+                                         N.ptr(out.assign), N.ptr(alpha), ctypes.c_double(beta),
+                                         ctypes.c_int32(Bl), N.stream_ptr()))
+            N.check(N.lib().fp_policy_backward(ctx.handle, N.ptr(self.grad), N.stream_ptr()))
+        else:
+            self.grad.zero_()
+        self.upd.finish(mk, ng)
         N.check(N.lib().fp_sgd_step(N.ptr(self.flat), N.ptr(self.grad),
                                     ctypes.c_int64(self.grad.numel()), ctypes.c_double(lr),
                                     N.stream_ptr()))
         self.updates += 1
         if record:
             mkh = mk.cpu().numpy()
-            return {"makespan": mkh, "advantage": -mkh - base_host, "epsilon": eps, "lr": lr,
-                    "assign": out.assign.cpu().numpy()}
+            rec = {"makespan": mkh, "advantage": -mkh - base_host, "epsilon": eps, "lr": lr,
+                   "assign": out.assign[:Bl].cpu().numpy()}
+            if out.step_lp is not None:
+                # imitation loss of each episode: -sum of its 2n log-probs
+                # (training.py:144-146; np.sum of the concatenated [1, 2n] row)
+                lp = out.step_lp[:Bl].cpu().numpy().reshape(Bl, 1, -1)
+                rec["loss"] = [float(-np.sum(lp[b])) for b in range(Bl)]
+            return rec
         return None
+
+
+def measure_teacher_agreement(ctx: PolicyContext, params, teacher, rollouts: int = 100,
+                              seed: int = 0) -> float:
+    """Fraction of teacher-forced steps where the policy's greedy action
+    matches the teacher's, select and place counted separately
+    (training.py:162-178).  All ``rollouts`` episodes run as one teacher-mode
+    batch on the GPU (episode k keyed by seed + k, as the reference's seeds)."""
+    if teacher is not None and not isinstance(teacher, CriticalPathRule):
+        raise NotImplementedError("the CUDA rollout executes CriticalPathRule natively")
+    if rollouts <= 0:
+        return 1.0
+    rb = ctx.rollout_batch(params, rollouts, 0.0, seed, mode="teacher", simulate=False,
+                           trace_steps=True)
+    st = rb.status.cpu().numpy()
+    if (st != 0).any():
+        raise RuntimeError(f"teacher rollout failed (status {sorted(set(st.tolist()))})")
+    vd = rb.step_vd.cpu().numpy()
+    am = rb.step_argmax.cpu().numpy()
+    agree = int((am[..., 0] == vd[..., 0]).sum()) + int((am[..., 1] == vd[..., 1]).sum())
+    total = 2 * vd.shape[0] * vd.shape[1]
+    return agree / total if total else 1.0
 
 
 def _stage(stage: str, graph, cluster, config: TrainConfig, pconfig: PolicyConfig, params,
@@ -251,15 +309,19 @@ def _stage(stage: str, graph, cluster, config: TrainConfig, pconfig: PolicyConfi
     curve = []
     best_mk, best_assign = None, None
     n_updates = (config.episodes + tr.Bg - 1) // tr.Bg
+    final_loss = None
     for u in range(n_updates):
-        st = tr.step(seed=seeds[min(u * tr.Bg, len(seeds) - 1)], record=True)
-        for b in range(tr.B):
+        # exactly config.episodes episodes: the last update may be short
+        ng = min(tr.Bg, config.episodes - u * tr.Bg)
+        st = tr.step(seed=seeds[u * tr.Bg], record=True, n_global=ng)
+        for b in range(len(st["makespan"])):
             idx = u * tr.Bg + rank * tr.B + b
             mk = float(st["makespan"][b])
             row = {"index": idx, "makespan_ms": mk, "advantage": float(st["advantage"][b]),
                    "epsilon": st["epsilon"], "lr": st["lr"]}
             if stage == "imitation":
                 row["advantage"] = 0.0
+                row["loss"] = final_loss = st["loss"][b]
             curve.append(row)
             if best_mk is None or mk < best_mk:
                 best_mk = mk
@@ -272,7 +334,8 @@ def _stage(stage: str, graph, cluster, config: TrainConfig, pconfig: PolicyConfi
     return StageResult(stage, params if isinstance(params, dict) else out_params, curve,
                        best_makespan=None if stage == "imitation" else best_mk,
                        best_assignment=None if stage == "imitation" else best_assign,
-                       encoder_invocations=ctx.encode_count - start_enc)
+                       encoder_invocations=ctx.encode_count - start_enc,
+                       final_loss=final_loss)
 
 
 def imitation_stage(graph, cluster, config, pconfig, params, teacher=None, context=None,

@@ -28,10 +28,13 @@ def test_reference_arm_line():
     assert d["impl"] == "reference"
     assert d["metric"] == "simulated placement episodes/sec" and d["unit"] == "episodes/s"
     assert d["value"] > 0 and d["higher_is_better"] is True
-    assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
+    ref_built = (ROOT / "oracle" / "_ref" / "flowplace" / "policy.py").exists()
+    assert d["cpu_baseline"]["kind"] == ("reference" if ref_built else "port")
+    assert d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"] == {"value": d["value"], "unit": d["unit"], "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}
-    assert d["config"]["workload"].startswith("FFNN")
+    assert d["config"]["workload"].startswith("Llama-7B block")
+    assert d["config"]["episodes_per_gpu"] == 1024 and d["config"]["global_batch"] == 1024
 
 
 @pytest.mark.gpu
@@ -48,4 +51,4 @@ def test_our_arm_line():
     r = d["roofline"]
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-12
-    assert d["rates"]["decisions_per_s"] == pytest.approx(d["value"] * 64)
+    assert d["rates"]["decisions_per_s"] == pytest.approx(d["value"] * 208)
