@@ -127,6 +127,11 @@ int fp_run_packed(int32_t n, int32_t d, const int32_t *pred_indptr, const int32_
                   const double *blev, int32_t strategy, double comm_factor, double sigma,
                   int64_t seed, double *makespan, fp_event *events, int64_t events_cap,
                   int64_t *n_events, uint8_t *blocked);
+/* fp_run_packed keeps, per host thread, the device problems of its last 4
+ * distinct inputs (keyed by the exact graph / cluster bytes) with grow-only
+ * device + pinned buffers and its own stream: repeated calls on one graph do
+ * no allocation.  This frees the calling thread's cache. */
+int fp_run_packed_cache_clear(void);
 
 /* Static per-vertex features (flowplace/features.py:51-96) on the host in
  * native code, bit-identical to the reference's sweep: matrix [n][5] =

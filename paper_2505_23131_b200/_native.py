@@ -88,7 +88,7 @@ def stream_ptr(stream=None) -> ctypes.c_void_p:
 
 EXPORTED = (
     "fp_last_error", "fp_version", "fp_problem_create", "fp_problem_destroy",
-    "fp_problem_sim_smem", "fp_sim_workspace_size", "fp_sim_batch", "fp_run_packed",
+    "fp_problem_sim_smem", "fp_sim_workspace_size", "fp_sim_batch", "fp_run_packed", "fp_run_packed_cache_clear",
     "fp_jitter_tables", "fp_static_features",
 )
 

@@ -1,0 +1,256 @@
+"""GPU parity at the BASELINE configs' own scale (round-2 goldens,
+tests/golden/make_r2_golden.py and make_dag10k_golden.py):
+
+* config 2: 1024 reference episodes (FFNN-64, 8 devices, h32) replayed as ONE
+  forced launch -- every block and wave; makespans exact, log-probs /
+  entropies 1e-9, argmaxes exact up to declared near-ties; the teacher and
+  greedy episodes re-derived on the GPU;
+* config 4: the Llama-layer (248-op) REINFORCE gradient vs the reference's
+  autodiff at 1e-8;
+* config 5: 1024 sampled 10k-op episodes in one launch vs the oracle's
+  episodes under the same Philox draws, and 10k-op simulator makespans /
+  event streams vs the C oracle;
+* Stage III: SimulatorExecutor makespans over the reference's seed stream;
+* imitation_stage curve / final params and measure_teacher_agreement vs the
+  reference (B = 1 semantics).
+"""
+import json
+
+import numpy as np
+import pytest
+
+from helpers import graph_from_golden
+from oracle import policy as OP
+from oracle import sim as osim
+from paper_2505_23131_b200 import builders
+from paper_2505_23131_b200.cluster import ClusterSpec
+from paper_2505_23131_b200.params import init_policy_params
+from paper_2505_23131_b200.policy import PolicyConfig, PolicyContext
+
+pytestmark = pytest.mark.gpu
+GOLDEN = __import__("pathlib").Path(__file__).resolve().parent / "golden"
+TOL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available()
+    return torch
+
+
+@pytest.fixture(scope="module")
+def r2():
+    return json.loads((GOLDEN / "r2_cases.json").read_text())
+
+
+def _rel(a, b):
+    return np.abs(a - b) / np.maximum(1.0, np.abs(b))
+
+
+def _ffnn_ctx():
+    g, cl = builders.build_ffnn(8, 4, 16, 4, 2), ClusterSpec.uniform(8, rate=1e6, bandwidth=1e5)
+    pc = PolicyConfig(hidden=32, k_rounds=2)
+    return g, cl, pc, PolicyContext(g, cl, pc)
+
+
+def _near_tie_ok(ctx, params, vd_b, t, got_am, want_am):
+    """A differing argmax is accepted only on a near-tie (|dp| <= 1e-9 p)."""
+    octx = OP.Ctx(ctx.graph, ctx.cluster, ctx.config.hidden, ctx.config.k_rounds,
+                  ctx.config.leaky_slope, ctx.config.shared_encoder, ctx.features)
+    ro = OP.rollout(OP.leaves(params, need=False), octx, 0.0, mode="forced",
+                    forced=[(int(a), int(b)) for a, b in vd_b])
+    s = ro["steps"][t]
+    cands = s["candidates"]
+    ps, pp = s["sel_probs"], s["plc_probs"]
+    if got_am[0] != want_am[0]:
+        a, b = cands.index(int(got_am[0])), cands.index(int(want_am[0]))
+        assert abs(ps[a] - ps[b]) <= 1e-9 * ps[b], (t, ps[a], ps[b])
+    if got_am[1] != want_am[1]:
+        a, b = int(got_am[1]), int(want_am[1])
+        assert abs(pp[a] - pp[b]) <= 1e-9 * pp[b], (t, pp[a], pp[b])
+
+
+def test_ffnn_1024_reference_episodes_one_launch(torch_cuda):
+    """Config 2: the reference's 1024 episodes, forced, in one launch (all
+    blocks and waves): the schedule (makespan) bit-exact, per-step log-probs /
+    entropies within 1e-9, argmaxes exact except declared near-ties."""
+    z = np.load(GOLDEN / "scale_ffnn1024.npz")
+    g, cl, pc, ctx = _ffnn_ctx()
+    params = init_policy_params(pc, seed=0)
+    B, n = z["vd"].shape[:2]
+    assert B == 1024 and n == len(g)
+    forced = z["vd"].astype(np.int32)
+    # forced mode records the mixture log-probs of the episode's own epsilon:
+    # one launch per epsilon value, the episodes keep their batch positions
+    lp = np.empty((B, n, 2))
+    ent = np.empty((B, n, 2))
+    am = np.empty((B, n, 2), dtype=np.int64)
+    mk = np.empty(B)
+    for eps in np.unique(z["epsilon"]):
+        rb = ctx.rollout_batch(params, B, float(eps), 0, mode="forced", forced=forced,
+                               trace_steps=True)
+        sel = z["epsilon"] == eps
+        assert (rb.status.cpu().numpy() == 0).all()
+        assert (rb.step_vd.cpu().numpy() == forced).all()
+        lp[sel] = rb.step_lp.cpu().numpy()[sel]
+        ent[sel] = rb.step_ent.cpu().numpy()[sel]
+        am[sel] = rb.step_argmax.cpu().numpy()[sel]
+        mk[sel] = rb.makespan.cpu().numpy()[sel]
+    assert (mk == z["makespan"]).all(), np.flatnonzero(mk != z["makespan"])[:10]
+    assert _rel(lp, z["lp"]).max() <= TOL, _rel(lp, z["lp"]).max()
+    assert _rel(ent, z["ent"]).max() <= TOL, _rel(ent, z["ent"]).max()
+    bad = np.argwhere((am != z["argmax"]).any(axis=2))
+    assert len(bad) <= 0.01 * B * n, len(bad)
+    for b, t in bad[:20]:
+        _near_tie_ok(ctx, params, forced[b], t, am[b, t], z["argmax"][b, t])
+    # the teacher episodes: the critical-path rule itself on the GPU (exact)
+    tsel = np.flatnonzero(z["kind"] == 2)
+    rb = ctx.rollout_batch(params, len(tsel), 0.2, 0, mode="teacher", trace_steps=True)
+    assert (rb.step_vd.cpu().numpy() == forced[tsel]).all()
+    assert (rb.makespan.cpu().numpy() == z["makespan"][tsel]).all()
+    assert _rel(rb.step_lp.cpu().numpy(), z["lp"][tsel]).max() <= TOL
+
+
+def test_llama_layer_rl_gradient_matches_reference(r2, torch_cuda):
+    """Config 4's graph: one Stage-II episode's full parameter gradient."""
+    case = r2["llama_layer_grad"]
+    g = graph_from_golden(case["graph"])
+    cl = ClusterSpec.from_dict(case["cluster"])
+    pc = PolicyConfig.from_dict(case["policy"])
+    assert len(g) == 248
+    ctx = PolicyContext(g, cl, pc)
+    params = init_policy_params(pc, seed=0)
+    acts = np.asarray(case["actions"], dtype=np.int32).reshape(1, -1, 2)
+    rb = ctx.rollout_batch(params, 1, case["epsilon"], 0, mode="forced", forced=acts,
+                           grad=True, trace_steps=True)
+    assert int(rb.status.cpu()[0]) == 0
+    assert float(rb.makespan.cpu()[0]) == case["makespan"]
+    assert _rel(rb.step_lp.cpu().numpy()[0], np.asarray(case["lp"])).max() <= TOL
+    grad = ctx.policy_gradient(rb, [-case["advantage"]], -case["entropy_weight"])
+    got = ctx.layout.unflatten(grad.cpu().numpy())
+    assert set(case["grads"]) <= set(got)
+    for name, vals in case["grads"].items():
+        np.testing.assert_allclose(got[name].data.reshape(-1), vals, rtol=1e-8, atol=1e-12,
+                                   err_msg=name)
+
+
+def test_dag10k_1024_sampled_episodes_match_oracle(torch_cuda):
+    """Config 5 at 10k ops: a 1024-episode sampled launch (wide kernel);
+    episodes 0 and 777 equal the oracle's under the same Philox draws
+    (actions exact, log-probs 1e-9, makespans bit-exact)."""
+    z = np.load(GOLDEN / "dag10k.npz")
+    g, cl = builders.sparse_dag(10_000, seed=0), ClusterSpec.uniform(8, 1e9, 1e7)
+    pc = PolicyConfig()
+    ctx = PolicyContext(g, cl, pc)
+    rb = ctx.rollout_batch(init_policy_params(pc, seed=0), 1024, float(z["epsilon"]),
+                           int(z["seed"]), trace_steps=True)
+    assert (rb.status.cpu().numpy() == 0).all()
+    vd = rb.step_vd.cpu().numpy()
+    lp = rb.step_lp.cpu().numpy()
+    ent = rb.step_ent.cpu().numpy()
+    mk = rb.makespan.cpu().numpy()
+    for k, ep in enumerate(z["episodes"]):
+        assert (vd[ep] == z["vd"][k]).all(), ep
+        want = z["lp_ent"][k]
+        got = np.stack([lp[ep, ::7, 0], lp[ep, ::7, 1], ent[ep, ::7, 0], ent[ep, ::7, 1]], 1)
+        assert _rel(got, want).max() <= TOL
+        assert mk[ep] == z["makespan"][k]
+    # every episode's makespan is its own assignment's (batched simulator)
+    from paper_2505_23131_b200.simulate import SimProblem
+    out = SimProblem(g, cl, ctx.features).simulate(rb.assign, "fifo")
+    assert (out["makespan"].cpu().numpy() == mk).all()
+
+
+def test_dag10k_simulator_traces_match_c_oracle(torch_cuda):
+    """Config 5 simulator at 10k ops: makespans and full event streams equal
+    the C oracle's (the reference's rescan loop) for three strategies."""
+    import torch
+    from paper_2505_23131_b200.simulate import SimProblem, decode_events
+    g, cl = builders.sparse_dag(10_000, seed=0), ClusterSpec.uniform(8, 1e9, 1e7)
+    prob = SimProblem(g, cl)
+    rng = np.random.default_rng(5)
+    a = rng.integers(0, 8, size=(3, len(g))).astype(np.int32)
+    for s, strategy in enumerate(("fifo", "depth_first", "breadth_first")):
+        out = prob.simulate(torch.from_numpy(a[s:s + 1]).cuda(), strategy, trace=True)
+        ref_mk, ref_ev = osim.exec_time(g, a[s], cl, strategy)
+        assert float(out["makespan"][0]) == ref_mk, strategy
+        assert int(out["status"][0]) == 0
+        ev = decode_events(out["events"][0].cpu().numpy(), int(out["trace_len"][0]))
+        assert ev == ref_ev, strategy
+
+
+def test_simulator_executor_matches_reference_stream(r2, torch_cuda):
+    """Stage III: per-call seeds base_seed + k, jitter 0.1 -- the reference's
+    makespans exactly, per call and as one batched launch."""
+    import torch
+    from paper_2505_23131_b200.training import SimulatorExecutor
+    case = r2["executor"]
+    g = graph_from_golden(case["graph"])
+    cl = ClusterSpec.from_dict(case["cluster"])
+    ex = SimulatorExecutor(cl, case["strategy"], case["jitter_sigma"], case["base_seed"])
+    got = [ex(g, a) for a in case["assign"]]
+    assert got == case["makespan"]
+    exb = SimulatorExecutor(cl, case["strategy"], case["jitter_sigma"], case["base_seed"])
+
+    class _Ctx:
+        graph = g
+    mk = exb.batch(_Ctx, torch.tensor(case["assign"], dtype=torch.int32, device="cuda"))
+    assert mk.cpu().numpy().tolist() == case["makespan"]
+
+
+def test_imitation_stage_matches_reference(r2, torch_cuda):
+    """imitation_stage at B = 1 (the reference's per-episode updates): curve
+    losses 1e-9, makespans exact, final parameters 1e-9; teacher agreement
+    before and after equal to the reference's."""
+    from paper_2505_23131_b200.heuristics import CriticalPathRule
+    from paper_2505_23131_b200.training import (TrainConfig, imitation_stage,
+                                                measure_teacher_agreement)
+    case = r2["imitation"]
+    g = graph_from_golden(case["graph"])
+    cl = ClusterSpec.from_dict(case["cluster"])
+    pc = PolicyConfig.from_dict(case["policy"])
+    ctx = PolicyContext(g, cl, pc)
+    params = init_policy_params(pc, seed=0)
+    teacher = CriticalPathRule(g, cl, ctx.features)
+    assert measure_teacher_agreement(ctx, params, teacher, 3, 0) == case["agreement_before"]
+    res = imitation_stage(g, cl, TrainConfig(**case["train"]), pc, params, context=ctx)
+    assert len(res.curve) == len(case["curve"])
+    for got, want in zip(res.curve, case["curve"]):
+        assert set(got) == set(want)
+        assert got["index"] == want["index"] and got["makespan_ms"] == want["makespan_ms"]
+        assert got["lr"] == pytest.approx(want["lr"], rel=1e-15)
+        assert abs(got["loss"] - want["loss"]) <= TOL * abs(want["loss"])
+        assert got["advantage"] == 0.0 and got["epsilon"] == 0.0
+    assert abs(res.final_loss - case["final_loss"]) <= TOL * abs(case["final_loss"])
+    for name, vals in case["final_params"].items():
+        np.testing.assert_allclose(res.params[name].data.reshape(-1), vals, rtol=1e-9,
+                                   atol=1e-13, err_msg=name)
+    assert measure_teacher_agreement(ctx, res.params, teacher, 3, 0) == case["agreement_after"]
+
+
+def test_short_last_batch_runs_exactly_the_requested_episodes(torch_cuda):
+    """episodes % batch != 0: exactly `episodes` updates' worth of episodes,
+    curve rows and baseline count (the last update is short)."""
+    from paper_2505_23131_b200.training import TrainConfig, sim_rl_stage
+    g, cl = builders.build_chainmm(64, 2), ClusterSpec.uniform(4, 1e6, 1e5)
+    pc = PolicyConfig(hidden=16, k_rounds=1)
+    res = sim_rl_stage(g, cl, TrainConfig(episodes=100, seed=0), pc,
+                       init_policy_params(pc, 0), batch_size=64)
+    assert [r["index"] for r in res.curve] == list(range(100))
+    assert res.best_makespan == min(r["makespan_ms"] for r in res.curve)
+
+
+def test_simulator_rejects_out_of_range_devices(torch_cuda):
+    """A device id outside [0, d) fails that episode (status BAD_ACTION)
+    instead of indexing past the per-device state."""
+    import torch
+    from paper_2505_23131_b200 import _native as N
+    from paper_2505_23131_b200.simulate import SimProblem
+    g, cl = builders.build_ffnn(8, 4, 16, 4, 2), ClusterSpec.uniform(8, 1e6, 1e5)
+    a = np.zeros((3, len(g)), dtype=np.int32)
+    a[1, 5] = 8
+    a[2, 7] = -1
+    out = SimProblem(g, cl).simulate(torch.from_numpy(a).cuda(), "fifo")
+    st = out["status"].cpu().numpy().tolist()
+    assert st == [0, N.EP_BAD_ACTION, N.EP_BAD_ACTION]
