@@ -523,8 +523,13 @@ int fp_run_packed(int32_t n, int32_t d, const int32_t *pred_indptr, const int32_
     const size_t off_b = off_m + 256;
     const size_t off_t = off_b + (size_t)fp_align64(n, 256);
     const size_t total = off_t + (size_t)std::max(cap, 1) * sizeof(fp_event);
-    // pinned staging: assign | jitter (upload), then the 256-byte result block
-    const size_t hup = off_m, htotal = hup + 256;
+    // pinned staging: assign | jitter (upload), the 256-byte result block,
+    // then (small traces) the whole event buffer, fetched in the same round
+    // trip as the result block -- a second synchronising copy costs more
+    // than moving up to 256 KB of unused capacity
+    const size_t ev_bytes = events ? (size_t)std::max(cap, 1) * sizeof(fp_event) : 0;
+    const bool ev_one_trip = ev_bytes <= (256u << 10);
+    const size_t hup = off_m, htotal = hup + 256 + (ev_one_trip ? ev_bytes : 0);
     if ((rc = slot->reserve(total, htotal))) return rc;
     cudaStream_t st = slot->stream;
     uint8_t *h = slot->hpin, *dmem = slot->dmem;
@@ -545,6 +550,8 @@ int fp_run_packed(int32_t n, int32_t d, const int32_t *pred_indptr, const int32_
     if (rc) return rc;
     uint8_t *hres = h + hup;
     FP_CUDA(cudaMemcpyAsync(hres, dmem + off_m, 256, cudaMemcpyDeviceToHost, st));
+    if (events && ev_one_trip)
+        FP_CUDA(cudaMemcpyAsync(hres + 256, dmem + off_t, ev_bytes, cudaMemcpyDeviceToHost, st));
     {
         cudaError_t e = cudaStreamSynchronize(st);
         if (e != cudaSuccess) {
@@ -557,9 +564,13 @@ int fp_run_packed(int32_t n, int32_t d, const int32_t *pred_indptr, const int32_
     std::memcpy(&mk, hres, 8);
     std::memcpy(&stt, hres + 64, 4);
     std::memcpy(&len, hres + 128, 4);
-    if (events && len > 0)
-        FP_CUDA(cudaMemcpy(events, dmem + off_t, (size_t)std::min(len, cap) * sizeof(fp_event),
-                           cudaMemcpyDeviceToHost));
+    if (events && len > 0) {
+        const size_t got = (size_t)std::min(len, cap) * sizeof(fp_event);
+        if (ev_one_trip)
+            std::memcpy(events, hres + 256, got);
+        else
+            FP_CUDA(cudaMemcpy(events, dmem + off_t, got, cudaMemcpyDeviceToHost));
+    }
     if (blocked && stt == FP_EP_DEADLOCK)
         FP_CUDA(cudaMemcpy(blocked, dmem + off_b, (size_t)n, cudaMemcpyDeviceToHost));
     *makespan = mk;
