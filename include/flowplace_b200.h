@@ -270,6 +270,13 @@ int fp_pg_reduce(fp_policy *pol, const double *grad_rows, const double *grad_ep,
 int fp_policy_backward(fp_policy *pol, double *grad, void *stream);
 int fp_sgd_step(double *params, const double *grad, int64_t count, double lr, void *stream);
 
+/* Tensor-core (tcgen05 + TMA) path self test: out[M][N] (fp32) = X . W with
+ * X [M][64] given as bf16 hi / lo planes (device, row pitch 128 bytes) and W
+ * [64][N] fp64 (device), N in {32, 64}; the three split products accumulate
+ * in TMEM.  Test hook for the bf16 encoder's GEMM machinery. */
+int fp_tc_gemm_selftest(const void *x_hi, const void *x_lo, const double *W, int32_t N,
+                        float *out, int32_t M, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -132,4 +132,5 @@ class FpRolloutArgs(ctypes.Structure):
 EXPORTED = EXPORTED + (
     "fp_policy_create", "fp_policy_destroy", "fp_policy_set_encoder", "fp_policy_prepare", "fp_policy_table",
     "fp_rollout_workspace_size", "fp_rollout_batch", "fp_grad_ep_stride", "fp_pg_reduce", "fp_policy_backward", "fp_sgd_step",
+    "fp_tc_gemm_selftest",
 )
