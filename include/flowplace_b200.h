@@ -238,8 +238,12 @@ int fp_policy_destroy(fp_policy *pol);
 /* Encoder implementation: 0 (default) = aggregation kernels + fp64 tensor-core
  * (DMMA) node-MLP kernels when hidden is a multiple of 8 (<= 64); 1 = one
  * fused CUDA-core kernel per round with the reference's per-column FMA order.
- * Both agree with the reference to rounding (1e-11). */
-int fp_policy_set_encoder(fp_policy *pol, int32_t fused);
+ * Both agree with the reference to rounding (1e-11).  2 = bf16 node MLPs on
+ * the 5th-gen tensor cores (tcgen05, TMA-fed, split bf16 operands, fp32
+ * accumulation in TMEM; ~1e-5 relative, the north star's bf16 MLP mode,
+ * forward only, hidden 16 / 32). */
+enum { FP_ENCODER_DMMA = 0, FP_ENCODER_FUSED = 1, FP_ENCODER_TC = 2 };
+int fp_policy_set_encoder(fp_policy *pol, int32_t mode);
 /* GNN encode + head tables for one parameter snapshot (params: device flat). */
 int fp_policy_prepare(fp_policy *pol, const double *params, void *stream);
 int fp_policy_table(const fp_policy *pol, int32_t which, const double **ptr, int64_t *count);

@@ -510,7 +510,11 @@ static int launch_gnn_tc(DevPolicy &P, cudaStream_t st, bool sel_head = true) {
             return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         return cudaSuccess;
     };
-    if (sel_head && !P.forest && P.rows <= kSmallEncodeRows) {
+    if (P.tc && (BWD || (H != 16 && H != 32))) {
+        set_error("the bf16 tensor-core encoder is forward-only, hidden 16 or 32");
+        return FP_ERR_UNSUPPORTED;
+    }
+    if (sel_head && !P.forest && P.rows <= kSmallEncodeRows && !P.tc) {
         // + shared-memory H_sel copy, path sums and SEL path lists (block 0)
         int64_t smem = 8LL * (sel_smem_doubles(H) + 3LL * P.n * H) +
                        4LL * (2 * (P.n + 1) + P.n_bpath + P.n_tpath);
@@ -537,6 +541,11 @@ static int launch_gnn_tc(DevPolicy &P, cudaStream_t st, bool sel_head = true) {
             const void *kern = (const void *)gnn_agg_kernel<H>;
             gnn_agg_kernel<H><<<dim3(grid_for(kern, 0, agg_blocks), P.n_enc), 256, 0, st>>>(P, k);
             FP_CUDA_RET(cudaGetLastError());
+        }
+        if (P.tc) {  // bf16 node MLPs on tcgen05, operands by TMA
+            const int rc = tc_node_launch(P, k, last, st);
+            if (rc) return rc;
+            continue;
         }
         const int64_t smem = 8LL * node_smem_doubles(H, k, last);
         const void *kern = k == 0 ? (const void *)gnn_node_kernel<H, true, BWD>
@@ -576,7 +585,7 @@ static int launch_gnn_tc(DevPolicy &P, cudaStream_t st, bool sel_head = true) {
 
 template <int H>
 static int launch_gnn_tc_any(DevPolicy &P, cudaStream_t st) {
-    return P.forest ? launch_gnn_tc<H, false>(P, st) : launch_gnn_tc<H, true>(P, st);
+    return (P.forest || P.tc) ? launch_gnn_tc<H, false>(P, st) : launch_gnn_tc<H, true>(P, st);
 }
 
 int gnn_encode_rows(DevPolicy &P, cudaStream_t st, bool bwd, bool sel_head) {
@@ -825,13 +834,38 @@ int fp_policy_destroy(fp_policy *pol) {
     if (!pol) return FP_OK;
     if (pol->train) fp_train_state_free(pol->train);
     if (pol->arena) cudaFree(pol->arena);
+    if (pol->tc_planes) cudaFree(pol->tc_planes);
     delete pol;
     return FP_OK;
 }
 
-int fp_policy_set_encoder(fp_policy *pol, int32_t fused) {
+int fp_policy_set_encoder(fp_policy *pol, int32_t mode) {
     if (!pol) { set_error("null argument"); return FP_ERR_INVALID; }
-    pol->fused_encoder = fused ? 1 : 0;
+    DevPolicy &P = pol->dev;
+    if (mode == FP_ENCODER_TC) {
+        if (P.h != 16 && P.h != 32) {
+            set_error("the bf16 tensor-core encoder needs hidden 16 or 32");
+            return FP_ERR_UNSUPPORTED;
+        }
+        if (!pol->tc_planes && P.n > 0) {
+            const int64_t bytes = tc_plane_bytes(P.n, P.K, P.n_enc);
+            if (cudaMalloc(&pol->tc_planes, bytes) != cudaSuccess) {
+                set_error("cudaMalloc failed for the bf16 encoder planes");
+                return FP_ERR_CUDA;
+            }
+            cudaMemset(pol->tc_planes, 0, bytes);
+        }
+        if (pol->tc_planes) tc_set_planes(P, pol->tc_planes, P.n);
+        P.tc = 1;
+        pol->fused_encoder = 0;
+        return FP_OK;
+    }
+    if (mode != FP_ENCODER_DMMA && mode != FP_ENCODER_FUSED) {
+        set_error("unknown encoder mode");
+        return FP_ERR_INVALID;
+    }
+    P.tc = 0;
+    pol->fused_encoder = mode == FP_ENCODER_FUSED;
     return FP_OK;
 }
 

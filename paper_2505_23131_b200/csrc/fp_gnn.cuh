@@ -24,6 +24,8 @@
 // half-warp fragment loads hit 16 distinct 8-byte banks.
 #pragma once
 
+#include <cuda_bf16.h>
+
 #include "fp_common.cuh"
 #include "fp_policy.cuh"
 
@@ -143,6 +145,13 @@ __device__ __forceinline__ void gnn_agg_body(const DevPolicy &P, int k, int e_, 
                 }
         }
         agg[(size_t)r * HL + l] = make_double2(ax, ay);
+        if (P.tc) {  // bf16 encoder: agg as split planes at X_k[:, 32 + 2l]
+            const __nv_bfloat162 hi = __floats2bfloat162_rn((float)ax, (float)ay);
+            const float2 hf = __bfloat1622float2(hi);
+            const __nv_bfloat162 lo = __floats2bfloat162_rn((float)ax - hf.x, (float)ay - hf.y);
+            *(__nv_bfloat162 *)(P.Xh[e][k] + (size_t)r * 64 + 32 + 2 * l) = hi;
+            *(__nv_bfloat162 *)(P.Xl[e][k] + (size_t)r * 64 + 32 + 2 * l) = lo;
+        }
     }
 }
 
@@ -188,6 +197,13 @@ __device__ __forceinline__ void gnn_proj0_body(const DevPolicy &P, int e_, int b
                 } else {
                     a = H0[(size_t)v * 7 + col];
                 }
+            }
+            if (P.tc && v < rows) {  // bf16 encoder: H0 as split planes, X_0[:, 0:8)
+                const float af = (float)a;
+                const __nv_bfloat16 hi = __float2bfloat16_rn(af);
+                P.Xh[e][0][(size_t)v * 64 + col] = __bfloat16_as_ushort(hi);
+                P.Xl[e][0][(size_t)v * 64 + col] =
+                    __bfloat16_as_ushort(__float2bfloat16_rn(af - __bfloat162float(hi)));
             }
 #pragma unroll
             for (int nt = 0; nt < NT2; ++nt) dmma(acc[nt], a, Bf[(kt * NT2 + nt) * 32 + lane]);

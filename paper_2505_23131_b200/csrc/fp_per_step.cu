@@ -40,10 +40,11 @@ struct PsLayout {
     int64_t dev, npl, cand, order, tstart, tend, avail, aflops, stat;
     int64_t H[2][kMaxRounds + 1], Pm[2][kMaxRounds], Qm[2][kMaxRounds], AG[2][kMaxRounds];
     int64_t Zs, A, G;
+    int64_t X;  // bf16 encoder planes (tc mode), 0 bytes otherwise
     int64_t bytes;
 };
 
-static PsLayout ps_layout(int n, int B, int h, int K, int n_enc, int W) {
+static PsLayout ps_layout(int n, int B, int h, int K, int n_enc, int W, bool tc) {
     PsLayout L{};
     int64_t o = 0;
     const int64_t R = (int64_t)n * B;
@@ -67,6 +68,7 @@ static PsLayout ps_layout(int n, int B, int h, int K, int n_enc, int W) {
         }
     }
     L.Zs = take(8 * R * h); L.A = take(8 * R * h); L.G = take(8 * R * h);
+    L.X = tc ? take(tc_plane_bytes(R, K, n_enc)) : 0;
     L.bytes = (o + 255) / 256 * 256;
     return L;
 }
@@ -528,7 +530,7 @@ int per_step_rollout(const fp_problem *p, const fp_policy *pol, const fp_rollout
         return FP_ERR_UNSUPPORTED;
     }
     const int n = PR.n, B = a.B;
-    const PsLayout L = ps_layout(n, B, PO.h, PO.K, PO.n_enc, PR.W);
+    const PsLayout L = ps_layout(n, B, PO.h, PO.K, PO.n_enc, PR.W, PO.tc != 0);
     if (ws_needed) { *ws_needed = L.bytes; return FP_OK; }
     if (!a.workspace || a.workspace_bytes < L.bytes) {
         set_error("workspace too small for the per_step rollout (see fp_rollout_workspace_size)");
@@ -556,6 +558,10 @@ int per_step_rollout(const fp_problem *p, const fp_policy *pol, const fp_rollout
         }
     }
     PB.Zs = (double *)(w + L.Zs); PB.A = (double *)(w + L.A); PB.G = (double *)(w + L.G);
+    if (PB.tc) {  // the B x n-row X planes; columns nobody writes stay zero
+        tc_set_planes(PB, w + L.X, (int64_t)n * B);
+        cudaMemsetAsync(w + L.X, 0, tc_plane_bytes((int64_t)n * B, PO.K, PO.n_enc), st);
+    }
     ps_init_kernel<<<(B + kPsWarps - 1) / kPsWarps, kPsWarps * 32, 0, st>>>(PR, S, B);
     const int D = PR.d, h = PO.h;
     for (int step = 0; step < n; ++step) {

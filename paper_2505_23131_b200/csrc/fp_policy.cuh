@@ -78,6 +78,11 @@ struct DevPolicy {
     double *ds, *dA, *dG, *dsmall; // reduced gradient tables
     double *partial;               // episode-chunk partials of the reduction
     int partial_rows;
+    // bf16 tensor-core encoder (fp_tc_node.cu): round inputs X_k = [H_k | agg_k]
+    // as split bf16 planes (hi, lo), [rows][64], H_k at columns [0, dk),
+    // agg_k at [32, 32 + h); zero elsewhere
+    int tc;
+    uint16_t *Xh[2][kMaxRounds], *Xl[2][kMaxRounds];
 
     __device__ __forceinline__ const double *W(int role) const { return params + off[role]; }
 };
@@ -85,6 +90,14 @@ struct DevPolicy {
 // GNN encode of every row of P (fp_encode.cu): aggregation + DMMA node MLPs
 // (+ forest path sums and the SEL head when sel_head).  0 or FP_ERR_*.
 int gnn_encode_rows(DevPolicy &P, cudaStream_t st, bool bwd, bool sel_head);
+
+// bf16 tensor-core node MLPs of round k (fp_tc_node.cu); needs P.tc planes.
+int tc_node_launch(const DevPolicy &P, int k, bool last, cudaStream_t st);
+// bytes of the X planes of a policy / per_step batch with `rows` rows
+inline int64_t tc_plane_bytes(int64_t rows, int K, int n_enc) {
+    return rows * 64 * 2 * 2 * (int64_t)K * n_enc;
+}
+void tc_set_planes(DevPolicy &P, void *base, int64_t rows);
 
 }  // namespace fp
 
@@ -97,5 +110,6 @@ struct fp_policy {
     const fp_problem *problem = nullptr;
     fp_train_state *train = nullptr;  // backward job lists (fp_train.cu)
     int fused_encoder = 0;            // 1: single fused per-vertex kernel (reference order)
+    void *tc_planes = nullptr;        // bf16 encoder planes (per-snapshot rows), lazily
     int64_t n_params = 0;
 };

@@ -26,6 +26,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <string>
 
 #include "fp_policy.cuh"
@@ -163,6 +164,335 @@ __global__ void __launch_bounds__(128) tc_gemm_selftest_kernel(
     tc::tc_fence_before();
     __syncthreads();
     if (warp == 1) tc::tmem_free<64>(tm);
+}
+
+// ---------------------------------------------------------------------------
+// The node-MLP kernel of round k (see the file header).  Persistent: CTA
+// (x, e) walks 128-row tiles t = x, x + gridDim.x, ... of encoder e.
+// ---------------------------------------------------------------------------
+template <int H>
+struct TcSmem {
+    static constexpr int kX = kTcStages * 2 * kTcTileBytes;  // X stages (hi, lo)
+    static constexpr int kA2 = 2 * kTcTileBytes;             // H' (| zp) tile, hi / lo
+    static constexpr int kB1 = 2 * H * 128;                  // phi^T, hi / lo
+    static constexpr int kB2 = 2 * 2 * H * 128;              // [psi_s | psi_d]^T or W1ad^T + W1b^T
+    static constexpr int kBytes = kX + kA2 + kB1 + kB2;
+};
+
+__device__ __forceinline__ float leakyf(float x, float s) { return x > 0.f ? x : s * x; }
+
+// 16 consecutive bf16 split values of one row into a SW128 tile (two 16B chunks)
+__device__ __forceinline__ void put_row16(uint8_t *hi, uint8_t *lo, int row, int col0,
+                                          const float (&v)[16]) {
+#pragma unroll
+    for (int c = 0; c < 16; c += 8) {
+        uint32_t ph[4], pl[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            __nv_bfloat16 h0, l0, h1, l1;
+            tc::split_bf16(v[c + 2 * i], h0, l0);
+            tc::split_bf16(v[c + 2 * i + 1], h1, l1);
+            ph[i] = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
+            pl[i] = (uint32_t)__bfloat16_as_ushort(l0) | ((uint32_t)__bfloat16_as_ushort(l1) << 16);
+        }
+        const uint32_t o = tc::sw128_off(row, col0 + c);
+        *(uint4 *)(hi + o) = make_uint4(ph[0], ph[1], ph[2], ph[3]);
+        *(uint4 *)(lo + o) = make_uint4(pl[0], pl[1], pl[2], pl[3]);
+    }
+}
+
+// the same 16 values into a row of a global [rows][64] plane pair
+__device__ __forceinline__ void put_plane16(uint16_t *hi, uint16_t *lo, int64_t row, int col0,
+                                            const float (&v)[16]) {
+#pragma unroll
+    for (int c = 0; c < 16; c += 8) {
+        uint32_t ph[4], pl[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            __nv_bfloat16 h0, l0, h1, l1;
+            tc::split_bf16(v[c + 2 * i], h0, l0);
+            tc::split_bf16(v[c + 2 * i + 1], h1, l1);
+            ph[i] = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
+            pl[i] = (uint32_t)__bfloat16_as_ushort(l0) | ((uint32_t)__bfloat16_as_ushort(l1) << 16);
+        }
+        *(uint4 *)(hi + row * 64 + col0 + c) = make_uint4(ph[0], ph[1], ph[2], ph[3]);
+        *(uint4 *)(lo + row * 64 + col0 + c) = make_uint4(pl[0], pl[1], pl[2], pl[3]);
+    }
+}
+
+template <int H>
+__global__ void __launch_bounds__(kTcThreads, 1)
+tc_node_kernel(const __grid_constant__ CUtensorMap mx_hi0, const __grid_constant__ CUtensorMap mx_lo0,
+               const __grid_constant__ CUtensorMap mx_hi1, const __grid_constant__ CUtensorMap mx_lo1,
+               DevPolicy P, int k, int last) {
+    static_assert(H == 16 || H == 32, "tensor-core encoder: hidden 16 or 32");
+    using L = TcSmem<H>;
+    extern __shared__ __align__(1024) uint8_t tc_smem_raw[];
+    uint8_t *sm = (uint8_t *)(((uintptr_t)tc_smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t *xs = sm;                      // [stage][hi/lo] tiles
+    uint8_t *a2h = sm + L::kX, *a2l = a2h + kTcTileBytes;
+    uint8_t *b1h = a2h + L::kA2, *b1l = b1h + H * 128;
+    uint8_t *b2h = b1h + L::kB1, *b2l = b2h + 2 * H * 128;
+    __shared__ uint64_t bar_full[kTcStages], bar_empty[kTcStages];
+    __shared__ uint64_t bar_d1, bar_a2, bar_d2, bar_done;
+    __shared__ uint32_t tmem_base;
+
+    const int e = blockIdx.y;
+    const CUtensorMap *mh = e == 0 ? &mx_hi0 : &mx_hi1;
+    const CUtensorMap *ml = e == 0 ? &mx_lo0 : &mx_lo1;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int DK = k == 0 ? 7 : H;
+    const bool feeds_sel = e == 0;
+    const bool feeds_plc = P.n_enc == 1 || e == 1;
+    const double *phw = P.W(gnn_role(e, k, 2)), *phb = P.W(gnn_role(e, k, 3));
+
+    // ---- weights (all threads): phi^T, then the second GEMM's B ----
+    stage_wt(b1h, b1l, H, [&](int kk, int n) {
+        if (kk < DK) return phw[kk * H + n];
+        if (kk >= 32 && kk < 32 + H) return phw[(DK + kk - 32) * H + n];
+        return 0.0;
+    });
+    if (!last) {
+        const double *nw = P.W(gnn_role(e, k + 1, 0));
+        stage_wt(b2h, b2l, 2 * H, [&](int kk, int n) {
+            if (kk >= H) return 0.0;
+            return n < H ? nw[kk * H + n] : nw[(H + kk) * H + (n - H)];
+        });
+    } else if (feeds_plc) {
+        // rows [0, H): [W1a; W1d]^T over K = [H' | zp] (64); rows [H, 2H): W1b^T over K = H'
+        const double *w1 = P.W(PR_PLC_H1_W);
+        stage_wt(b2h, b2l, 2 * H, [&](int kk, int n) {
+            if (n < H) {
+                if (kk < H) return w1[kk * H + n];
+                if (kk >= 32 && kk < 32 + H) return w1[(3 * H + kk - 32) * H + n];
+                return 0.0;
+            }
+            return kk < H ? w1[(H + kk) * H + (n - H)] : 0.0;
+        });
+    }
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kTcStages; ++i) {
+            tc::mbar_init(&bar_full[i], 1);
+            tc::mbar_init(&bar_empty[i], 1);
+        }
+        tc::mbar_init(&bar_d1, 1);
+        tc::mbar_init(&bar_a2, 128);
+        tc::mbar_init(&bar_d2, 1);
+        tc::mbar_init(&bar_done, 128);
+        tc::fence_mbar_init();
+        tc::tma_prefetch(mh);
+        tc::tma_prefetch(ml);
+    }
+    // A2 columns no epilogue writes (e.g. [H, 32) at H = 16) must read as 0,
+    // not as stale bits that could be NaN (NaN * 0 weights = NaN)
+    for (int i = threadIdx.x; i < L::kA2 / 16; i += blockDim.x)
+        ((uint4 *)a2h)[i] = make_uint4(0u, 0u, 0u, 0u);
+    if (warp == 1) tc::tmem_alloc<128>(&tmem_base);
+    tc::fence_proxy_async_smem();
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tm = tmem_base;
+    const int rows = P.rows;
+    const int tiles = (rows + kTcRows - 1) / kTcRows;
+
+    if (warp == 0) {
+        // ===== TMA producer =====
+        if (lane == 0) {
+            int it = 0;
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+                const int s = it % kTcStages;
+                const uint32_t ph = (it / kTcStages) & 1;
+                tc::mbar_wait(&bar_empty[s], ph ^ 1);
+                uint8_t *dh = xs + s * 2 * kTcTileBytes, *dl = dh + kTcTileBytes;
+                tc::mbar_arrive_expect_tx(&bar_full[s], 2 * kTcTileBytes);
+                tc::tma_load_2d(dh, mh, &bar_full[s], 0, t * kTcRows);
+                tc::tma_load_2d(dl, ml, &bar_full[s], 0, t * kTcRows);
+            }
+        }
+    } else if (warp == 1) {
+        // ===== MMA issuer =====
+        const uint32_t id1 = tc::idesc_bf16_f32(kTcRows, H);
+        const uint32_t id2 = tc::idesc_bf16_f32(kTcRows, last ? H : 2 * H);
+        int it = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+            const int s = it % kTcStages;
+            const uint32_t ph = (it / kTcStages) & 1;
+            tc::mbar_wait(&bar_full[s], ph);
+            if (it > 0) tc::mbar_wait(&bar_done, (it - 1) & 1);
+            tc::tc_fence_after();
+            if (lane == 0) {
+                const uint8_t *xh = xs + s * 2 * kTcTileBytes, *xl = xh + kTcTileBytes;
+                mma_split(tm, xh, xl, b1h, b1l, kTcK / 16, id1, false);
+                tc::mma_commit(&bar_empty[s]);
+                tc::mma_commit(&bar_d1);
+            }
+            __syncwarp();
+            tc::mbar_wait(&bar_a2, it & 1);
+            tc::tc_fence_after();
+            if (lane == 0) {
+                if (!last) {
+                    mma_split(tm + 64, a2h, a2l, b2h, b2l, H / 16, id2, false);
+                } else if (feeds_plc) {
+                    // A = [H' | zp] . [W1a; W1d] (K 64), G = H' . W1b (K = H)
+                    mma_split(tm + 64, a2h, a2l, b2h, b2l, kTcK / 16, id2, false);
+                    mma_split(tm + 64 + H, a2h, a2l, b2h + H * 128, b2l + H * 128, H / 16, id2,
+                              false);
+                }
+                tc::mma_commit(&bar_d2);
+            }
+            __syncwarp();
+        }
+    } else {
+        // ===== epilogue: warps 2..5, TMEM lane quarter warp % 4 =====
+        const int q = warp & 3;
+        const int rloc = q * 32 + lane;
+        const uint32_t tq = tm + ((uint32_t)(q * 32) << 16);
+        const float slope = (float)P.slope;
+        float bphi[H];
+#pragma unroll
+        for (int j = 0; j < H; ++j) bphi[j] = (float)phb[j];
+        int it = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+            const int64_t row = (int64_t)t * kTcRows + rloc;
+            const bool ok = row < rows;
+            tc::mbar_wait(&bar_d1, it & 1);
+            tc::tc_fence_after();
+            float hv[H];
+#pragma unroll
+            for (int c = 0; c < H; c += 16) {
+                float v[16];
+                tc::tmem_ld16(tq + c, v);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) hv[c + i] = leakyf(v[i] + bphi[c + i], slope);
+            }
+            // H' -> next round's planes / H_K (fp64), and the A2 tile
+#pragma unroll
+            for (int c = 0; c < H; c += 16) {
+                float v[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] = hv[c + i];
+                put_row16(a2h, a2l, rloc, c, v);
+                if (ok && !last) put_plane16(P.Xh[e][k + 1], P.Xl[e][k + 1], row, c, v);
+            }
+            if (ok && last) {
+                double *hk = P.H[e][k + 1] + row * H;
+#pragma unroll
+                for (int j = 0; j < H; j += 2) *(double2 *)(hk + j) = make_double2(hv[j], hv[j + 1]);
+            }
+            if (last) {
+                // z heads on the CUDA cores (K = 5): Zs (SEL), zp -> A2[:, 32:32+H) (PLC)
+                const int n = P.n;
+                double x5[5];
+#pragma unroll
+                for (int i = 0; i < 5; ++i) x5[i] = ok ? P.x[(size_t)(row % n) * 5 + i] : 0.0;
+                if (feeds_sel) {
+                    const double *zw = P.W(PR_SEL_Z_W), *zb = P.W(PR_SEL_Z_B);
+                    for (int j = 0; j < H; j += 2) {
+                        double z0 = zb[j], z1 = zb[j + 1];
+#pragma unroll
+                        for (int i = 0; i < 5; ++i) {
+                            z0 = fma(x5[i], zw[i * H + j], z0);
+                            z1 = fma(x5[i], zw[i * H + j + 1], z1);
+                        }
+                        if (ok) *(double2 *)(P.Zs + row * H + j) = make_double2(z0, z1);
+                    }
+                }
+                if (feeds_plc) {
+                    const double *zw = P.W(PR_PLC_Z_W), *zb = P.W(PR_PLC_Z_B);
+#pragma unroll
+                    for (int c = 0; c < H; c += 16) {
+                        float v[16];
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            double z = zb[c + i];
+#pragma unroll
+                            for (int r5 = 0; r5 < 5; ++r5) z = fma(x5[r5], zw[r5 * H + c + i], z);
+                            v[i] = (float)z;
+                        }
+                        put_row16(a2h, a2l, rloc, 32 + c, v);
+                    }
+                }
+            }
+            tc::fence_proxy_async_smem();
+            tc::tc_fence_before();
+            tc::mbar_arrive(&bar_a2);
+            tc::mbar_wait(&bar_d2, it & 1);
+            tc::tc_fence_after();
+            if (!last) {
+                // [P | Q] of round k + 1 (the aggregation adds the bias)
+#pragma unroll
+                for (int c = 0; c < 2 * H; c += 16) {
+                    float v[16];
+                    tc::tmem_ld16(tq + 64 + c, v);
+                    if (ok) {
+                        double *dst = c < H ? P.Pm[e][k + 1] + row * H + c
+                                            : P.Qm[e][k + 1] + row * H + (c - H);
+#pragma unroll
+                        for (int i = 0; i < 16; i += 2) *(double2 *)(dst + i) = make_double2(v[i], v[i + 1]);
+                    }
+                }
+            } else if (feeds_plc) {
+#pragma unroll
+                for (int c = 0; c < 2 * H; c += 16) {
+                    float v[16];
+                    tc::tmem_ld16(tq + 64 + c, v);
+                    if (ok) {
+                        double *dst = c < H ? P.A + row * H + c : P.G + row * H + (c - H);
+#pragma unroll
+                        for (int i = 0; i < 16; i += 2) *(double2 *)(dst + i) = make_double2(v[i], v[i + 1]);
+                    }
+                }
+            }
+            tc::tc_fence_before();
+            tc::mbar_arrive(&bar_done);
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tc::tmem_free<128>(tm);
+}
+
+template <int H>
+static int tc_node_launch_t(const DevPolicy &P, int k, bool last, cudaStream_t st) {
+    CUtensorMap m[2][2];
+    for (int e = 0; e < 2; ++e) {
+        const int ee = e < P.n_enc ? e : 0;
+        int rc = tc_plane_map(&m[e][0], P.Xh[ee][k], P.rows);
+        if (rc) return rc;
+        if ((rc = tc_plane_map(&m[e][1], P.Xl[ee][k], P.rows))) return rc;
+    }
+    const int smem = 1024 + TcSmem<H>::kBytes;
+    const void *kern = (const void *)tc_node_kernel<H>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int tiles = (P.rows + kTcRows - 1) / kTcRows;
+    const int gx = std::max(1, std::min(tiles, sms / P.n_enc));
+    tc_node_kernel<H><<<dim3(gx, P.n_enc), kTcThreads, smem, st>>>(m[0][0], m[0][1], m[1][0],
+                                                                    m[1][1], P, k, (int)last);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FP_ERR_CUDA; }
+    return FP_OK;
+}
+
+int tc_node_launch(const DevPolicy &P, int k, bool last, cudaStream_t st) {
+    if (P.h == 32) return tc_node_launch_t<32>(P, k, last, st);
+    if (P.h == 16) return tc_node_launch_t<16>(P, k, last, st);
+    set_error("the tensor-core encoder needs hidden 16 or 32");
+    return FP_ERR_UNSUPPORTED;
+}
+
+void tc_set_planes(DevPolicy &P, void *base, int64_t rows) {
+    uint8_t *b = (uint8_t *)base;
+    const int64_t plane = rows * 64 * 2;
+    for (int e = 0; e < P.n_enc; ++e)
+        for (int k = 0; k < P.K; ++k) {
+            P.Xh[e][k] = (uint16_t *)b;
+            P.Xl[e][k] = (uint16_t *)(b + plane);
+            b += 2 * plane;
+        }
 }
 
 }  // namespace fp

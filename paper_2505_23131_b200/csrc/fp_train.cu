@@ -498,6 +498,7 @@ int fp_policy_backward(fp_policy *pol, double *grad, void *stream) {
     DevPolicy &P = pol->dev;
     if (!P.params) { set_error("fp_policy_prepare must run before backward"); return FP_ERR_INVALID; }
     if (P.forest) { set_error("backward needs explicit SEL path lists (policy built in forest form)"); return FP_ERR_UNSUPPORTED; }
+    if (P.tc) { set_error("backward needs the fp64 encoder (the bf16 tensor-core encoder is forward only)"); return FP_ERR_UNSUPPORTED; }
     if (!pol->train) pol->train = new fp_train_state();
     auto *ts = pol->train;
     if (ts->bound_grad != grad || ts->bound_params != P.params || ts->batches.empty()) {

@@ -274,10 +274,20 @@ class PolicyContext:
                       int(self.features.path_lengths("t").max(initial=1)))
         return int(np.ceil(np.log2(longest))) if longest > 1 else 0
 
-    def set_encoder(self, fused: bool):
-        """Select the fused per-vertex encoder (reference FMA order) instead of
-        the default aggregation + DMMA node-MLP kernels."""
-        N.check(N.lib().fp_policy_set_encoder(self.handle, ctypes.c_int32(int(fused))))
+    ENCODERS = {"dmma": 0, "fused": 1, "tc": 2}
+
+    def set_encoder(self, mode):
+        """Encoder implementation: ``"dmma"`` (default: aggregation kernels +
+        fp64 tensor-core node MLPs, 1e-11 of the reference), ``"fused"`` (one
+        per-vertex kernel in the reference's FMA order) or ``"tc"`` (bf16
+        node MLPs on tcgen05 fed by TMA, split-bf16 operands, ~1e-5 relative;
+        forward only).  A bool selects fused (True) / dmma (False)."""
+        if isinstance(mode, bool):
+            mode = "fused" if mode else "dmma"
+        if mode not in self.ENCODERS:
+            raise ValueError(f"encoder must be one of {sorted(self.ENCODERS)}")
+        N.check(N.lib().fp_policy_set_encoder(self.handle, ctypes.c_int32(self.ENCODERS[mode])))
+        self.encoder = mode
         self._prepared_key = None
 
     def flat_params(self, params) -> "object":
