@@ -190,7 +190,9 @@ def bench_config(args, world: int, desc: str) -> dict:
     """The config both arms report (same keys, so the driver can pair them)."""
     return {"workload": desc, "episodes_per_gpu": args.batch,
             "global_batch": args.batch * world, "mode": args.mode, "epsilon": EPSILON,
-            "policy": f"hidden 32, K 2, {args.mp_mode}", "parallelism": f"episode-dp{world}",
+            "policy": f"hidden 32, K 2, {args.mp_mode}" + (
+                "" if args.encoder == "dmma" else f", {args.encoder} encoder"),
+            "parallelism": f"episode-dp{world}",
             "l2": "GPU arm: flushed between timed steps (256 MiB write); e2e: steps pipelined "
                   "(D2H on a side stream, double-buffered outputs), 256 MiB flush on the side "
                   "stream every step"}
@@ -290,6 +292,8 @@ def run_ours(args):
     pc = PolicyConfig(mp_mode=args.mp_mode)
     params = init_policy_params(pc, seed=0)
     ctx = PolicyContext(g, cl, pc)
+    if args.encoder != "dmma":
+        ctx.set_encoder(args.encoder)
     B = args.batch
     train = args.mode == "train"
     trainer = None
@@ -445,7 +449,7 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64" if args.encoder == "dmma" else "f64 (node MLPs: split-bf16 tcgen05, f32 accumulate)",
             "data": "synthetic (builder graph; random-init policy seed 0; Philox episodes)",
             "config": bench_config(args, world, desc),
             "e2e": {"value": e2e_value, "unit": UNIT,
@@ -523,6 +527,8 @@ def main():
     ap.add_argument("--mp-mode", default="per_episode", choices=("per_episode", "per_step"),
                     help="message passing once per snapshot (reference default) or per step")
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--encoder", default="dmma", choices=("dmma", "tc"),
+                    help="GNN node MLPs: fp64 DMMA (reference-exact) or bf16 tcgen05")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-step-seconds", type=float, default=4.0)
     ap.add_argument("--no-cpu", action="store_true")

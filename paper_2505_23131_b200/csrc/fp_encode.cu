@@ -538,8 +538,13 @@ static int launch_gnn_tc(DevPolicy &P, cudaStream_t st, bool sel_head = true) {
     for (int k = 0; k < P.K; ++k) {
         const bool last = k == P.K - 1;
         {
-            const void *kern = (const void *)gnn_agg_kernel<H>;
-            gnn_agg_kernel<H><<<dim3(grid_for(kern, 0, agg_blocks), P.n_enc), 256, 0, st>>>(P, k);
+            if (P.tc) {
+                const void *kern = (const void *)gnn_agg_kernel<H, true>;
+                gnn_agg_kernel<H, true><<<dim3(grid_for(kern, 0, agg_blocks), P.n_enc), 256, 0, st>>>(P, k);
+            } else {
+                const void *kern = (const void *)gnn_agg_kernel<H>;
+                gnn_agg_kernel<H><<<dim3(grid_for(kern, 0, agg_blocks), P.n_enc), 256, 0, st>>>(P, k);
+            }
             FP_CUDA_RET(cudaGetLastError());
         }
         if (P.tc) {  // bf16 node MLPs on tcgen05, operands by TMA

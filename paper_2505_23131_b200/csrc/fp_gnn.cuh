@@ -95,7 +95,19 @@ __device__ __forceinline__ void zero_acc(double (&acc)[NT][2]) {
 // ---------------------------------------------------------------------------
 // Aggregation (HBM-bound gather / segment reduce)
 // ---------------------------------------------------------------------------
-template <int H>
+// P/Q rows as fp64 (reference-exact encoders) or fp32 (bf16 tensor-core
+// encoder: half the gathered bytes)
+template <bool F32>
+__device__ __forceinline__ double2 pq_load(const void *base, size_t i) {
+    if constexpr (F32) {
+        const float2 f = ((const float2 *)base)[i];
+        return make_double2(f.x, f.y);
+    } else {
+        return ((const double2 *)base)[i];
+    }
+}
+
+template <int H, bool F32 = false>
 __device__ __forceinline__ void gnn_agg_body(const DevPolicy &P, int k, int e_, int bx_, int gx_, double *gsm) {
     constexpr int HL = H / 2;                   // lanes per destination (double2 each)
     constexpr int VPW = HL >= 32 ? 1 : 32 / HL; // destinations per warp
@@ -110,8 +122,8 @@ __device__ __forceinline__ void gnn_agg_body(const DevPolicy &P, int k, int e_, 
     // parameter rows sit at arbitrary offsets of the flat vector: scalar loads
     const double2 we = make_double2(psw[(size_t)(2 * dk) * H + 2 * l], psw[(size_t)(2 * dk) * H + 2 * l + 1]);
     const double2 bb = make_double2(psb[2 * l], psb[2 * l + 1]);
-    const double2 *Pm = (const double2 *)P.Pm[e][k];
-    const double2 *Qm = (const double2 *)P.Qm[e][k];
+    const void *Pm = P.Pm[e][k];
+    const void *Qm = P.Qm[e][k];
     double2 *agg = (double2 *)P.AG[e][k];
     const double s = P.slope;
     const int warps = blockDim.x >> 5;
@@ -120,7 +132,7 @@ __device__ __forceinline__ void gnn_agg_body(const DevPolicy &P, int k, int e_, 
         const int r = vb + sub;  // row = episode * n + vertex
         if (r >= rows || (HL < 32 && lane >= VPW * HL)) continue;
         const int v = r % n, base = r - v;
-        const double2 q = Qm[(size_t)r * HL + l];
+        const double2 q = pq_load<F32>(Qm, (size_t)r * HL + l);
         double ax = 0.0, ay = 0.0;
         const int m1 = P.adj_ptr[v + 1];
         for (int m = P.adj_ptr[v]; m < m1; m += 4) {
@@ -135,7 +147,7 @@ __device__ __forceinline__ void gnn_agg_body(const DevPolicy &P, int k, int e_, 
             double2 p[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u)
-                p[u] = m + u < m1 ? Pm[(size_t)w[u] * HL + l] : make_double2(0.0, 0.0);
+                p[u] = m + u < m1 ? pq_load<F32>(Pm, (size_t)w[u] * HL + l) : make_double2(0.0, 0.0);
 #pragma unroll
             for (int u = 0; u < 4; ++u)
                 if (m + u < m1) {
@@ -144,7 +156,7 @@ __device__ __forceinline__ void gnn_agg_body(const DevPolicy &P, int k, int e_, 
                     ay += gleaky(p[u].y + q.y + ev[u] * we.y + bb.y, s);
                 }
         }
-        agg[(size_t)r * HL + l] = make_double2(ax, ay);
+        if (!F32) agg[(size_t)r * HL + l] = make_double2(ax, ay);
         if (P.tc) {  // bf16 encoder: agg as split planes at X_k[:, 32 + 2l]
             const __nv_bfloat162 hi = __floats2bfloat162_rn((float)ax, (float)ay);
             const float2 hf = __bfloat1622float2(hi);
@@ -155,10 +167,10 @@ __device__ __forceinline__ void gnn_agg_body(const DevPolicy &P, int k, int e_, 
     }
 }
 
-template <int H>
+template <int H, bool F32 = false>
 __global__ void __launch_bounds__(256) gnn_agg_kernel(DevPolicy P, int k) {
     extern __shared__ __align__(16) double gsm[];
-    gnn_agg_body<H>(P, k, blockIdx.y, blockIdx.x, gridDim.x, gsm);
+    gnn_agg_body<H, F32>(P, k, blockIdx.y, blockIdx.x, gridDim.x, gsm);
 }
 
 // ---------------------------------------------------------------------------
@@ -212,6 +224,12 @@ __device__ __forceinline__ void gnn_proj0_body(const DevPolicy &P, int e_, int b
 #pragma unroll
             for (int nt = 0; nt < NT2; ++nt) {
                 const int col = nt * 8 + c * 2;
+                if (P.tc) {  // fp32 P/Q for the bf16 encoder's aggregation
+                    float *dst = col < H ? (float *)P.Pm[e][0] + (size_t)v * H + col
+                                         : (float *)P.Qm[e][0] + (size_t)v * H + (col - H);
+                    *(float2 *)dst = make_float2((float)acc[nt][0], (float)acc[nt][1]);
+                    continue;
+                }
                 double *dst = col < H ? P.Pm[e][0] + (size_t)v * H + col
                                       : P.Qm[e][0] + (size_t)v * H + (col - H);
                 *(double2 *)dst = make_double2(acc[nt][0], acc[nt][1]);

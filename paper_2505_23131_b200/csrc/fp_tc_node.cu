@@ -42,7 +42,6 @@ constexpr int kTcRows = 128;             // M per tile (TMEM lanes)
 constexpr int kTcK = 64;                 // X row: 64 bf16 = 128 bytes = one swizzle atom
 constexpr int kTcTileBytes = kTcRows * 128;  // one plane of one X tile (16 KB)
 constexpr int kTcStages = 2;
-constexpr int kTcThreads = 192;
 
 // ---------------------------------------------------------------------------
 // driver entry point for the tensor-map encoder (no -lcuda link)
@@ -170,20 +169,29 @@ __global__ void __launch_bounds__(128) tc_gemm_selftest_kernel(
 // The node-MLP kernel of round k (see the file header).  Persistent: CTA
 // (x, e) walks 128-row tiles t = x, x + gridDim.x, ... of encoder e.
 // ---------------------------------------------------------------------------
+// NG epilogue groups of 4 warps (one per TMEM lane quarter), each with its
+// own TMEM accumulator set (128 columns) and A2 tile: tiles it = g, g + NG,
+// ... go to group g, so NG tiles are in their epilogues at once while the
+// MMA warp runs one tile ahead (GEMM1 of tile it before GEMM2 of it - 1).
+constexpr int kTcGroups = 4;
+constexpr int kTcThreadsG = 96 + 128 * kTcGroups;
+
 template <int H>
 struct TcSmem {
     static constexpr int kX = kTcStages * 2 * kTcTileBytes;  // X stages (hi, lo)
-    static constexpr int kA2 = 2 * kTcTileBytes;             // H' (| zp) tile, hi / lo
+    static constexpr int kA2 = 2 * kTcTileBytes;             // per group: H' (| zp), hi / lo
     static constexpr int kB1 = 2 * H * 128;                  // phi^T, hi / lo
     static constexpr int kB2 = 2 * 2 * H * 128;              // [psi_s | psi_d]^T or W1ad^T + W1b^T
-    static constexpr int kBytes = kX + kA2 + kB1 + kB2;
+    static constexpr int kBytes = kX + kTcGroups * kA2 + kB1 + kB2;
 };
 
 __device__ __forceinline__ float leakyf(float x, float s) { return x > 0.f ? x : s * x; }
 
-// 16 consecutive bf16 split values of one row into a SW128 tile (two 16B chunks)
-__device__ __forceinline__ void put_row16(uint8_t *hi, uint8_t *lo, int row, int col0,
-                                          const float (&v)[16]) {
+// 16 consecutive split values of one row: into a SW128 tile (two 16B chunks
+// per plane) and, when `g_hi` is set, into a global [rows][64] plane pair
+__device__ __forceinline__ void put16(uint8_t *hi, uint8_t *lo, int row, int col0,
+                                      const float (&v)[16], uint16_t *g_hi = nullptr,
+                                      uint16_t *g_lo = nullptr, int64_t grow = 0) {
 #pragma unroll
     for (int c = 0; c < 16; c += 8) {
         uint32_t ph[4], pl[4];
@@ -195,47 +203,74 @@ __device__ __forceinline__ void put_row16(uint8_t *hi, uint8_t *lo, int row, int
             ph[i] = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
             pl[i] = (uint32_t)__bfloat16_as_ushort(l0) | ((uint32_t)__bfloat16_as_ushort(l1) << 16);
         }
+        const uint4 vh = make_uint4(ph[0], ph[1], ph[2], ph[3]);
+        const uint4 vl = make_uint4(pl[0], pl[1], pl[2], pl[3]);
         const uint32_t o = tc::sw128_off(row, col0 + c);
-        *(uint4 *)(hi + o) = make_uint4(ph[0], ph[1], ph[2], ph[3]);
-        *(uint4 *)(lo + o) = make_uint4(pl[0], pl[1], pl[2], pl[3]);
+        *(uint4 *)(hi + o) = vh;
+        *(uint4 *)(lo + o) = vl;
+        if (g_hi) {
+            *(uint4 *)(g_hi + grow * 64 + col0 + c) = vh;
+            *(uint4 *)(g_lo + grow * 64 + col0 + c) = vl;
+        }
     }
 }
 
-// the same 16 values into a row of a global [rows][64] plane pair
-__device__ __forceinline__ void put_plane16(uint16_t *hi, uint16_t *lo, int64_t row, int col0,
-                                            const float (&v)[16]) {
+
+// One warp's 32 consecutive rows, 2H fp32 values per row (thread = row):
+// two [rows][H] outputs A (values [0, H)) and B ([H, 2H)), fp32 or fp64.
+// The rows of a warp are one contiguous block of each output, so the values
+// go through `stg` (8 KB at H = 32; 16-byte chunks XOR-swizzled by row) and
+// leave as coalesced 16-byte row stores (lanes [0, H/2): A row, the rest: B).
+template <int H, bool F64>
+__device__ __forceinline__ void warp_store_rows(uint8_t *stg, int lane, const uint32_t (&v)[2 * H],
+                                                int64_t row0, int64_t rows, void *outA,
+                                                void *outB) {
+    constexpr int CH = 2 * H / 4;  // 16-byte chunks per staged row
 #pragma unroll
-    for (int c = 0; c < 16; c += 8) {
-        uint32_t ph[4], pl[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            __nv_bfloat16 h0, l0, h1, l1;
-            tc::split_bf16(v[c + 2 * i], h0, l0);
-            tc::split_bf16(v[c + 2 * i + 1], h1, l1);
-            ph[i] = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
-            pl[i] = (uint32_t)__bfloat16_as_ushort(l0) | ((uint32_t)__bfloat16_as_ushort(l1) << 16);
-        }
-        *(uint4 *)(hi + row * 64 + col0 + c) = make_uint4(ph[0], ph[1], ph[2], ph[3]);
-        *(uint4 *)(lo + row * 64 + col0 + c) = make_uint4(pl[0], pl[1], pl[2], pl[3]);
+    for (int c = 0; c < CH; ++c) {
+        const int pc = c ^ (lane & (CH - 1));
+        *(uint4 *)(stg + lane * (2 * H * 4) + pc * 16) =
+            make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
     }
+    __syncwarp();
+    constexpr int LPR = H / 2;  // lanes per half-row, 2 values each
+    void *dst = lane / LPR ? outB : outA;
+    if (lane < 2 * LPR && dst) {
+        const int half = lane / LPR, li = lane % LPR, col = half * H + 2 * li;
+#pragma unroll 4
+        for (int r = 0; r < 32; ++r) {
+            if (row0 + r >= rows) break;
+            const int pc = (col / 4) ^ (r & (CH - 1));
+            const float2 f = *(const float2 *)(stg + r * (2 * H * 4) + pc * 16 + (col % 4) * 4);
+            const int64_t o = (row0 + r) * H + 2 * li;
+            if (F64) *(double2 *)((double *)dst + o) = make_double2(f.x, f.y);
+            else *(float2 *)((float *)dst + o) = f;
+        }
+    }
+    __syncwarp();
 }
 
 template <int H>
-__global__ void __launch_bounds__(kTcThreads, 1)
+__global__ void __launch_bounds__(kTcThreadsG, 1)
 tc_node_kernel(const __grid_constant__ CUtensorMap mx_hi0, const __grid_constant__ CUtensorMap mx_lo0,
                const __grid_constant__ CUtensorMap mx_hi1, const __grid_constant__ CUtensorMap mx_lo1,
                DevPolicy P, int k, int last) {
     static_assert(H == 16 || H == 32, "tensor-core encoder: hidden 16 or 32");
     using L = TcSmem<H>;
+    constexpr int NG = kTcGroups;
     extern __shared__ __align__(1024) uint8_t tc_smem_raw[];
-    uint8_t *sm = (uint8_t *)(((uintptr_t)tc_smem_raw + 1023) & ~(uintptr_t)1023);
-    uint8_t *xs = sm;                      // [stage][hi/lo] tiles
-    uint8_t *a2h = sm + L::kX, *a2l = a2h + kTcTileBytes;
-    uint8_t *b1h = a2h + L::kA2, *b1l = b1h + H * 128;
+    // 1024-byte aligned by offset arithmetic on the shared array, so the
+    // compiler keeps the shared state space (STS, not generic stores)
+    uint8_t *sm = tc_smem_raw + ((1024u - (tc::smem_u32(tc_smem_raw) & 1023u)) & 1023u);
+    uint8_t *xs = sm;                       // [stage][hi/lo] tiles
+    uint8_t *a2 = sm + L::kX;               // [group][hi/lo] tiles
+    uint8_t *b1h = a2 + NG * L::kA2, *b1l = b1h + H * 128;
     uint8_t *b2h = b1h + L::kB1, *b2l = b2h + 2 * H * 128;
     __shared__ uint64_t bar_full[kTcStages], bar_empty[kTcStages];
-    __shared__ uint64_t bar_d1, bar_a2, bar_d2, bar_done;
+    __shared__ uint64_t bar_d1[NG], bar_a2[NG], bar_d2[NG], bar_done[NG];
     __shared__ uint32_t tmem_base;
+    __shared__ float bphi_s[H];
+    __shared__ double zs_s[6 * H], zp_s[6 * H];   // z-head weights (5 x H) + bias (last round)
 
     const int e = blockIdx.y;
     const CUtensorMap *mh = e == 0 ? &mx_hi0 : &mx_hi1;
@@ -270,24 +305,35 @@ tc_node_kernel(const __grid_constant__ CUtensorMap mx_hi0, const __grid_constant
             return kk < H ? w1[(H + kk) * H + (n - H)] : 0.0;
         });
     }
+    for (int j = threadIdx.x; j < H; j += blockDim.x) bphi_s[j] = (float)phb[j];
+    if (last) {
+        const double *zsw = P.W(PR_SEL_Z_W), *zsb = P.W(PR_SEL_Z_B);
+        const double *zpw = P.W(PR_PLC_Z_W), *zpb = P.W(PR_PLC_Z_B);
+        for (int j = threadIdx.x; j < 6 * H; j += blockDim.x) {
+            if (feeds_sel) zs_s[j] = j < 5 * H ? zsw[j] : zsb[j - 5 * H];
+            if (feeds_plc) zp_s[j] = j < 5 * H ? zpw[j] : zpb[j - 5 * H];
+        }
+    }
+    // A2 columns no epilogue writes (e.g. [H, 32) at H = 16) must read as 0,
+    // not as stale bits that could be NaN (NaN * 0 weights = NaN)
+    for (int i = threadIdx.x; i < NG * L::kA2 / 16; i += blockDim.x)
+        ((uint4 *)a2)[i] = make_uint4(0u, 0u, 0u, 0u);
     if (threadIdx.x == 0) {
         for (int i = 0; i < kTcStages; ++i) {
             tc::mbar_init(&bar_full[i], 1);
             tc::mbar_init(&bar_empty[i], 1);
         }
-        tc::mbar_init(&bar_d1, 1);
-        tc::mbar_init(&bar_a2, 128);
-        tc::mbar_init(&bar_d2, 1);
-        tc::mbar_init(&bar_done, 128);
+        for (int g = 0; g < NG; ++g) {
+            tc::mbar_init(&bar_d1[g], 1);
+            tc::mbar_init(&bar_a2[g], 128);
+            tc::mbar_init(&bar_d2[g], 1);
+            tc::mbar_init(&bar_done[g], 128);
+        }
         tc::fence_mbar_init();
         tc::tma_prefetch(mh);
         tc::tma_prefetch(ml);
     }
-    // A2 columns no epilogue writes (e.g. [H, 32) at H = 16) must read as 0,
-    // not as stale bits that could be NaN (NaN * 0 weights = NaN)
-    for (int i = threadIdx.x; i < L::kA2 / 16; i += blockDim.x)
-        ((uint4 *)a2h)[i] = make_uint4(0u, 0u, 0u, 0u);
-    if (warp == 1) tc::tmem_alloc<128>(&tmem_base);
+    if (warp == 1) tc::tmem_alloc<128 * NG>(&tmem_base);
     tc::fence_proxy_async_smem();
     tc::tc_fence_before();
     __syncthreads();
@@ -295,162 +341,160 @@ tc_node_kernel(const __grid_constant__ CUtensorMap mx_hi0, const __grid_constant
     const uint32_t tm = tmem_base;
     const int rows = P.rows;
     const int tiles = (rows + kTcRows - 1) / kTcRows;
+    const int my_tiles = blockIdx.x < tiles ? (tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
     if (warp == 0) {
         // ===== TMA producer =====
-        if (lane == 0) {
-            int it = 0;
-            for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+        if (lane == 0)
+            for (int it = 0; it < my_tiles; ++it) {
+                const int t = blockIdx.x + it * gridDim.x;
                 const int s = it % kTcStages;
-                const uint32_t ph = (it / kTcStages) & 1;
-                tc::mbar_wait(&bar_empty[s], ph ^ 1);
+                tc::mbar_wait(&bar_empty[s], ((it / kTcStages) & 1) ^ 1);
                 uint8_t *dh = xs + s * 2 * kTcTileBytes, *dl = dh + kTcTileBytes;
                 tc::mbar_arrive_expect_tx(&bar_full[s], 2 * kTcTileBytes);
                 tc::tma_load_2d(dh, mh, &bar_full[s], 0, t * kTcRows);
                 tc::tma_load_2d(dl, ml, &bar_full[s], 0, t * kTcRows);
             }
-        }
     } else if (warp == 1) {
-        // ===== MMA issuer =====
+        // ===== GEMM1 issuer: U = X . phi into accumulator set it % NG =====
         const uint32_t id1 = tc::idesc_bf16_f32(kTcRows, H);
-        const uint32_t id2 = tc::idesc_bf16_f32(kTcRows, last ? H : 2 * H);
-        int it = 0;
-        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
-            const int s = it % kTcStages;
-            const uint32_t ph = (it / kTcStages) & 1;
-            tc::mbar_wait(&bar_full[s], ph);
-            if (it > 0) tc::mbar_wait(&bar_done, (it - 1) & 1);
+        for (int it = 0; it < my_tiles; ++it) {
+            const int g = it % NG, s = it % kTcStages;
+            tc::mbar_wait(&bar_full[s], (it / kTcStages) & 1);
+            if (it >= NG) tc::mbar_wait(&bar_done[g], ((it / NG) - 1) & 1);
             tc::tc_fence_after();
             if (lane == 0) {
                 const uint8_t *xh = xs + s * 2 * kTcTileBytes, *xl = xh + kTcTileBytes;
-                mma_split(tm, xh, xl, b1h, b1l, kTcK / 16, id1, false);
+                mma_split(tm + 128 * g, xh, xl, b1h, b1l, kTcK / 16, id1, false);
                 tc::mma_commit(&bar_empty[s]);
-                tc::mma_commit(&bar_d1);
+                tc::mma_commit(&bar_d1[g]);
             }
             __syncwarp();
-            tc::mbar_wait(&bar_a2, it & 1);
+        }
+    } else if (warp == 2) {
+        // ===== GEMM2 issuer (a separate thread: its commits track only its
+        // own MMAs, so it never waits behind GEMM1 of later tiles) =====
+        const uint32_t id2 = tc::idesc_bf16_f32(kTcRows, last ? H : 2 * H);
+        for (int it = 0; it < my_tiles; ++it) {
+            const int g = it % NG;
+            tc::mbar_wait(&bar_a2[g], (it / NG) & 1);
             tc::tc_fence_after();
             if (lane == 0) {
+                const uint8_t *ah = a2 + g * L::kA2, *al = ah + kTcTileBytes;
+                const uint32_t d = tm + 128 * g + 64;
                 if (!last) {
-                    mma_split(tm + 64, a2h, a2l, b2h, b2l, H / 16, id2, false);
+                    mma_split(d, ah, al, b2h, b2l, H / 16, id2, false);
                 } else if (feeds_plc) {
                     // A = [H' | zp] . [W1a; W1d] (K 64), G = H' . W1b (K = H)
-                    mma_split(tm + 64, a2h, a2l, b2h, b2l, kTcK / 16, id2, false);
-                    mma_split(tm + 64 + H, a2h, a2l, b2h + H * 128, b2l + H * 128, H / 16, id2,
-                              false);
+                    mma_split(d, ah, al, b2h, b2l, kTcK / 16, id2, false);
+                    mma_split(d + H, ah, al, b2h + H * 128, b2l + H * 128, H / 16, id2, false);
                 }
-                tc::mma_commit(&bar_d2);
+                tc::mma_commit(&bar_d2[g]);
             }
             __syncwarp();
         }
     } else {
-        // ===== epilogue: warps 2..5, TMEM lane quarter warp % 4 =====
+        // ===== epilogue group g: warps 3 + 4g .. 6 + 4g, TMEM lane quarter warp % 4 =====
+        const int g = (warp - 3) >> 2;
         const int q = warp & 3;
         const int rloc = q * 32 + lane;
-        const uint32_t tq = tm + ((uint32_t)(q * 32) << 16);
+        const uint32_t tq = tm + 128 * g + ((uint32_t)(q * 32) << 16);
+        uint8_t *ah = a2 + g * L::kA2, *al = ah + kTcTileBytes;
         const float slope = (float)P.slope;
-        float bphi[H];
-#pragma unroll
-        for (int j = 0; j < H; ++j) bphi[j] = (float)phb[j];
-        int it = 0;
-        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+        const int n = P.n;
+        for (int it = g; it < my_tiles; it += NG) {
+            const int t = blockIdx.x + it * gridDim.x;
+            const uint32_t ph = (it / NG) & 1;
             const int64_t row = (int64_t)t * kTcRows + rloc;
             const bool ok = row < rows;
-            tc::mbar_wait(&bar_d1, it & 1);
+            tc::mbar_wait(&bar_d1[g], ph);
             tc::tc_fence_after();
-            float hv[H];
+            // H' = leaky(U + b): into the A2 tile (GEMM2's A operand) and, not
+            // last, the next round's planes; kept in hv for the last round
+            uint32_t hv[2 * H];
+            {
+                uint32_t d1r[H / 16][16];
 #pragma unroll
-            for (int c = 0; c < H; c += 16) {
-                float v[16];
-                tc::tmem_ld16(tq + c, v);
+                for (int c = 0; c < H; c += 16) tc::tmem_ld16_async(tq + c, d1r[c / 16]);
+                tc::tmem_wait_ld();
 #pragma unroll
-                for (int i = 0; i < 16; ++i) hv[c + i] = leakyf(v[i] + bphi[c + i], slope);
-            }
-            // H' -> next round's planes / H_K (fp64), and the A2 tile
+                for (int c = 0; c < H; c += 16) {
+                    float v[16];
 #pragma unroll
-            for (int c = 0; c < H; c += 16) {
-                float v[16];
-#pragma unroll
-                for (int i = 0; i < 16; ++i) v[i] = hv[c + i];
-                put_row16(a2h, a2l, rloc, c, v);
-                if (ok && !last) put_plane16(P.Xh[e][k + 1], P.Xl[e][k + 1], row, c, v);
-            }
-            if (ok && last) {
-                double *hk = P.H[e][k + 1] + row * H;
-#pragma unroll
-                for (int j = 0; j < H; j += 2) *(double2 *)(hk + j) = make_double2(hv[j], hv[j + 1]);
+                    for (int i = 0; i < 16; ++i) {
+                        v[i] = leakyf(__uint_as_float(d1r[c / 16][i]) + bphi_s[c + i], slope);
+                        hv[c + i] = __float_as_uint(v[i]);
+                    }
+                    if (!last && ok)
+                        put16(ah, al, rloc, c, v, P.Xh[e][k + 1], P.Xl[e][k + 1], row);
+                    else
+                        put16(ah, al, rloc, c, v);
+                }
             }
             if (last) {
-                // z heads on the CUDA cores (K = 5): Zs (SEL), zp -> A2[:, 32:32+H) (PLC)
-                const int n = P.n;
+                // z heads on the CUDA cores (K = 5, weights in shared memory):
+                // zp -> A2[:, 32:32+H) for GEMM2, Zs -> hv[H, 2H) (stored below)
                 double x5[5];
 #pragma unroll
                 for (int i = 0; i < 5; ++i) x5[i] = ok ? P.x[(size_t)(row % n) * 5 + i] : 0.0;
-                if (feeds_sel) {
-                    const double *zw = P.W(PR_SEL_Z_W), *zb = P.W(PR_SEL_Z_B);
-                    for (int j = 0; j < H; j += 2) {
-                        double z0 = zb[j], z1 = zb[j + 1];
-#pragma unroll
-                        for (int i = 0; i < 5; ++i) {
-                            z0 = fma(x5[i], zw[i * H + j], z0);
-                            z1 = fma(x5[i], zw[i * H + j + 1], z1);
-                        }
-                        if (ok) *(double2 *)(P.Zs + row * H + j) = make_double2(z0, z1);
-                    }
-                }
                 if (feeds_plc) {
-                    const double *zw = P.W(PR_PLC_Z_W), *zb = P.W(PR_PLC_Z_B);
 #pragma unroll
                     for (int c = 0; c < H; c += 16) {
                         float v[16];
 #pragma unroll
                         for (int i = 0; i < 16; ++i) {
-                            double z = zb[c + i];
+                            double z = zp_s[5 * H + c + i];
 #pragma unroll
-                            for (int r5 = 0; r5 < 5; ++r5) z = fma(x5[r5], zw[r5 * H + c + i], z);
+                            for (int r5 = 0; r5 < 5; ++r5) z = fma(x5[r5], zp_s[r5 * H + c + i], z);
                             v[i] = (float)z;
                         }
-                        put_row16(a2h, a2l, rloc, 32 + c, v);
+                        put16(ah, al, rloc, 32 + c, v);
+                    }
+                }
+                if (feeds_sel) {
+#pragma unroll
+                    for (int j = 0; j < H; ++j) {
+                        double z = zs_s[5 * H + j];
+#pragma unroll
+                        for (int r5 = 0; r5 < 5; ++r5) z = fma(x5[r5], zs_s[r5 * H + j], z);
+                        hv[H + j] = __float_as_uint((float)z);
                     }
                 }
             }
             tc::fence_proxy_async_smem();
             tc::tc_fence_before();
-            tc::mbar_arrive(&bar_a2);
-            tc::mbar_wait(&bar_d2, it & 1);
+            tc::mbar_arrive(&bar_a2[g]);
+            tc::mbar_wait(&bar_d2[g], ph);
             tc::tc_fence_after();
-            if (!last) {
-                // [P | Q] of round k + 1 (the aggregation adds the bias)
+            // the group's A2 tile is free once GEMM2 has completed: per-warp
+            // staging for the coalesced row stores
+            uint8_t *stg = ah + q * 32 * (2 * H * 4);
+            const int64_t row0 = (int64_t)t * kTcRows + q * 32;
+            if (!last || feeds_plc) {
+                // [P | Q] of round k + 1 (fp32; the aggregation adds the bias), or A | G (fp64)
+                uint32_t d2r[2 * H];
 #pragma unroll
-                for (int c = 0; c < 2 * H; c += 16) {
-                    float v[16];
-                    tc::tmem_ld16(tq + 64 + c, v);
-                    if (ok) {
-                        double *dst = c < H ? P.Pm[e][k + 1] + row * H + c
-                                            : P.Qm[e][k + 1] + row * H + (c - H);
-#pragma unroll
-                        for (int i = 0; i < 16; i += 2) *(double2 *)(dst + i) = make_double2(v[i], v[i + 1]);
-                    }
-                }
-            } else if (feeds_plc) {
-#pragma unroll
-                for (int c = 0; c < 2 * H; c += 16) {
-                    float v[16];
-                    tc::tmem_ld16(tq + 64 + c, v);
-                    if (ok) {
-                        double *dst = c < H ? P.A + row * H + c : P.G + row * H + (c - H);
-#pragma unroll
-                        for (int i = 0; i < 16; i += 2) *(double2 *)(dst + i) = make_double2(v[i], v[i + 1]);
-                    }
-                }
+                for (int c = 0; c < 2 * H; c += 16)
+                    tc::tmem_ld16_async(tq + 64 + c, *(uint32_t(*)[16])(d2r + c));
+                tc::tmem_wait_ld();
+                if (!last)
+                    warp_store_rows<H, false>(stg, lane, d2r, row0, rows, P.Pm[e][k + 1],
+                                              P.Qm[e][k + 1]);
+                else
+                    warp_store_rows<H, true>(stg, lane, d2r, row0, rows, P.A, P.G);
+            }
+            if (last) {
+                // H_K (fp64, read by the SEL path sums / PLC steps) and Zs
+                warp_store_rows<H, true>(stg, lane, hv, row0, rows, P.H[e][k + 1],
+                                         feeds_sel ? P.Zs : nullptr);
             }
             tc::tc_fence_before();
-            tc::mbar_arrive(&bar_done);
+            tc::mbar_arrive(&bar_done[g]);
         }
     }
     tc::tc_fence_before();
     __syncthreads();
-    if (warp == 1) tc::tmem_free<128>(tm);
+    if (warp == 1) tc::tmem_free<128 * NG>(tm);
 }
 
 template <int H>
@@ -470,7 +514,7 @@ static int tc_node_launch_t(const DevPolicy &P, int k, bool last, cudaStream_t s
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int tiles = (P.rows + kTcRows - 1) / kTcRows;
     const int gx = std::max(1, std::min(tiles, sms / P.n_enc));
-    tc_node_kernel<H><<<dim3(gx, P.n_enc), kTcThreads, smem, st>>>(m[0][0], m[0][1], m[1][0],
+    tc_node_kernel<H><<<dim3(gx, P.n_enc), kTcThreadsG, smem, st>>>(m[0][0], m[0][1], m[1][0],
                                                                     m[1][1], P, k, (int)last);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FP_ERR_CUDA; }

@@ -22,6 +22,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=1000000)
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--shuffle", action="store_true", help="random vertex ids (no gather locality)")
+ap.add_argument("--encoder", default="dmma", choices=("dmma", "tc", "fused"))
 a = ap.parse_args()
 t0 = time.perf_counter()
 g = builders.sparse_dag(a.n, seed=0)
@@ -30,6 +31,7 @@ if a.shuffle:
 cl = ClusterSpec.uniform(8, rate=1e9, bandwidth=1e7)
 pc = PolicyConfig()
 ctx = PolicyContext(g, cl, pc)
+ctx.set_encoder(a.encoder)
 flat = ctx.flat_params(init_policy_params(pc, seed=0))
 setup = time.perf_counter() - t0
 ctx.prepare(flat)
@@ -42,5 +44,5 @@ for _ in range(a.reps):
     ev[1].record()
     torch.cuda.synchronize()
     ms.append(ev[0].elapsed_time(ev[1]))
-print(json.dumps({"n": a.n, "edges": len(g.edges), "shuffle": a.shuffle, "prepare_ms_min": min(ms),
+print(json.dumps({"n": a.n, "edges": len(g.edges), "shuffle": a.shuffle, "encoder": a.encoder, "prepare_ms_min": min(ms),
                   "prepare_ms": ms, "host_setup_s": setup}))
