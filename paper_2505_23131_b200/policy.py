@@ -276,12 +276,14 @@ class PolicyContext:
 
     ENCODERS = {"dmma": 0, "fused": 1, "tc": 2}
 
-    def set_encoder(self, mode):
+    def set_encoder(self, mode=None, *, fused: bool | None = None):
         """Encoder implementation: ``"dmma"`` (default: aggregation kernels +
         fp64 tensor-core node MLPs, 1e-11 of the reference), ``"fused"`` (one
         per-vertex kernel in the reference's FMA order) or ``"tc"`` (bf16
         node MLPs on tcgen05 fed by TMA, split-bf16 operands, ~1e-5 relative;
         forward only).  A bool selects fused (True) / dmma (False)."""
+        if fused is not None:
+            mode = bool(fused)
         if isinstance(mode, bool):
             mode = "fused" if mode else "dmma"
         if mode not in self.ENCODERS:
