@@ -31,11 +31,22 @@ static __device__ unsigned long long g_phase_count[64];
                     atomicAdd(&g_phase_count[(base) + i_], (unsigned long long)fp_cnt_[i_]); \
                 }                                                               \
     } while (0)
+// milestone of an episode (slots 40..47): cycles since the block started
+#define FP_MARK(id, t0)                                                        \
+    do {                                                                       \
+        if ((threadIdx.x & 31) == 0) {                                         \
+            atomicAdd(&g_phase_cycles[id], (unsigned long long)(clock64() - (t0))); \
+            atomicAdd(&g_phase_count[id], 1ull);                               \
+        }                                                                      \
+    } while (0)
+#define FP_T0_DECL(var) const long long var = clock64()
 #else
 #define FP_PHASE_DECL
 #define FP_PHASE_BEGIN(var)
 #define FP_PHASE_END(var, id)
 #define FP_PHASE_FLUSH(base)
+#define FP_MARK(id, t0)
+#define FP_T0_DECL(var)
 #endif
 
 namespace fp {

@@ -1002,6 +1002,7 @@ rollout_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
     // PLC warp by (slot & 1) == ((slot >> 2) & 1) spreads them over all four;
     // any other slot pattern falls back to warp 1 (both warps decide alike).
     __shared__ unsigned hw_slot[2 * EPB];
+    FP_T0_DECL(t0_);
     const bool is_plc = plc_role(hw_slot, warp);
     const int ep = blockIdx.x * EPB + slot;
     const int n = PR.n;
@@ -1026,6 +1027,7 @@ rollout_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
         // SEL warp: the vertex order, then -- while the PLC warp is still
         // placing -- the simulation, chasing the placement frontier
         const bool ok = sel_chain<GRAD, LEAN>(PR, PO, A, base, L, s_sm, ep, want_lp, want_amax);
+        FP_MARK(40, t0_);
         if (ok && A.simulate) {
             const volatile int *order = (const volatile int *)(base + L.order);
             int *pos = (int *)(base + L.clist);     // SEL scratch, free now
@@ -1055,6 +1057,7 @@ rollout_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
                 (!LEAN && A.trace) ? A.trace + (size_t)ep * A.trace_cap : nullptr, A.trace_cap,
                 nullptr,
                 SimSync{flag, flag + 1, maxsucc, iw});
+            FP_MARK(42, t0_);
             if (lane == 0) {
                 simres[0] = o.makespan;
                 ((int *)simres)[2] = o.status;
@@ -1064,6 +1067,7 @@ rollout_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
     } else {
         status = plc_chain<MAXD, HPL, GRAD, false, LEAN>(PR, PO, A, base, base, L, ep, want_lp,
                                                          want_amax);
+        FP_MARK(41, t0_);
         if (status != FP_EP_OK && lane == 0) flag[1] = 1;  // release a waiting simulator
         const uint8_t *dev = base + L.assign;
 #pragma unroll 1

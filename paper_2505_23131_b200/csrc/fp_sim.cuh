@@ -104,9 +104,13 @@ struct SimSync {
 __device__ __forceinline__ bool sim_wait_placed(const SimSync &S, int need) {
     int ok = 1;
     if (need >= 0 && lane_id() == 0) {
+        // back off (a PLC step is ~1-3 us): the spin's loads and branches
+        // would otherwise take issue slots from the placing warps
+        unsigned ns = 64;
         while (*S.placed <= need) {
             if (*S.abort) { ok = 0; break; }
-            __nanosleep(32);  // leave the issue slots to the placing warps
+            __nanosleep(ns);
+            ns = min(ns * 2u, 512u);
         }
         __threadfence_block();  // acquire: the devices written before the counter
     }
@@ -333,6 +337,7 @@ __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *nb, 
             }
             need = __reduce_max_sync(FP_FULL_MASK, need);
             if (!sim_wait_placed(sync, need)) return SimOut{0.0, FP_EP_BAD_ACTION, 0};
+            FP_PHASE_END(pq_, 22);
         }
         int done_exec = 0;
 #pragma unroll

@@ -24,7 +24,8 @@ from paper_2505_23131_b200.policy import PolicyConfig, PolicyContext  # noqa: E4
 NAMES = {0: "sel.compact", 1: "sel.softmax", 2: "sel.decide+publish", 3: "sel.lp/ent",
          4: "sel.cand-update", 5: "sel.tree-decide", 6: "sel.publish+lp", 7: "sel.tree-update", 10: "plc.wait-order", 11: "plc.features", 12: "plc.stats+xn",
          13: "plc.preact+reduce", 14: "plc.softmax", 15: "plc.decide", 16: "plc.lp/grad",
-         17: "plc.commit", 21: "sim.start", 23: "sim.tmin", 24: "sim.complete"}
+         17: "plc.commit", 21: "sim.start", 22: "sim.wait-placed", 23: "sim.tmin", 24: "sim.complete"}
+MARKS = {40: "SEL chain done", 41: "PLC chain done", 42: "simulation done"}
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="ffnn")
@@ -68,3 +69,6 @@ for i in sorted(NAMES):
         print(f"  {NAMES[i]:22s} {per:8.1f} cyc/call  calls/episode {cnt[i] / a.batch:7.1f}"
               f"  total/episode {cyc[i] / a.batch:10.0f}")
 print("  per-episode cycles:", {k: int(v) for k, v in tot.items()})
+for i, name in MARKS.items():
+    if cnt[i]:
+        print(f"  milestone {name:18s} {cyc[i] / cnt[i]:10.0f} cycles after the block start")
