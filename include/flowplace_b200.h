@@ -223,7 +223,8 @@ typedef struct fp_rollout_args {
     int32_t *step_ncand;     /* [B][n] out or NULL: candidate-set size */
     double *makespan;        /* [B] out (simulate = 1) */
     int32_t *status;         /* [B] out: FP_EP_* */
-    double *grad_rows;       /* [B][n][4][hidden] out or NULL: REINFORCE rows */
+    double *grad_rows;       /* [B][n][fp_grad_rec_stride] out or NULL: REINFORCE
+                                decision records (consumed by fp_pg_reduce) */
     double *grad_ep;         /* [B][fp_grad_ep_stride] out (with grad_rows) */
     fp_event *trace;         /* optional simulator trace [B][trace_cap] */
     int32_t trace_cap;
@@ -250,20 +251,24 @@ int fp_policy_table(const fp_policy *pol, int32_t which, const double **ptr, int
 /* Device workspace fp_rollout_batch needs for B episodes (0 on the compact
  * shared-memory path; graphs beyond it run the wide path, whose per-episode
  * n-sized state lives in this caller-owned HBM scratch).  grad = 1 for a
- * rollout that writes REINFORCE rows (compact path only): its per-decision
- * records (B*n*(56*d + 8) + 4*B bytes) also live in the workspace. */
+ * REINFORCE rollout (compact path only; its per-decision records go to
+ * grad_rows, not the workspace). */
 int fp_rollout_workspace_size(const fp_problem *p, const fp_policy *pol, int32_t B,
                               int32_t flags, int32_t grad, int64_t *bytes);
 /* Batched SEL/PLC episodes (+ fused WC simulation) — one warp per episode. */
 int fp_rollout_batch(const fp_problem *p, const fp_policy *pol, const fp_rollout_args *args,
                      void *stream);
 int fp_grad_ep_stride(const fp_policy *pol, int32_t d, int64_t *stride);
+/* doubles per (episode, step) REINFORCE decision record in grad_rows:
+ * normalised device features [5d], PLC logits [d], (vertex, device) int2 */
+int fp_grad_rec_stride(const fp_policy *pol, int32_t d, int64_t *stride);
 
 /* ------------------------------------------------------------------------
  * Stage-II update (flowplace/training.py:181-216, nn.py:184-277).
- * fp_pg_reduce contracts the rollout's REINFORCE rows with per-episode
- * coefficients alpha[e] (= -advantage_e / B_global for Stage II, -1/B for
- * imitation) and beta (= -entropy_weight / B_global), deterministically;
+ * fp_pg_reduce replays the rollout's REINFORCE decision records with
+ * per-episode coefficients alpha[e] (= -advantage_e / B_global for Stage II,
+ * -1/B for imitation) and beta (= -entropy_weight / B_global) folded in, and
+ * reduces the episodes deterministically (fixed order, no atomics);
  * fp_policy_backward turns the reduced tables into the flat parameter
  * gradient (same layout as the params); fp_sgd_step applies
  * params -= lr * grad (nn.py:271-277).
@@ -273,6 +278,11 @@ int fp_pg_reduce(fp_policy *pol, const double *grad_rows, const double *grad_ep,
                  void *stream);
 int fp_policy_backward(fp_policy *pol, double *grad, void *stream);
 int fp_sgd_step(double *params, const double *grad, int64_t count, double lr, void *stream);
+/* as fp_sgd_step, skipped on the device when *skip != 0 (skip: device int32,
+ * e.g. a sticky "some rollout of this batch failed" flag), so a trainer can
+ * keep the step free of host synchronisation and raise afterwards */
+int fp_sgd_step_masked(double *params, const double *grad, int64_t count, double lr,
+                       const int32_t *skip, void *stream);
 
 /* Tensor-core (tcgen05 + TMA) path self test: out[M][N] (fp32) = X . W with
  * X [M][64] given as bf16 hi / lo planes (device, row pitch 128 bytes) and W

@@ -59,8 +59,6 @@ def lib() -> ctypes.CDLL:
                 " (or __graft_entry__.build()). There is no CPU fallback.")
         _lib = ctypes.CDLL(str(path))
         _lib.fp_last_error.restype = ctypes.c_char_p
-        for name in dir(_lib):
-            pass
     return _lib
 
 
@@ -131,6 +129,7 @@ class FpRolloutArgs(ctypes.Structure):
 
 EXPORTED = EXPORTED + (
     "fp_policy_create", "fp_policy_destroy", "fp_policy_set_encoder", "fp_policy_prepare", "fp_policy_table",
-    "fp_rollout_workspace_size", "fp_rollout_batch", "fp_grad_ep_stride", "fp_pg_reduce", "fp_policy_backward", "fp_sgd_step",
+    "fp_rollout_workspace_size", "fp_rollout_batch", "fp_grad_ep_stride", "fp_grad_rec_stride",
+    "fp_pg_reduce", "fp_policy_backward", "fp_sgd_step", "fp_sgd_step_masked",
     "fp_tc_gemm_selftest",
 )

@@ -745,8 +745,6 @@ int fp_policy_create(const fp_problem *p, const fp_policy_desc *desc, fp_policy 
            o_De = take(nh), o_dhid = take(nh), o_demb = take(nh * 4), o_dZ = take(nh * 2),
            o_ds = take((size_t)n * 8), o_dA = take(nh), o_dG = take(nh),
            o_dsm = take((size_t)(16 * h + 64) * 8);
-    const int prow = 16;  // episode chunks of the deterministic reduction
-    size_t o_part = take((size_t)prow * ((size_t)std::max(n, 1) * (2 * h + 1) + 16 * h + 64) * 8);
 
     fp_policy *pol = new fp_policy();
     pol->problem = p;
@@ -830,7 +828,7 @@ int fp_policy_create(const fp_problem *p, const fp_policy_desc *desc, fp_policy 
     P.dhid = (double *)(b + o_dhid); P.demb = (double *)(b + o_demb); P.dZ = (double *)(b + o_dZ);
     P.ds = (double *)(b + o_ds); P.dA = (double *)(b + o_dA);
     P.dG = (double *)(b + o_dG); P.dsmall = (double *)(b + o_dsm);
-    P.partial = (double *)(b + o_part); P.partial_rows = prow;
+
     *out = pol;
     return FP_OK;
 }

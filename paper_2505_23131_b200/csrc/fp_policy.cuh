@@ -76,8 +76,6 @@ struct DevPolicy {
     double *dH[2], *dHn[2], *dU, *Dsrc, *Ddst, *dagg, *De;
     double *dhid, *demb, *dZ;      // SEL head / z backward rows
     double *ds, *dA, *dG, *dsmall; // reduced gradient tables
-    double *partial;               // episode-chunk partials of the reduction
-    int partial_rows;
     // bf16 tensor-core encoder (fp_tc_node.cu): round inputs X_k = [H_k | agg_k]
     // as split bf16 planes (hi, lo), [rows][64], H_k at columns [0, dk),
     // agg_k at [32, 32 + h); zero elsewhere

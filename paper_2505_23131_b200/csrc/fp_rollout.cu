@@ -14,7 +14,10 @@ namespace fp {
                                                         const fp_rollout_args &, cudaStream_t);  \
     extern template int launch_rollout_wide<MAXD, HPL>(const fp_problem *, const fp_policy *,    \
                                                        const fp_rollout_args &, int64_t *,       \
-                                                       cudaStream_t);
+                                                       cudaStream_t);                            \
+    extern template int launch_plc_replay<MAXD, HPL>(                                            \
+        const fp_problem *, const fp_policy *, const double *, const double *, const int32_t *, \
+        const double *, double, int, double *, int64_t *, cudaStream_t);
 FP_ROLLOUT_CONFIGS(FP_DECL)
 #undef FP_DECL
 
@@ -53,11 +56,31 @@ static int dispatch_grad(const fp_problem *p, const fp_policy *pol, const fp_rol
         return launch_rollout_wide<MAXD, HPL>(p, pol, a, ws_needed, st);
     }
     if (ws_needed) {
-        *ws_needed = grad ? grad_rec_bytes(a.B, p->dev.n, p->dev.d) : 0;
+        *ws_needed = 0;  // REINFORCE records live in grad_rows
         return FP_OK;
     }
     return grad ? launch_rollout<MAXD, HPL, true>(p, pol, a, st)
                 : launch_rollout<MAXD, HPL, false>(p, pol, a, st);
+}
+
+// Stage-II replay of the PLC decision records + deterministic episode
+// reduction (fp_pg_reduce); scratch_bytes != NULL: size query only.
+int plc_replay(const fp_problem *p, const fp_policy *pol, const double *rec, const double *gep,
+               const int32_t *assign, const double *alpha, double beta, int B, double *scratch,
+               int64_t *scratch_bytes, cudaStream_t st) {
+    const int D = p->dev.d, h = pol->dev.h;
+#define FP_RP(MD, HP) \
+    return launch_plc_replay<MD, HP>(p, pol, rec, gep, assign, alpha, beta, B, scratch, scratch_bytes, st)
+    if (h <= 32) {
+        if (D <= 4) FP_RP(4, 1);
+        if (D <= 8) FP_RP(8, 1);
+        if (D <= 16) FP_RP(16, 1);
+        FP_RP(32, 1);
+    }
+    if (D <= 8) FP_RP(8, 2);
+    if (D <= 16) FP_RP(16, 2);
+    FP_RP(32, 2);
+#undef FP_RP
 }
 
 int per_step_rollout(const fp_problem *p, const fp_policy *pol, const fp_rollout_args &a,
@@ -89,6 +112,12 @@ extern "C" {
 int fp_grad_ep_stride(const fp_policy *pol, int32_t d, int64_t *stride) {
     if (!pol || !stride) { set_error("null argument"); return FP_ERR_INVALID; }
     *stride = grad_ep_stride(pol->dev.n, pol->dev.h, d);
+    return FP_OK;
+}
+
+int fp_grad_rec_stride(const fp_policy *pol, int32_t d, int64_t *stride) {
+    if (!pol || !stride) { set_error("null argument"); return FP_ERR_INVALID; }
+    *stride = grad_rec_stride(d, (pol->dev.n + 31) / 32);
     return FP_OK;
 }
 

@@ -51,14 +51,15 @@ __host__ __device__ inline int64_t grad_ep_stride(int n, int h, int d) {
     return ((2LL * n + 12LL * h + 2 + 2LL * d * h) + 3) / 4 * 4;
 }
 
-// REINFORCE decision records (compact GRAD rollouts): per (episode, step) the
-// normalised device features xn[5d] and the head-2 adjoints gl[d], ge[d]
-// (7d doubles), then per (episode, step) the (vertex, device) pair, then a
-// per-episode "PLC chain completed" flag.  The PLC warp only records; the
-// gradient arithmetic runs afterwards in plc_grad_kernel, off the chain.
-__host__ __device__ inline int64_t grad_rec_bytes(int B, int n, int d) {
-    return (int64_t)B * n * 7 * d * 8 + (int64_t)B * n * 8 + (int64_t)B * 4;
-}
+// REINFORCE decision records (compact GRAD rollouts), in the caller's
+// grad_rows buffer, grad_rec_stride(d, W) doubles per (episode, step): the
+// PLC warp's normalised device features xn[5d], logits[d] and (vertex,
+// device) int2; the SEL warp's softmax max and normaliser over the
+// candidates, the chosen vertex and the candidate bitset (W words).  The PLC warp also writes
+// grad_ep[2n] = chain completed, [2n + 1] = epsilon.  fp_pg_reduce replays
+// the records (plc_replay_kernel) -- the log-prob / entropy adjoints never
+// run on the rollout's decision chains.
+__host__ __device__ inline int grad_rec_stride(int d, int W) { return 6 * d + 4 + (W + 1) / 2; }
 
 template <int MAXD>
 struct PlcLog {  // log2(MAXD)
@@ -81,8 +82,6 @@ __device__ __forceinline__ bool sel_chain(const DevProblem &PR, const DevPolicy 
     int *clist = (int *)(base + L.clist);
     double *ce = (double *)(base + L.ce);
     double *cc = (double *)(base + L.cc);
-    double *dsl = (double *)(base + L.dsl);
-    double *dse = (double *)(base + L.dse);
     volatile int *order = (volatile int *)(base + L.order);
     const double eps = A.epsilon, ome = 1.0 - eps;
     const uint32_t k0 = (uint32_t)A.seed, k1 = (uint32_t)(A.seed >> 32);
@@ -100,7 +99,6 @@ __device__ __forceinline__ bool sel_chain(const DevProblem &PR, const DevPolicy 
     for (int v = lane; v < n; v += 32) {
         const int np = pp[v + 1] - pp[v];
         npl[v] = np;
-        if constexpr (GRAD) { dsl[v] = 0.0; dse[v] = 0.0; }
         if (np == 0) atomicOr(&cand[v >> 5], 1u << (v & 31));
     }
     __syncwarp();
@@ -135,12 +133,13 @@ __device__ __forceinline__ bool sel_chain(const DevProblem &PR, const DevPolicy 
         FP_PHASE_END(ps, 0);
         const bool fast = k <= 32;  // candidate i on lane i, values in registers
         int idx = -1;
-        double e0 = 0.0, cum0 = 0.0, tot;
+        double e0 = 0.0, cum0 = 0.0, tot, mxr;
         int myv = -1;
         if (fast) {
             myv = lane < k ? clist[lane] : -1;
             const double sv = lane < k ? s_sm[myv] : -INFINITY;
             const double mx = warp_max_redux(sv);
+            mxr = mx;
             e0 = lane < k ? exp(sv - mx) : 0.0;
             cum0 = warp_inclusive_scan(e0);
             tot = __shfl_sync(FP_FULL_MASK, cum0, 31);
@@ -179,6 +178,7 @@ __device__ __forceinline__ bool sel_chain(const DevProblem &PR, const DevPolicy 
                 carry = __shfl_sync(FP_FULL_MASK, cum, 31);
             }
             tot = carry;
+            mxr = mx;
             __syncwarp();
             if (mode == FP_MODE_FORCED) {
                 const int fv = frow[2 * step];
@@ -243,31 +243,26 @@ __device__ __forceinline__ bool sel_chain(const DevProblem &PR, const DevPolicy 
         // publish early: the PLC warp only needs the vertex (a single 32-bit
         // store replacing the -3 sentinel is the whole hand-off)
         if (lane == 0) order[step] = v;
+        if constexpr (GRAD) {  // SEL part of the decision record (replayed by fp_pg_reduce)
+            double *rec = A.grad_rows + ((size_t)ep * n + step) * grad_rec_stride(PR.d, W) +
+                          6 * PR.d + 1;
+            if (lane == 0) { rec[0] = mxr; rec[1] = tot; rec[2] = (double)v; }
+            if (lane < W) ((uint32_t *)(rec + 3))[lane] = cw;
+        }
         FP_PHASE_END(ps, 2);
         if (want_lp && fast) {
             // candidate i on lane i: p, mix, log(mix) once per lane; the
             // chosen candidate's terms by shuffle (the sums below are the
             // slow path's, same reduction tree)
             const double ek = eps / (double)k;
-            double p = 0.0, mix = 0.0, lm = 0.0, q = 0.0;
+            double p = 0.0, mix = 0.0, lm = 0.0;
             if (lane < k) {
                 p = e0 / tot;
                 mix = __dadd_rn(__dmul_rn(p, ome), ek);
                 lm = log(__dadd_rn(mix, 1e-30));
-                if constexpr (GRAD) q = -ome * (lm + mix / __dadd_rn(mix, 1e-30));
             }
             const double ent = -warp_sum(lane < k ? mix * lm : 0.0);
             const double lp = __shfl_sync(FP_FULL_MASK, lm, idx);
-            if constexpr (GRAD) {
-                const double pidx = __shfl_sync(FP_FULL_MASK, p, idx);
-                const double midx = __shfl_sync(FP_FULL_MASK, mix, idx);
-                const double qp = warp_sum(lane < k ? q * p : 0.0);
-                const double c1 = ome * pidx / __dadd_rn(midx, 1e-30);
-                if (lane < k) {
-                    dsl[myv] += c1 * ((lane == idx ? 1.0 : 0.0) - p);
-                    dse[myv] += p * (q - qp);
-                }
-            }
             if (lane == 0) {
                 const size_t o = (size_t)ep * n + step;
                 if (A.step_lp) A.step_lp[2 * o] = lp;
@@ -275,32 +270,16 @@ __device__ __forceinline__ bool sel_chain(const DevProblem &PR, const DevPolicy 
             }
         } else if (want_lp) {
             const double ek = eps / (double)k;
-            double entp = 0.0, lp = 0.0, pidx = 0.0, midx = 0.0, qp = 0.0;
+            double entp = 0.0, lp = 0.0;
             for (int i = lane; i < k; i += 32) {
                 const double p = (fast ? e0 : ce[i]) / tot;
                 const double mix = __dadd_rn(__dmul_rn(p, ome), ek);
                 const double lm = log(__dadd_rn(mix, 1e-30));
                 entp += mix * lm;
-                if (i == idx) { lp = lm; pidx = p; midx = mix; }
-                if constexpr (GRAD) qp += -ome * (lm + mix / __dadd_rn(mix, 1e-30)) * p;
+                if (i == idx) lp = lm;
             }
             const double ent = -warp_sum(entp);
             lp = warp_sum(lp);  // exactly one lane non-zero
-            if constexpr (GRAD) {
-                pidx = warp_sum(pidx);
-                midx = warp_sum(midx);
-                qp = warp_sum(qp);
-                const double c1 = ome * pidx / __dadd_rn(midx, 1e-30);
-                for (int i = lane; i < k; i += 32) {
-                    const double p = (fast ? e0 : ce[i]) / tot;
-                    const double mix = __dadd_rn(__dmul_rn(p, ome), ek);
-                    const double lm = log(__dadd_rn(mix, 1e-30));
-                    const double q = -ome * (lm + mix / __dadd_rn(mix, 1e-30));
-                    const int u = clist[i];
-                    dsl[u] += c1 * ((i == idx ? 1.0 : 0.0) - p);
-                    dse[u] += p * (q - qp);
-                }
-            }
             if (lane == 0) {
                 const size_t o = (size_t)ep * n + step;
                 if (A.step_lp) A.step_lp[2 * o] = lp;
@@ -325,10 +304,6 @@ __device__ __forceinline__ bool sel_chain(const DevProblem &PR, const DevPolicy 
         FP_PHASE_END(ps, 4);
     }
     FP_PHASE_FLUSH(0);
-    if constexpr (GRAD) {
-        double *g = A.grad_ep + (size_t)ep * grad_ep_stride(n, PO.h, PR.d);
-        for (int v = lane; v < n; v += 32) { g[v] = dsl[v]; g[n + v] = dse[v]; }
-    }
     return true;
 }
 
@@ -691,8 +666,7 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
     const double *__restrict__ tdur = PR.tdur;
     const double *__restrict__ edur = PR.edur;
     const double b2p = PO.W(PR_PLC_H2_B)[0];
-    double *rec_x = GRAD ? (double *)A.workspace : nullptr;  // decision records (GRAD)
-    int2 *rec_vd = GRAD ? (int2 *)(rec_x + (size_t)A.B * n * 7 * D) : nullptr;
+    double *rec_x = GRAD ? A.grad_rows : nullptr;  // decision records (GRAD)
 
 #pragma unroll 1
     for (int v = lane; v < n; v += 32) { tstart[v] = 0.0; tend[v] = 0.0; dev[v] = 0xFF; }
@@ -926,19 +900,12 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
                 if (A.step_lp) A.step_lp[2 * o + 1] = lp;
                 if (A.step_ent) A.step_ent[2 * o + 1] = entv;
             }
-            if constexpr (GRAD) {
-                const double pj = __shfl_sync(FP_FULL_MASK, pd, jdx);
-                const double mj = __shfl_sync(FP_FULL_MASK, mixd, jdx);
-                const double q = lane < D ? -ome * (lmd + mixd / __dadd_rn(mixd, 1e-30)) : 0.0;
-                const double qpd = warp_sum(lane < D ? q * pd : 0.0);
-                const double gl = lane < D ? ome * pj / __dadd_rn(mj, 1e-30) *
-                                                 ((lane == jdx ? 1.0 : 0.0) - pd) : 0.0;
-                const double ge = lane < D ? pd * (q - qpd) : 0.0;
-                double *rec = rec_x + ((size_t)ep * n + step) * (7 * D);
-                for (int i = lane; i < 5 * D; i += 32) rec[i] = xn[i];
-                if (lane < D) { rec[5 * D + lane] = gl; rec[6 * D + lane] = ge; }
-                if (lane == 0) rec_vd[(size_t)ep * n + step] = make_int2(v, jdx);
-            }
+        }
+        if constexpr (GRAD) {  // decision record: the adjoints are formed by fp_pg_reduce
+            double *rec = rec_x + ((size_t)ep * n + step) * grad_rec_stride(D, PR.W);
+            for (int i = lane; i < 5 * D; i += 32) rec[i] = xn[i];
+            if (lane < D) rec[5 * D + lane] = lg;
+            if (lane == 0) *(int2 *)(rec + 6 * D) = make_int2(v, jdx);
         }
         FP_PHASE_END(pp_, 16);
         // ---- commit (timeline.py:47-58) ----
@@ -968,8 +935,96 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
     }
     FP_PHASE_FLUSH(0);
     if constexpr (GRAD)
-        if (lane == 0) ((int *)(rec_vd + (size_t)A.B * n))[ep] = status == FP_EP_OK;
+        if (lane == 0) {
+            double *g = A.grad_ep + (size_t)ep * grad_ep_stride(n, h, D);
+            g[2 * n] = status == FP_EP_OK ? 1.0 : 0.0;
+            g[2 * n + 1] = eps;
+        }
     return status;
+}
+
+// REINFORCE terms of the SEL decisions, off both decision chains: steps
+// [t0, t1) of the recorded SEL decisions, run by a warp that would otherwise
+// wait -- the PLC warp once its chain is done (the first ~70% of the steps)
+// and the SEL warp once the simulation is done (the rest).  Per step the
+// recorded candidate bitset is compacted to the ascending candidate list
+// and, with the recorded softmax max / normaliser, the mixture's log-prob /
+// entropy adjoints w.r.t. the SEL logits (policy.py:186-204, 301-322 in
+// reverse) accumulate into dsl (dlp/ds) and dse (dent/ds) per vertex (lane
+// = candidate, one update per candidate per step, steps in order).
+__device__ __forceinline__ int sel_grad_split(int n) { return (7 * n) / 10; }
+
+__device__ __forceinline__ void sel_grad_terms(const DevProblem &PR, const fp_rollout_args &A,
+                                               const double *s_sm, int ep, int t0, int t1,
+                                               int *cl, double *dsl, double *dse) {
+    const int lane = lane_id();
+    const int n = PR.n, D = PR.d, W = PR.W;
+    const double eps = A.epsilon, ome = 1.0 - eps;
+    const int rstride = grad_rec_stride(D, W);
+    const double *rec = A.grad_rows + (size_t)ep * n * rstride;
+#pragma unroll 1
+    for (int v = lane; v < n; v += 32) { dsl[v] = 0.0; dse[v] = 0.0; }
+    if (t0 >= t1) { __syncwarp(); return; }
+    // step t's record fields, fetched one step ahead
+    auto fetch = [&](int t, int &v, double &mx, double &tot, uint32_t &cw) {
+        const double *r = rec + (size_t)t * rstride;
+        mx = r[6 * D + 1];
+        tot = r[6 * D + 2];
+        v = (int)r[6 * D + 3];
+        cw = lane < W ? ((const uint32_t *)(r + 6 * D + 4))[lane] : 0u;
+    };
+    int v, nv = 0;
+    double mx, tot, nmx = 0.0, ntot = 0.0;
+    uint32_t cw, ncw = 0u;
+    fetch(t0, v, mx, tot, cw);
+    __syncwarp();
+#pragma unroll 1
+    for (int t = t0; t < t1; ++t) {
+        if (t + 1 < t1) fetch(t + 1, nv, nmx, ntot, ncw);
+        const int pc = __popc(cw);
+        const int incl = warp_inclusive_scan(pc);
+        const int k = __shfl_sync(FP_FULL_MASK, incl, 31);
+        {
+            int o = incl - pc;
+            uint32_t m = cw;
+            while (m) {
+                const int b = __ffs(m) - 1;
+                m &= m - 1;
+                cl[o++] = lane * 32 + b;
+            }
+        }
+        __syncwarp();
+        const double ek = eps / (double)k;
+        double p0 = 0.0, q0 = 0.0, acc = 0.0;
+#pragma unroll 1
+        for (int i = lane; i < k; i += 32) {
+            const double p = exp(s_sm[cl[i]] - mx) / tot;
+            const double mix = __dadd_rn(__dmul_rn(p, ome), ek);
+            const double lm = log(__dadd_rn(mix, 1e-30));
+            const double q = -ome * (lm + mix / __dadd_rn(mix, 1e-30));
+            acc += q * p;
+            if (i < 32) { p0 = p; q0 = q; }
+        }
+        const double qp = warp_sum(acc);
+        const double pv = exp(s_sm[v] - mx) / tot;
+        const double mv = __dadd_rn(__dmul_rn(pv, ome), ek);
+        const double c1 = ome * pv / __dadd_rn(mv, 1e-30);
+#pragma unroll 1
+        for (int i = lane; i < k; i += 32) {
+            double p = p0, q = q0;
+            if (i >= 32) {
+                p = exp(s_sm[cl[i]] - mx) / tot;
+                const double mix = __dadd_rn(__dmul_rn(p, ome), ek);
+                const double lm = log(__dadd_rn(mix, 1e-30));
+                q = -ome * (lm + mix / __dadd_rn(mix, 1e-30));
+            }
+            const int u = cl[i];
+            dsl[u] += c1 * ((u == v ? 1.0 : 0.0) - p);
+            dse[u] += p * (q - qp);
+        }
+        __syncwarp();
+        v = nv; mx = nmx; tot = ntot; cw = ncw;
+    }
 }
 
 // Which warp of an episode's (SEL, PLC) pair runs the PLC chain, by hardware
@@ -1019,15 +1074,19 @@ rollout_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
     }
     __syncthreads();
     if (ep >= A.B) return;
-    const bool want_lp = GRAD || (!LEAN && (A.step_lp != nullptr || A.step_ent != nullptr));
+    const bool want_out = !LEAN && (A.step_lp != nullptr || A.step_ent != nullptr);
     const bool want_amax = !LEAN && A.step_argmax != nullptr;
     double *simres = (double *)(base + L.simres);  // makespan, status
     int status = FP_EP_OK;
     if (!is_plc) {
         // SEL warp: the vertex order, then -- while the PLC warp is still
         // placing -- the simulation, chasing the placement frontier
-        const bool ok = sel_chain<GRAD, LEAN>(PR, PO, A, base, L, s_sm, ep, want_lp, want_amax);
+        const bool ok = sel_chain<GRAD, LEAN>(PR, PO, A, base, L, s_sm, ep, want_out, want_amax);
         FP_MARK(40, t0_);
+        if constexpr (GRAD)  // no simulation to chase: the second part of the SEL terms now
+            if (ok && !A.simulate)
+                sel_grad_terms(PR, A, s_sm, ep, sel_grad_split(n), n, (int *)(base + L.clist),
+                               (double *)(base + L.ce), (double *)(base + L.cc));
         if (ok && A.simulate) {
             const volatile int *order = (const volatile int *)(base + L.order);
             int *pos = (int *)(base + L.clist);     // SEL scratch, free now
@@ -1058,6 +1117,11 @@ rollout_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
                 nullptr,
                 SimSync{flag, flag + 1, maxsucc, iw});
             FP_MARK(42, t0_);
+            // second part of the SEL terms (SEL / simulator scratch, free now)
+            if constexpr (GRAD)
+                if (o.status == FP_EP_OK && !flag[1])
+                    sel_grad_terms(PR, A, s_sm, ep, sel_grad_split(n), n, (int *)(base + L.clist),
+                                   (double *)(base + L.ce), (double *)(base + L.cc));
             if (lane == 0) {
                 simres[0] = o.makespan;
                 ((int *)simres)[2] = o.status;
@@ -1065,16 +1129,32 @@ rollout_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
             }
         }
     } else {
-        status = plc_chain<MAXD, HPL, GRAD, false, LEAN>(PR, PO, A, base, base, L, ep, want_lp,
+        status = plc_chain<MAXD, HPL, GRAD, false, LEAN>(PR, PO, A, base, base, L, ep, want_out,
                                                          want_amax);
         FP_MARK(41, t0_);
         if (status != FP_EP_OK && lane == 0) flag[1] = 1;  // release a waiting simulator
+        if constexpr (GRAD)  // first part of the SEL terms (cons: unused by the overlapped sim)
+            if (status == FP_EP_OK)
+                sel_grad_terms(PR, A, s_sm, ep, 0, sel_grad_split(n), (int *)(base + L.cons),
+                               (double *)(base + L.dsl), (double *)(base + L.dse));
         const uint8_t *dev = base + L.assign;
 #pragma unroll 1
         for (int v = lane; v < n; v += 32)
             A.assign[(size_t)ep * n + v] = dev[v] == 0xFF ? -1 : dev[v];
     }
     __syncthreads();
+    if constexpr (GRAD)
+        if (is_plc && status == FP_EP_OK &&
+            (!A.simulate || ((const int *)simres)[2] == FP_EP_OK)) {  // the two parts of the SEL terms
+            const double *dsl = (const double *)(base + L.dsl), *dse = (const double *)(base + L.dse);
+            const double *dsl2 = (const double *)(base + L.ce), *dse2 = (const double *)(base + L.cc);
+            double *g = A.grad_ep + (size_t)ep * grad_ep_stride(n, PO.h, PR.d);
+#pragma unroll 1
+            for (int u = lane; u < n; u += 32) {
+                g[u] = dsl[u] + dsl2[u];
+                g[n + u] = dse[u] + dse2[u];
+            }
+        }
     if (is_plc && lane == 0) {
         double mk = 0.0;
         if (status == FP_EP_OK && A.simulate) {
@@ -1086,47 +1166,112 @@ rollout_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
     }
 }
 
-// Deferred REINFORCE pass of the PLC head: the PLC warp records each
-// decision (xn, gl, ge, v, jdx) and this kernel -- off the latency-bound
-// placement chain, one warp per episode -- walks the records in placement
-// order with the PLC's arithmetic: it rebuilds the per-device sums S_d and the
-// pre-activations from (A, G, M, c) and xn, and produces the per-vertex rows
-// (d logit / d S-row terms, running per-device sums at placement) and the
-// per-episode sums (dM, dw2, db2, total per-device sums) that fp_pg_reduce and
-// the backward consume.  The next step's record, vertex rows and (vertex,
-// device) pair are fetched while the current step is reduced (measured: a
-// block of 4 warps per episode splitting the devices, with one barrier per
-// step, was slower -- 500 vs 302 us at Llama-layer x 1024).
-constexpr int kGradWarps = 4;
+// Stage-II REINFORCE replay (fp_pg_reduce), off the rollout's latency-bound
+// decision chains: the rollout only records each PLC decision (normalised
+// device features, logits, vertex / device; grad_rec_stride), and its idle
+// warps fold the SEL decisions' terms into grad_ep (sel_grad_terms).
+// plc_replay_kernel, one CTA of kChunkWarps warps per episode:
+//   1. the placement order from the records (thread = step);
+//   2. PLC adjoints (thread = step): the device softmax of the recorded
+//      logits, the sampled mixture's log-prob / entropy adjoints
+//      (policy.py:301-322 in reverse), folded with the episode's
+//      coefficients: c_d = alpha_e dlp/dlogit_d + beta dent/dlogit_d;
+//   3. PLC rows (warp = chunk of consecutive steps, lane = hidden column):
+//      each chunk warp rebuilds S_d at its first step (prefix of the placed G
+//      rows, in step order), then replays its steps: pre-activations from
+//      (A, G, M, c) and xn, folded rows (dA row; the chunk-local running
+//      per-device sum at placement, for dG) into a [B][n][2h] slab, and
+//      chunk sums.  The chunk totals give, per chunk, final-sum-minus-
+//      prefix tables, so dG needs no second pass over the episode.
+// pg_rows_kernel contracts the slab over the episodes (a streaming pass,
+// episode chunks in parallel, each in episode order; plus the SEL terms of
+// grad_ep with alpha / beta) and pg_final_kernel sums the chunk partials in
+// chunk order: bitwise deterministic, no atomics.
+constexpr int kChunkWarps = 2;
+constexpr int kPgChunks = 16;
+
+__host__ __device__ inline int64_t pg_part_stride(int n, int h) {
+    return 2LL * n * h + 6LL * h + 1 + n;  // dA | dG | dM dw2 db2 | ds
+}
 
 template <int MAXD, int HPL>
-__global__ void __launch_bounds__(kGradWarps * 32)
-plc_grad_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A) {
-    __shared__ double stage[kGradWarps][2][7 * MAXD];
+__global__ void __launch_bounds__(kChunkWarps * 32)
+plc_replay_kernel(DevProblem PR, DevPolicy PO, const double *__restrict__ rec, int rstride,
+                  const double *__restrict__ gep, int64_t gstride,
+                  const double *__restrict__ alpha, double beta, int B, double *__restrict__ cbuf,
+                  double *__restrict__ slab, double *__restrict__ tbuf, double *__restrict__ sbuf,
+                  int *__restrict__ posbuf) {
+    constexpr int K = kChunkWarps;
+    __shared__ double stage[K][2][6 * MAXD];
+    // dynamic: rtot[K][D][h] | rsm[K][6h+1] | vt[n] jt[n]
+    extern __shared__ __align__(16) double dyn[];
+    const int e = blockIdx.x;
+    const int n = PR.n, D = PR.d, h = PO.h, W = PR.W;
+    const double *ge = gep + (size_t)e * gstride;
+    if (ge[2 * n] == 0.0) return;  // failed chain: no contribution (pg_rows skips it)
     const int lane = lane_id();
     const int wi = threadIdx.x >> 5;
-    const int ep = blockIdx.x * kGradWarps + wi;
-    if (ep >= A.B) return;
-    const int n = PR.n, D = PR.d, h = PO.h;
-    const int RD = 7 * D;
-    const double slope = PO.slope;
-    const double *recd = (const double *)A.workspace + (size_t)ep * n * RD;
-    const int2 *recv = (const int2 *)((const double *)A.workspace + (size_t)A.B * n * RD) +
-                       (size_t)ep * n;
-    const int ok = ((const int *)((const int2 *)((const double *)A.workspace +
-                                                 (size_t)A.B * n * RD) + (size_t)A.B * n))[ep];
-    double *q = A.grad_ep + (size_t)ep * grad_ep_stride(n, h, D) + 2 * n;
-    double *rows = A.grad_rows + (size_t)ep * n * 4 * h;
-    if (!ok) {  // failed chain: zero rows / sums (finite under a zero advantage)
-        for (int i = lane; i < n * 4 * h; i += 32) rows[i] = 0.0;
-        for (int i = lane; i < 12 * h + 2 + 2 * D * h; i += 32) q[i] = 0.0;
-        return;
+    const int tid = threadIdx.x, nth = blockDim.x;
+    FP_PHASE_DECL;
+    FP_PHASE_BEGIN(rp_);
+    double *rtot = dyn;
+    double *rsm = rtot + (size_t)K * D * h;
+    int *vt = (int *)(rsm + (size_t)K * (6 * h + 1)), *jt = vt + n;
+    const double al = alpha[e];
+    const double eps = ge[2 * n + 1], ome = 1.0 - eps, ekd = eps / (double)D;
+    const double *recd = rec + (size_t)e * n * rstride;
+    auto recp = [&](int t) { return recd + (size_t)t * rstride; };
+    // ---- 1. placement order ----
+    for (int t = tid; t < n; t += nth) {
+        const int2 vj = *(const int2 *)(recp(t) + 6 * D);
+        vt[t] = vj.x;
+        jt[t] = vj.y;
+        posbuf[(size_t)e * n + vj.x] = t;
     }
+    __syncthreads();
+    FP_PHASE_END(rp_, 25);
+    // ---- 2. PLC adjoints (thread = step) ----
+    double *cep = cbuf + (size_t)e * n * D;
+    for (int t = tid; t < n; t += nth) {
+        const double *r = recp(t);
+        const double *lg = r + 5 * D;
+        const int jdx = ((const int2 *)(r + 6 * D))->y;
+        double mx = -INFINITY;
+        for (int d = 0; d < D; ++d) mx = fmax(mx, lg[d]);
+        double ed[MAXD], tot = 0.0;
+#pragma unroll
+        for (int d = 0; d < MAXD; ++d) {
+            ed[d] = d < D ? exp(lg[d] - mx) : 0.0;
+            tot += ed[d];
+        }
+        double pd[MAXD], q[MAXD], qp = 0.0, pj = 0.0, mj = 0.0;
+#pragma unroll
+        for (int d = 0; d < MAXD; ++d) {
+            if (d >= D) { pd[d] = q[d] = 0.0; continue; }
+            pd[d] = ed[d] / tot;
+            const double mix = __dadd_rn(__dmul_rn(pd[d], ome), ekd);
+            const double lm = log(__dadd_rn(mix, 1e-30));
+            q[d] = -ome * (lm + mix / __dadd_rn(mix, 1e-30));
+            qp += q[d] * pd[d];
+            if (d == jdx) { pj = pd[d]; mj = mix; }
+        }
+        const double g0 = ome * pj / __dadd_rn(mj, 1e-30);
+#pragma unroll
+        for (int d = 0; d < MAXD; ++d)
+            if (d < D)
+                cep[(size_t)t * D + d] =
+                    al * (g0 * ((d == jdx ? 1.0 : 0.0) - pd[d])) + beta * (pd[d] * (q[d] - qp));
+    }
+    __syncthreads();
+    FP_PHASE_END(rp_, 26);
+    // ---- 3. PLC rows, warp = chunk of steps, lane = hidden column ----
+    const int L = (n + K - 1) / K;
+    const int t0 = min(n, wi * L), t1 = min(n, t0 + L);
+    const double slope = PO.slope;
     const double *__restrict__ Atab = PO.A;
     const double *__restrict__ Gtab = PO.G;
-    double Mr[5][HPL], cr[HPL], w2r[HPL], Sd[MAXD][HPL], rsl[MAXD][HPL], rse[MAXD][HPL];
-    double dMl[5][HPL], dMe[5][HPL], dwl[HPL], dwe[HPL];
-    double db2l = 0.0, db2e = 0.0;
+    double Mr[5][HPL], cr[HPL], w2r[HPL], Sd[MAXD][HPL], rc[MAXD][HPL], dM[5][HPL], dw[HPL];
+    double db2 = 0.0;
     {
         const double *w2p = PO.W(PR_PLC_H2_W);
 #pragma unroll
@@ -1134,131 +1279,269 @@ plc_grad_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A) {
             const int j = lane + 32 * t;
             const bool in = j < h;
 #pragma unroll
-            for (int c = 0; c < 5; ++c) {
-                Mr[c][t] = in ? PO.M[c * h + j] : 0.0;
-                dMl[c][t] = dMe[c][t] = 0.0;
-            }
+            for (int c = 0; c < 5; ++c) { Mr[c][t] = in ? PO.M[c * h + j] : 0.0; dM[c][t] = 0.0; }
             cr[t] = in ? PO.c[j] : 0.0;
             w2r[t] = in ? w2p[j] : 0.0;
-            dwl[t] = dwe[t] = 0.0;
+            dw[t] = 0.0;
 #pragma unroll
-            for (int d = 0; d < MAXD; ++d) Sd[d][t] = rsl[d][t] = rse[d][t] = 0.0;
+            for (int d = 0; d < MAXD; ++d) Sd[d][t] = rc[d][t] = 0.0;
         }
     }
-    double *st0 = stage[wi][0];
-    for (int i = lane; i < RD; i += 32) st0[i] = recd[i];
-    int2 vj = recv[0];
-    int2 vj1 = n > 1 ? recv[1] : vj;
-    double Av[HPL], Gv[HPL];
-#pragma unroll
-    for (int t = 0; t < HPL; ++t) {
-        const int j = lane + 32 * t;
-        Av[t] = j < h ? Atab[(size_t)vj.x * h + j] : 0.0;
-        Gv[t] = j < h ? Gtab[(size_t)vj.x * h + j] : 0.0;
-    }
-    __syncwarp();
+    // S_d at the chunk's first step: the placed G rows, in step order (rows
+    // fetched four steps at a time)
 #pragma unroll 1
-    for (int step = 0; step < n; ++step) {
-        const double *x = stage[wi][step & 1];
-        const int v = vj.x, jdx = vj.y;
-        // fetch the next record, vertex rows and (vertex, device) pair while
-        // this step is reduced
-        double nx[(7 * MAXD + 31) / 32], nA[HPL], nG[HPL];
-        int2 vj2 = vj1;
-        if (step + 1 < n) {
-            const double *nr = recd + (size_t)(step + 1) * RD;
+    for (int tb = 0; tb < t0; tb += 4) {
+        double g4[4][HPL];
+        int j4[4];
 #pragma unroll
-            for (int k = 0; k < (7 * MAXD + 31) / 32; ++k) {
-                const int i = lane + 32 * k;
-                nx[k] = i < RD ? nr[i] : 0.0;
-            }
+        for (int u = 0; u < 4; ++u) {
+            const int t = tb + u;
+            j4[u] = t < t0 ? jt[t] : -1;
+            const int v = t < t0 ? vt[t] : 0;
 #pragma unroll
-            for (int t = 0; t < HPL; ++t) {
-                const int j = lane + 32 * t;
-                nA[t] = j < h ? Atab[(size_t)vj1.x * h + j] : 0.0;
-                nG[t] = j < h ? Gtab[(size_t)vj1.x * h + j] : 0.0;
-            }
-            if (step + 2 < n) vj2 = recv[step + 2];
-        }
-        double arl[HPL], are[HPL];
-#pragma unroll
-        for (int t = 0; t < HPL; ++t) arl[t] = are[t] = 0.0;
-#pragma unroll
-        for (int d = 0; d < MAXD; ++d) {
-            if (d >= D) continue;
-            const double x0 = x[d * 5], x1 = x[d * 5 + 1], x2 = x[d * 5 + 2], x3 = x[d * 5 + 3],
-                         x4 = x[d * 5 + 4];
-            const double gld = x[5 * D + d], ged = x[6 * D + d];
-            if (lane == 0) { db2l += gld; db2e += ged; }
-#pragma unroll
-            for (int t = 0; t < HPL; ++t) {
-                double a = Av[t] + Sd[d][t] + cr[t];
-                a = fma(x0, Mr[0][t], a);
-                a = fma(x1, Mr[1][t], a);
-                a = fma(x2, Mr[2][t], a);
-                a = fma(x3, Mr[3][t], a);
-                a = fma(x4, Mr[4][t], a);
-                const double dl = gld * w2r[t] * lkd(a, slope);
-                const double de = ged * w2r[t] * lkd(a, slope);
-                const double lv = lk(a, slope);
-                dwl[t] = fma(gld, lv, dwl[t]);
-                dwe[t] = fma(ged, lv, dwe[t]);
-                arl[t] += dl;
-                are[t] += de;
-                rsl[d][t] += dl;
-                rse[d][t] += de;
-                dMl[0][t] = fma(x0, dl, dMl[0][t]); dMe[0][t] = fma(x0, de, dMe[0][t]);
-                dMl[1][t] = fma(x1, dl, dMl[1][t]); dMe[1][t] = fma(x1, de, dMe[1][t]);
-                dMl[2][t] = fma(x2, dl, dMl[2][t]); dMe[2][t] = fma(x2, de, dMe[2][t]);
-                dMl[3][t] = fma(x3, dl, dMl[3][t]); dMe[3][t] = fma(x3, de, dMe[3][t]);
-                dMl[4][t] = fma(x4, dl, dMl[4][t]); dMe[4][t] = fma(x4, de, dMe[4][t]);
+            for (int q = 0; q < HPL; ++q) {
+                const int j = lane + 32 * q;
+                g4[u][q] = (t < t0 && j < h) ? Gtab[(size_t)v * h + j] : 0.0;
             }
         }
-        double *row = rows + (size_t)v * 4 * h;
 #pragma unroll
-        for (int t = 0; t < HPL; ++t) {
-            const int j = lane + 32 * t;
-            double sl = 0.0, se = 0.0;
+        for (int u = 0; u < 4; ++u)
 #pragma unroll
-            for (int d = 0; d < MAXD; ++d)
-                if (d == jdx) { sl = rsl[d][t]; se = rse[d][t]; Sd[d][t] += Gv[t]; }
-            if (j < h) {
-                row[j] = arl[t];
-                row[h + j] = are[t];
-                row[2 * h + j] = sl;
-                row[3 * h + j] = se;
-            }
-        }
-        if (step + 1 < n) {
-            double *ns = stage[wi][(step + 1) & 1];
+            for (int q = 0; q < HPL; ++q)
 #pragma unroll
-            for (int k = 0; k < (7 * MAXD + 31) / 32; ++k) {
-                const int i = lane + 32 * k;
-                if (i < RD) ns[i] = nx[k];
-            }
+                for (int d = 0; d < MAXD; ++d)
+                    if (d == j4[u]) Sd[d][q] += g4[u][q];
+    }
+    FP_PHASE_END(rp_, 29);
+    const int RS = 6 * D;  // staged: xn[5D] | c[D]
+    double *myslab = slab + (size_t)e * n * 2 * h;
+    if (t0 < t1) {
+        double *st0 = stage[wi][0];
+        for (int i = lane; i < RS; i += 32)
+            st0[i] = i < 5 * D ? recp(t0)[i] : cep[(size_t)t0 * D + i - 5 * D];
+        int vv = vt[t0], jj = jt[t0];
+        double Av[HPL], Gv[HPL];
 #pragma unroll
-            for (int t = 0; t < HPL; ++t) { Av[t] = nA[t]; Gv[t] = nG[t]; }
-            vj = vj1;
-            vj1 = vj2;
+        for (int q = 0; q < HPL; ++q) {
+            const int j = lane + 32 * q;
+            Av[q] = j < h ? Atab[(size_t)vv * h + j] : 0.0;
+            Gv[q] = j < h ? Gtab[(size_t)vv * h + j] : 0.0;
         }
         __syncwarp();
-    }
+#pragma unroll 1
+        for (int step = t0; step < t1; ++step) {
+            const double *x = stage[wi][(step - t0) & 1];
+            const int v = vv, jdx = jj;
+            // fetch the next record and vertex rows while this step is replayed
+            double nx[(6 * MAXD + 31) / 32], nA[HPL], nG[HPL];
+            if (step + 1 < t1) {
+                const double *nr = recp(step + 1);
+                const int nv = vt[step + 1];
 #pragma unroll
-    for (int t = 0; t < HPL; ++t) {
-        const int j = lane + 32 * t;
-        if (j >= h) continue;
+                for (int k = 0; k < (6 * MAXD + 31) / 32; ++k) {
+                    const int i = lane + 32 * k;
+                    nx[k] = i < 5 * D ? nr[i] : i < RS ? cep[(size_t)(step + 1) * D + i - 5 * D] : 0.0;
+                }
 #pragma unroll
-        for (int c = 0; c < 5; ++c) { q[c * h + j] = dMl[c][t]; q[5 * h + c * h + j] = dMe[c][t]; }
-        q[10 * h + j] = dwl[t];
-        q[11 * h + j] = dwe[t];
+                for (int q = 0; q < HPL; ++q) {
+                    const int j = lane + 32 * q;
+                    nA[q] = j < h ? Atab[(size_t)nv * h + j] : 0.0;
+                    nG[q] = j < h ? Gtab[(size_t)nv * h + j] : 0.0;
+                }
+            }
+            double ar[HPL];
 #pragma unroll
-        for (int d = 0; d < MAXD; ++d) {
-            if (d >= D) continue;
-            q[12 * h + 2 + d * h + j] = rsl[d][t];
-            q[12 * h + 2 + D * h + d * h + j] = rse[d][t];
+            for (int q = 0; q < HPL; ++q) ar[q] = 0.0;
+#pragma unroll
+            for (int d = 0; d < MAXD; ++d) {
+                if (d >= D) continue;
+                const double x0 = x[d * 5], x1 = x[d * 5 + 1], x2 = x[d * 5 + 2],
+                             x3 = x[d * 5 + 3], x4 = x[d * 5 + 4];
+                const double cd = x[5 * D + d];
+                if (lane == 0) db2 += cd;
+#pragma unroll
+                for (int q = 0; q < HPL; ++q) {
+                    double a = Av[q] + Sd[d][q] + cr[q];
+                    a = fma(x0, Mr[0][q], a);
+                    a = fma(x1, Mr[1][q], a);
+                    a = fma(x2, Mr[2][q], a);
+                    a = fma(x3, Mr[3][q], a);
+                    a = fma(x4, Mr[4][q], a);
+                    const double df = cd * w2r[q] * lkd(a, slope);
+                    dw[q] = fma(cd, lk(a, slope), dw[q]);
+                    ar[q] += df;
+                    rc[d][q] += df;
+                    dM[0][q] = fma(x0, df, dM[0][q]);
+                    dM[1][q] = fma(x1, df, dM[1][q]);
+                    dM[2][q] = fma(x2, df, dM[2][q]);
+                    dM[3][q] = fma(x3, df, dM[3][q]);
+                    dM[4][q] = fma(x4, df, dM[4][q]);
+                }
+            }
+            double *row = myslab + (size_t)v * 2 * h;
+#pragma unroll
+            for (int q = 0; q < HPL; ++q) {
+                const int j = lane + 32 * q;
+                double sl = 0.0;
+#pragma unroll
+                for (int d = 0; d < MAXD; ++d)
+                    if (d == jdx) { sl = rc[d][q]; Sd[d][q] += Gv[q]; }
+                if (j < h) { row[j] = ar[q]; row[h + j] = sl; }
+            }
+            if (step + 1 < t1) {
+                double *ns = stage[wi][(step + 1 - t0) & 1];
+#pragma unroll
+                for (int k = 0; k < (6 * MAXD + 31) / 32; ++k) {
+                    const int i = lane + 32 * k;
+                    if (i < RS) ns[i] = nx[k];
+                }
+#pragma unroll
+                for (int q = 0; q < HPL; ++q) { Av[q] = nA[q]; Gv[q] = nG[q]; }
+                vv = vt[step + 1];
+                jj = jt[step + 1];
+            }
+            __syncwarp();
         }
     }
-    if (lane == 0) { q[12 * h] = db2l; q[12 * h + 1] = db2e; }
+    // chunk totals / sums
+    {
+        double *Tw = rtot + (size_t)wi * D * h;
+        double *sw = rsm + (size_t)wi * (6 * h + 1);
+#pragma unroll
+        for (int q = 0; q < HPL; ++q) {
+            const int j = lane + 32 * q;
+            if (j >= h) continue;
+#pragma unroll
+            for (int d = 0; d < MAXD; ++d)
+                if (d < D) Tw[d * h + j] = rc[d][q];
+#pragma unroll
+            for (int c = 0; c < 5; ++c) sw[c * h + j] = dM[c][q];
+            sw[5 * h + j] = dw[q];
+        }
+        if (lane == 0) sw[6 * h] = db2;
+    }
+    FP_PHASE_END(rp_, 30);
+    __syncthreads();
+    FP_PHASE_END(rp_, 31);
+    FP_PHASE_FLUSH(0);
+    // per chunk c: (final per-device sum) - (sum over the chunks before c)
+    for (int i = tid; i < D * h; i += nth) {
+        double tot = 0.0;
+        for (int c = 0; c < K; ++c) tot += rtot[(size_t)c * D * h + i];
+        double pre = 0.0;
+        for (int c = 0; c < K; ++c) {
+            tbuf[((size_t)e * K + c) * D * h + i] = tot - pre;
+            pre += rtot[(size_t)c * D * h + i];
+        }
+    }
+    for (int k = tid; k < 6 * h + 1; k += nth) {
+        double acc = 0.0;
+        for (int c = 0; c < K; ++c) acc += rsm[(size_t)c * (6 * h + 1) + k];
+        sbuf[(size_t)e * (6 * h + 1) + k] = acc;
+    }
+}
+
+// Episode contraction of the replay's slab: item = (v, j) of dA / dG, the
+// small sums, and the SEL logits' terms ds[v]; episode chunk = blockIdx.y,
+// episodes of a chunk in order.  dG[v] collects, per episode, the final
+// per-device sum on v's device minus the running sum at v's placement
+// (chunk table of v's step minus the chunk-local running sum).
+static __global__ void pg_rows_kernel(DevPolicy P, int D, int B, int L,
+                                      const double *__restrict__ slab,
+                                      const double *__restrict__ tbuf,
+                                      const double *__restrict__ sbuf,
+                                      const int *__restrict__ posbuf,
+                                      const double *__restrict__ gep, int64_t gstride,
+                                      const int32_t *__restrict__ assign,
+                                      const double *__restrict__ alpha, double beta,
+                                      double *__restrict__ part) {
+    const int n = P.n, h = P.h, nh = n * h;
+    const int64_t PSt = pg_part_stride(n, h);
+    const int item = blockIdx.x * blockDim.x + threadIdx.x;
+    const int per = (B + kPgChunks - 1) / kPgChunks;
+    const int e0 = blockIdx.y * per, e1 = min(B, e0 + per);
+    double *pc = part + (size_t)blockIdx.y * PSt;
+    if (item < nh) {
+        const int v = item / h, j = item - v * h;
+        double a = 0.0, g = 0.0;
+#pragma unroll 4
+        for (int e = e0; e < e1; ++e) {
+            if (gep[(size_t)e * gstride + 2 * n] == 0.0) continue;  // failed chain
+            const double *r = slab + ((size_t)e * n + v) * 2 * h;
+            const int dv = assign[(size_t)e * n + v];
+            const int c = posbuf[(size_t)e * n + v] / L;
+            a += r[j];
+            g += tbuf[(((size_t)e * kChunkWarps + c) * D + dv) * h + j] - r[h + j];
+        }
+        pc[item] = a;
+        pc[nh + item] = g;
+    } else if (item < nh + 6 * h + 1) {
+        const int k = item - nh;
+        double acc = 0.0;
+        for (int e = e0; e < e1; ++e)
+            if (gep[(size_t)e * gstride + 2 * n] != 0.0) acc += sbuf[(size_t)e * (6 * h + 1) + k];
+        pc[nh + item] = acc;
+    } else if (item < nh + 6 * h + 1 + n) {
+        const int v = item - nh - 6 * h - 1;
+        double acc = 0.0;
+        for (int e = e0; e < e1; ++e)
+        {
+            const double *g = gep + (size_t)e * gstride;
+            if (g[2 * n] != 0.0) acc += alpha[e] * g[v] + beta * g[n + v];
+        }
+        pc[nh + item] = acc;
+    }
+}
+
+// chunk partials -> dA, dG, [dM | dw2 | db2], ds, summed in chunk order
+static __global__ void pg_final_kernel(DevPolicy P, const double *__restrict__ part) {
+    const int n = P.n, h = P.h, nh = n * h;
+    const int64_t PSt = pg_part_stride(n, h);
+    const int item = blockIdx.x * blockDim.x + threadIdx.x;
+    if (item >= PSt) return;
+    double acc = 0.0;
+#pragma unroll
+    for (int c = 0; c < kPgChunks; ++c) acc += part[(size_t)c * PSt + item];
+    if (item < nh) P.dA[item] = acc;
+    else if (item < 2 * nh) P.dG[item - nh] = acc;
+    else if (item < 2 * nh + 6 * h + 1) P.dsmall[h + (item - 2 * nh)] = acc;  // [dc | dM | dw2 | db2]
+    else P.ds[item - 2 * nh - 6 * h - 1] = acc;
+}
+
+template <int MAXD, int HPL>
+int launch_plc_replay(const fp_problem *p, const fp_policy *pol, const double *rec,
+                      const double *gep, const int32_t *assign, const double *alpha, double beta,
+                      int B, double *scratch, int64_t *scratch_bytes, cudaStream_t st) {
+    constexpr int K = kChunkWarps;
+    const DevProblem &PR = p->dev;
+    const DevPolicy &PO = pol->dev;
+    const int n = PR.n, D = PR.d, h = PO.h;
+    const int64_t slab_d = (int64_t)B * n * 2 * h, t_d = (int64_t)B * K * D * h,
+                  s_d = (int64_t)B * (6 * h + 1), PSt = pg_part_stride(n, h),
+                  c_d = (int64_t)B * n * D, pos_d = ((int64_t)B * n + 1) / 2;
+    if (scratch_bytes) {
+        *scratch_bytes = (slab_d + t_d + s_d + c_d + pos_d + kPgChunks * PSt) * 8;
+        return FP_OK;
+    }
+    double *slab = scratch, *tbuf = slab + slab_d, *sbuf = tbuf + t_d, *part = sbuf + s_d,
+           *cbuf = part + kPgChunks * PSt;
+    int *posbuf = (int *)(cbuf + c_d);
+    const int64_t gstride = grad_ep_stride(n, h, D);
+    const int64_t dyn = 8LL * ((int64_t)K * D * h + (int64_t)K * (6 * h + 1)) + 8LL * n;
+    auto kern = plc_replay_kernel<MAXD, HPL>;
+    cudaError_t e0 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)dyn);
+    if (e0 != cudaSuccess) { set_error(cudaGetErrorString(e0)); return FP_ERR_CUDA; }
+    kern<<<B, K * 32, dyn, st>>>(PR, PO, rec, grad_rec_stride(D, PR.W), gep, gstride, alpha, beta,
+                                 B, cbuf, slab, tbuf, sbuf, posbuf);
+    const int items = n * h + 6 * h + 1 + n;
+    pg_rows_kernel<<<dim3((items + 127) / 128, kPgChunks), 128, 0, st>>>(
+        PO, D, B, (n + K - 1) / K, slab, tbuf, sbuf, posbuf, gep, gstride, assign, alpha, beta,
+        part);
+    pg_final_kernel<<<(int)((PSt + 127) / 128), 128, 0, st>>>(PO, part);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FP_ERR_CUDA; }
+    return FP_OK;
 }
 
 template <int MAXD, int HPL, bool GRAD>
@@ -1268,8 +1551,8 @@ int launch_rollout(const fp_problem *p, const fp_policy *pol, const fp_rollout_a
     const DevProblem &PR = p->dev;
     const EpLayout L = make_layout(PR.n, PR.W, PR.R, PR.SM, true, 0);
     const int64_t smem = fp_align(8 * PR.n, 16) + (int64_t)L.bytes * EPB;
-    if (GRAD && (!a.workspace || a.workspace_bytes < grad_rec_bytes(a.B, PR.n, PR.d))) {
-        set_error("REINFORCE rollout needs fp_rollout_workspace_size bytes of workspace");
+    if (GRAD && (!a.grad_rows || !a.grad_ep)) {
+        set_error("REINFORCE rollout needs grad_rows (decision records) and grad_ep");
         return FP_ERR_INVALID;
     }
     if (smem > 227 * 1024) {
@@ -1287,9 +1570,6 @@ int launch_rollout(const fp_problem *p, const fp_policy *pol, const fp_rollout_a
     if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FP_ERR_CUDA; }
     const int grid = (a.B + EPB - 1) / EPB;
     kern<<<grid, EPB * 64, smem, st>>>(PR, pol->dev, a, L);
-    if constexpr (GRAD)
-        plc_grad_kernel<MAXD, HPL><<<(a.B + kGradWarps - 1) / kGradWarps, kGradWarps * 32, 0,
-                                     st>>>(PR, pol->dev, a);
     e = cudaGetLastError();
     if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FP_ERR_CUDA; }
     return FP_OK;

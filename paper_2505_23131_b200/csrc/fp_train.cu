@@ -5,12 +5,14 @@
 //   (alpha_e = -advantage_e / B_global, beta = -w_entropy / B_global; the
 //   reference's per-episode loss at B = 1; imitation: alpha = -1/B, beta = 0)
 //
-// 1. pg_reduce: the rollout kernel wrote, per episode, the gradients of
-//    sum lp and sum ent w.r.t. the per-vertex tables (SEL logit s[v]; PLC rows
-//    A[v], G[v] via running per-device sums; M, w2, b2).  This kernel contracts
-//    them with (alpha_e, beta) over the batch — a streaming, HBM-bound pass
-//    over B*n*4h doubles — in a fixed episode order (chunked partials, then an
-//    ordered chunk sum): bitwise deterministic, no atomics.
+// 1. pg_reduce: the rollout's SEL warp wrote, per episode, the gradients of
+//    sum lp and sum ent w.r.t. the SEL logits s[v]; its PLC warp recorded each
+//    decision.  plc_replay_kernel (fp_rollout.cuh) replays the records with
+//    the episode's (alpha_e, beta) folded in from the first step, producing
+//    the PLC table gradients (A, G rows via running per-device sums; M, w2,
+//    b2) and the SEL terms, reduced over the CTA's episodes in episode order;
+//    pg_final_kernel sums the CTA partials in CTA order: bitwise
+//    deterministic, no atomics, no per-episode rows through HBM.
 // 2. head backward (SEL head + paths, PLC tables), 3. GNN backward (K rounds
 //    per encoder, gather-formulated message gradients), 4. weight gradients as
 //    row-contractions X^T Y over vertices (outer kernel, job list), 5. SGD.
@@ -23,81 +25,12 @@
 
 namespace fp {
 
-__host__ __device__ inline int64_t grad_ep_stride_t(int n, int h, int d) {
-    return ((2LL * n + 12LL * h + 2 + 2LL * d * h) + 3) / 4 * 4;
-}
+int plc_replay(const fp_problem *p, const fp_policy *pol, const double *rec, const double *gep,
+               const int32_t *assign, const double *alpha, double beta, int B, double *scratch,
+               int64_t *scratch_bytes, cudaStream_t st);  // fp_rollout.cu
 
 __device__ __forceinline__ double lkd_t(double x, double s) { return x > 0.0 ? 1.0 : s; }
 __device__ __forceinline__ double lk_t(double x, double s) { return x > 0.0 ? x : s * x; }
-
-constexpr int kChunks = 16;
-
-// items: [0, n*h) (v, j) -> dA, dG; [n*h, n*h+n) -> ds[v];
-// then 5h dM, h dw2, 1 db2
-__global__ void pg_reduce_partial(DevPolicy P, int n, int h, int D, int B,
-                                  const double *__restrict__ rows, const double *__restrict__ gep,
-                                  const int32_t *__restrict__ assign,
-                                  const double *__restrict__ alpha, double beta) {
-    const int item = blockIdx.x * blockDim.x + threadIdx.x;
-    const int chunk = blockIdx.y;
-    const int nh = n * h;
-    const int items = nh + n + 6 * h + 1;
-    if (item >= items) return;
-    const int per = (B + kChunks - 1) / kChunks;
-    const int e0 = chunk * per, e1 = min(B, e0 + per);
-    const int64_t S = grad_ep_stride_t(n, h, D);
-    double *part = P.partial + (size_t)chunk * (2 * (size_t)nh + n + 6 * h + 1);
-    if (item < nh) {
-        const int v = item / h, j = item - v * h;
-        double a = 0.0, g = 0.0;
-        const size_t rstride = (size_t)n * 4 * h;
-        const double *r = rows + (size_t)v * 4 * h + j;
-        const double *tq = gep + 2 * n + 12 * h + 2 + j;
-#pragma unroll 4
-        for (int e = e0; e < e1; ++e) {
-            const double al = alpha[e];
-            const double *re = r + (size_t)e * rstride;
-            const double r0 = re[0], r1 = re[h], r2 = re[2 * h], r3 = re[3 * h];
-            const int dv = assign[(size_t)e * n + v];
-            const double *te = tq + (size_t)e * S + dv * h;
-            const double tl = te[0], tn = te[D * h];
-            a += al * r0 + beta * r1;
-            g += al * (tl - r2) + beta * (tn - r3);
-        }
-        part[item] = a;
-        part[nh + item] = g;
-        return;
-    }
-    int k = item - nh;
-    double acc = 0.0;
-    if (k < n) {  // ds[v]
-        for (int e = e0; e < e1; ++e)
-            acc += alpha[e] * gep[(size_t)e * S + k] + beta * gep[(size_t)e * S + n + k];
-    } else {
-        k -= n;  // small vectors: dM (5h), dw2 (h), db2 (1) -> lp part at 2n+off, ent at +5h/+h/+1
-        int lo, eo;
-        if (k < 5 * h) { lo = 2 * n + k; eo = 2 * n + 5 * h + k; }
-        else if (k < 6 * h) { lo = 2 * n + 10 * h + (k - 5 * h); eo = lo + h; }
-        else { lo = 2 * n + 12 * h; eo = lo + 1; }
-        for (int e = e0; e < e1; ++e)
-            acc += alpha[e] * gep[(size_t)e * S + lo] + beta * gep[(size_t)e * S + eo];
-    }
-    part[nh + item] = acc;
-}
-
-__global__ void pg_reduce_final(DevPolicy P, int n, int h) {
-    const int item = blockIdx.x * blockDim.x + threadIdx.x;
-    const int nh = n * h;
-    const int total = 2 * nh + n + 6 * h + 1;
-    if (item >= total) return;
-    const size_t stride = 2 * (size_t)nh + n + 6 * h + 1;
-    double acc = 0.0;
-    for (int c = 0; c < kChunks; ++c) acc += P.partial[c * stride + item];
-    if (item < nh) P.dA[item] = acc;
-    else if (item < 2 * nh) P.dG[item - nh] = acc;
-    else if (item < 2 * nh + n) P.ds[item - 2 * nh] = acc;
-    else P.dsmall[h + (item - 2 * nh - n)] = acc;  // dsmall: [dc (h) | dM (5h) | dw2 (h) | db2]
-}
 
 // ---------------------------------------------------------------------------
 // head backward, warp per vertex, lane = hidden column
@@ -371,7 +304,9 @@ __global__ void __launch_bounds__(256) small_bwd_kernel(DevPolicy P, double *gra
     }
 }
 
-__global__ void sgd_kernel(double *params, const double *grad, int64_t count, double lr) {
+__global__ void sgd_kernel(double *params, const double *grad, int64_t count, double lr,
+                           const int32_t *skip) {
+    if (skip && *skip) return;  // a failed rollout in this (or an earlier) batch: no update
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < count) params[i] = params[i] - lr * grad[i];
 }
@@ -386,11 +321,14 @@ struct fp_train_state {
     std::vector<int> stage_offset;
     double *bound_grad = nullptr;
     const double *bound_params = nullptr;
+    void *replay = nullptr;        // fp_pg_reduce scratch: episode-row slab + CTA partials
+    int64_t replay_bytes = 0;
 };
 
 void fp_train_state_free(fp_train_state *ts) {
     if (!ts) return;
     if (ts->jobs_dev) cudaFree(ts->jobs_dev);
+    if (ts->replay) cudaFree(ts->replay);
     delete ts;
 }
 
@@ -480,17 +418,25 @@ int fp_pg_reduce(fp_policy *pol, const double *grad_rows, const double *grad_ep,
         set_error("bad pg_reduce arguments");
         return FP_ERR_INVALID;
     }
-    DevPolicy &P = pol->dev;
-    const int n = P.n, h = P.h, D = pol->problem->dev.d;
-    const int items = n * h + n + 6 * h + 1;
+    if (!pol->train) pol->train = new fp_train_state();
+    auto *ts = pol->train;
     cudaStream_t st = (cudaStream_t)stream;
-    pg_reduce_partial<<<dim3((items + 127) / 128, kChunks), 128, 0, st>>>(
-        P, n, h, D, B, grad_rows, grad_ep, assign, alpha, beta);
-    const int total = 2 * n * h + n + 6 * h + 1;
-    pg_reduce_final<<<(total + 127) / 128, 128, 0, st>>>(P, n, h);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FP_ERR_CUDA; }
-    return FP_OK;
+    int64_t need = 0;
+    int rc = plc_replay(pol->problem, pol, grad_rows, grad_ep, assign, alpha, beta, B, nullptr,
+                        &need, st);
+    if (rc) return rc;
+    if (ts->replay_bytes < need) {  // grown on demand, kept for the next updates
+        if (ts->replay) { cudaStreamSynchronize(st); cudaFree(ts->replay); }
+        ts->replay = nullptr;
+        ts->replay_bytes = 0;
+        if (cudaMalloc(&ts->replay, need) != cudaSuccess) {
+            set_error("cudaMalloc failed for the REINFORCE replay scratch");
+            return FP_ERR_CUDA;
+        }
+        ts->replay_bytes = need;
+    }
+    return plc_replay(pol->problem, pol, grad_rows, grad_ep, assign, alpha, beta, B,
+                      (double *)ts->replay, nullptr, st);
 }
 
 int fp_policy_backward(fp_policy *pol, double *grad, void *stream) {
@@ -527,14 +473,19 @@ int fp_policy_backward(fp_policy *pol, double *grad, void *stream) {
     return FP_OK;
 }
 
-int fp_sgd_step(double *params, const double *grad, int64_t count, double lr, void *stream) {
+int fp_sgd_step_masked(double *params, const double *grad, int64_t count, double lr,
+                       const int32_t *skip, void *stream) {
     if (!params || !grad || count < 0) { set_error("bad sgd arguments"); return FP_ERR_INVALID; }
     if (count == 0) return FP_OK;
     sgd_kernel<<<(unsigned)((count + 255) / 256), 256, 0, (cudaStream_t)stream>>>(params, grad,
-                                                                                  count, lr);
+                                                                                  count, lr, skip);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FP_ERR_CUDA; }
     return FP_OK;
+}
+
+int fp_sgd_step(double *params, const double *grad, int64_t count, double lr, void *stream) {
+    return fp_sgd_step_masked(params, grad, count, lr, nullptr, stream);
 }
 
 }  // extern "C"

@@ -414,6 +414,12 @@ class PolicyContext:
         batch._alpha = alpha
         return grad
 
+    def grad_rec_stride(self) -> int:
+        s = ctypes.c_int64()
+        N.check(N.lib().fp_grad_rec_stride(self.handle, ctypes.c_int32(self.cluster.device_count),
+                                           ctypes.byref(s)))
+        return s.value
+
     def grad_ep_stride(self) -> int:
         s = ctypes.c_int64()
         N.check(N.lib().fp_grad_ep_stride(self.handle, ctypes.c_int32(self.cluster.device_count),
@@ -437,7 +443,8 @@ class PolicyContext:
             rb.step_argmax = torch.empty((B, n, 2), dtype=i32, device=dev)
             rb.step_ncand = torch.empty((B, n), dtype=i32, device=dev)
         if grad:
-            rb.grad_rows = torch.empty((B, n, 4, h), dtype=f64, device=dev)
+            # per-decision REINFORCE records (fp_grad_rec_stride doubles each)
+            rb.grad_rows = torch.empty((B, n, self.grad_rec_stride()), dtype=f64, device=dev)
             rb.grad_ep = torch.empty((B, self.grad_ep_stride()), dtype=f64, device=dev)
         if sim_trace:
             cap = 2 * (n + n * d) + 2

@@ -178,6 +178,13 @@ class BatchedTrainer:
         self.lr_sched = LinearSchedule(config.lr0, config.lr1, config.episodes)
         self.eps_sched = LinearSchedule(config.epsilon0, 0.0, config.episodes)
         self.out = None
+        # failed rollouts are detected without a host sync inside the step: a
+        # sticky device flag (count of failed episodes) masks every later SGD
+        # update, and its pinned host copy is checked -- raising -- at the
+        # next step once it has landed, or by check() (blocking)
+        self.failed = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self._failed_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+        self._failed_ev = None
 
     def load_flat(self, flat):
         self.flat.copy_(flat)
@@ -192,6 +199,18 @@ class BatchedTrainer:
         # + backward (head 2 + outer 2 + small 1 + per (enc, round) 3 (+copy)) + sgd
         per_round = n_enc * pc.k_rounds * 4 - n_enc
         return self.ctx.encode_launches() + 1 + 2 + 5 + per_round + 1
+
+    def check(self, block: bool = True) -> None:
+        """Raise if a rollout of an earlier step failed (the parameters were
+        left at their value before that step: its SGD update was masked)."""
+        ev = self._failed_ev
+        if ev is None or (not block and not ev.query()):
+            return
+        ev.synchronize()
+        nbad = int(self._failed_host[0])
+        if nbad:
+            raise RuntimeError(f"rollout failed for {nbad} episode(s); parameters kept at their "
+                               "value before the failing update")
 
     def local_count(self, n_global: int) -> int:
         """Episodes of a (possibly short) update of ``n_global`` episodes that
@@ -208,6 +227,7 @@ class BatchedTrainer:
         import torch
 
         ctx = self.ctx
+        self.check(block=False)
         ng = self.Bg if n_global is None else int(n_global)
         if not 0 < ng <= self.Bg:
             raise ValueError(f"n_global must be in 1..{self.Bg}")
@@ -239,7 +259,9 @@ class BatchedTrainer:
             mk = torch.tensor(mkl, dtype=torch.float64, device="cuda")
         else:
             mk = out.makespan[:Bl]
-        if Bl and bool((out.status[:Bl] != 0).any()):
+        if Bl:  # no host sync: counted on the device, SGD masked, raised later
+            self.failed += (out.status[:Bl] != 0).sum(dtype=torch.int32)
+        if record and Bl and bool((out.status[:Bl] != 0).any()):
             st = out.status[:Bl].cpu().numpy()
             raise RuntimeError(f"rollout failed for {int((st != 0).sum())} of {Bl} episodes "
                                f"(status codes {sorted(set(st.tolist()) - {0})})")
@@ -261,9 +283,13 @@ class BatchedTrainer:
         else:
             self.grad.zero_()
         self.upd.finish(mk, ng)
-        N.check(N.lib().fp_sgd_step(N.ptr(self.flat), N.ptr(self.grad),
-                                    ctypes.c_int64(self.grad.numel()), ctypes.c_double(lr),
-                                    N.stream_ptr()))
+        N.check(N.lib().fp_sgd_step_masked(N.ptr(self.flat), N.ptr(self.grad),
+                                           ctypes.c_int64(self.grad.numel()), ctypes.c_double(lr),
+                                           N.ptr(self.failed), N.stream_ptr()))
+        self._failed_host.copy_(self.failed, non_blocking=True)
+        if self._failed_ev is None:
+            self._failed_ev = torch.cuda.Event()
+        self._failed_ev.record()
         self.updates += 1
         if record:
             mkh = mk.cpu().numpy()
@@ -326,6 +352,7 @@ def _stage(stage: str, graph, cluster, config: TrainConfig, pconfig: PolicyConfi
             if best_mk is None or mk < best_mk:
                 best_mk = mk
                 best_assign = Assignment(tuple(int(x) for x in st["assign"][b]), "doppler")
+    tr.check()
     out_params = tr.params()
     if isinstance(params, dict):  # keep the caller's dict in sync (reference mutates in place)
         for k, v in out_params.items():
