@@ -142,3 +142,31 @@ def test_system_rl_batched_executor_matches_per_call():
     m1 = [row["makespan_ms"] for row in r1.curve]
     m2 = [row["makespan_ms"] for row in r2.curve]
     assert m1 == m2 and len(m1) == 8
+
+
+def test_trainer_failed_rollout_masks_update_and_raises(torch_cuda):
+    """A failed episode (status != 0) is counted on the device: that step's
+    SGD update (and every later one) is skipped without a host sync inside
+    the step, and the trainer raises at its next check."""
+    from paper_2505_23131_b200.training import BatchedTrainer, TrainConfig
+    g, cl = builders.build_ffnn(8, 4, 16, 4, 2), ClusterSpec.uniform(8, 1e6, 1e5)
+    pc = PolicyConfig()
+    ctx = PolicyContext(g, cl, pc)
+    tr = BatchedTrainer(ctx, init_policy_params(pc, seed=0), TrainConfig(episodes=64),
+                        batch_size=16)
+    tr.step(seed=1)
+    tr.check()                      # clean step: nothing to raise
+    before = tr.flat.clone()
+    real = ctx.rollout_batch
+
+    def failing(*a, **kw):          # the rollout reports a deadlock for episode 3
+        out = real(*a, **kw)
+        kw["out"].status[3] = 1
+        return out
+
+    ctx.rollout_batch = failing
+    tr.step(seed=2)
+    ctx.rollout_batch = real
+    assert (tr.flat == before).all()   # masked on the device
+    with pytest.raises(RuntimeError, match="rollout failed"):
+        tr.check()
