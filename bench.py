@@ -425,8 +425,8 @@ def run_ours(args):
         per_ep = 4 * n + 12
         per_launch = (n + 1) * 8 + E * 8 + 16 * n + 8 * n + 2 * n * h * 8
         alg = B * per_ep + per_launch
-        if train:
-            alg += B * n * 4 * h * 8  # REINFORCE rows written
+        if train:  # REINFORCE decision records written (grad_rec_stride doubles per step)
+            alg += B * n * ctx.grad_rec_stride() * 8
         per_step = args.mp_mode == "per_step"
         K = pc.k_rounds
         prep_launches = ctx.encode_launches()
@@ -439,13 +439,16 @@ def run_ours(args):
         else:
             launches = prep_launches + 1
         achieved = alg / (kms * 1e-3) / 1e9
-        traffic = None
-        tpath = ROOT / "profiles" / "r1_traffic.json"
-        if tpath.exists():
-            rec = json.loads(tpath.read_text()).get(
-                f"{args.workload}/rollout_kernel{'(grad)' if train else ''}")
-            if rec and rec.get("batch") == B and not per_step:
-                traffic = rec["dram_bytes_read"] + rec["dram_bytes_write"]
+        # DRAM traffic and executed instructions of this very kernel and config,
+        # from the ncu capture of the same bench command committed this round
+        # (tools/roofline_capture.sh -> profiles/r2/rollout_ncu.json)
+        traffic, ncu_rec = None, None
+        tpath = ROOT / "profiles" / "r2" / "rollout_ncu.json"
+        if tpath.exists() and not per_step:
+            ncu_rec = json.loads(tpath.read_text()).get(
+                f"{args.workload}/{'train' if train else 'rollout'}/B{B}")
+            if ncu_rec:
+                traffic = ncu_rec["dram_bytes_read"] + ncu_rec["dram_bytes_write"]
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -473,6 +476,9 @@ def run_ours(args):
         line["rates"] = _episode_rates(g, out.assign.cpu().numpy(), value)
         if clk:
             line["clocks"] = clk.summary(local)
+        if not per_step:
+            sm_mhz = (line.get("clocks") or {}).get("sm_mhz") or 1965.0
+            line["roofline"]["latency"] = latency_roofline(n, B, kms, sm_mhz, ncu_rec, tpath)
         if world == 1 and not args.no_cpu:
             v, eps_done, wall = cpu_throughput(args.workload, args.cpu_seconds, os.cpu_count(),
                                                train, args.mp_mode == "per_step")
@@ -482,6 +488,43 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+# Dependent-latency floor of one PLC decision (the chain that bounds the
+# rollout kernel): dependent operations on the decision
+# chain of plc_chain (fp_rollout.cuh) x their measured latencies on this B200
+# (tools/micro/lat.cu, cycles per dependent trip minus its ~19-cycle loop).
+# Loads from the graph tables (L1/L2) are counted as prefetchable, i.e. not
+# part of the floor.
+PLC_CHAIN_OPS = {          # op: (dependent count per decision, latency cycles)
+    "LDS round trip (order, dev/tend, xd column, stats, xn, flag)": (6, 23),
+    "fp64 add/fma (column sums 8 + centred squares 3x8 + pre-activation 8 + misc 13)": (53, 4),
+    "SHFL (transpose reduction 5, device scan 3, broadcasts 3)": (11, 7),
+    "REDUX (fp64 max as two 32-bit reductions) x2": (2, 20),
+    "fp64 exp (device softmax)": (1, 154),
+    "fp64 sqrt_rn (column std)": (1, 93),
+    "fp64 reciprocal (column std)": (1, 70),
+}
+
+
+def latency_roofline(n, B, kernel_ms, sm_mhz, ncu_rec, src):
+    """The rollout kernel against its latency bound: every episode of the
+    batch is in flight at once (one wave up to 8 x 148 episodes), so the
+    kernel time is the per-episode chain; per decision that is
+    kernel_cycles / n, against the dependent-latency floor above."""
+    waves = -(-B // (8 * 148))
+    cycles = kernel_ms * 1e-3 * sm_mhz * 1e6 / waves
+    floor = sum(c * l for c, l in PLC_CHAIN_OPS.values())
+    out = {"unit": "cycles per decision", "achieved": cycles / n, "floor": floor,
+           "frac": floor / (cycles / n), "waves": waves,
+           "floor_model": "PLC decision chain: dependent op counts x tools/micro/lat.cu latencies "
+                          "(bench.PLC_CHAIN_OPS, DESIGN.md section 4)"}
+    if ncu_rec:
+        inst = ncu_rec["inst_executed"]
+        out["warp_instructions_per_decision"] = inst / (B * n)
+        out["ipc_per_sm"] = ncu_rec.get("ipc")
+        out["ncu_source"] = str(src.relative_to(ROOT))
+    return out
 
 
 def run_reference(args):
