@@ -13,8 +13,10 @@ Differences from the reference, by design:
     recorded mixture log-probs are the reference's;
   * ``EpisodeTrace.logprob_tensors`` / ``entropy_tensors`` stay empty: the
     REINFORCE gradient is produced natively (``training.py``);
-  * teachers: ``CriticalPathRule`` runs natively; any other teacher must be a
-    ``ForcedActions`` replay (no per-step Python callbacks on the GPU path).
+  * teachers: ``CriticalPathRule`` runs natively; ``ForcedActions`` replays
+    recorded actions; any other object with the reference's select / place
+    interface is stepped on the host (``teacher_actions``) and its actions
+    replayed in FORCED mode (no per-step Python callbacks inside the kernel).
 """
 
 from __future__ import annotations
@@ -169,6 +171,52 @@ class RolloutBatch:
     grad_ep: object | None = None
     trace: object | None = None
     trace_len: object | None = None
+
+
+def is_native_teacher(teacher) -> bool:
+    """CriticalPathRule runs inside the rollout kernel (FP_MODE_TEACHER)."""
+    return isinstance(teacher, CriticalPathRule) or type(teacher).__name__ == "CriticalPathRule"
+
+
+def teacher_actions(graph: DataflowGraph, cluster, teacher, episodes: int = 1) -> np.ndarray:
+    """Actions of an arbitrary (duck-typed) teacher, stepped on the host the
+    way the reference's rollout calls it (policy.py:353-389): at every step
+    ``teacher.select(candidates)`` on the ascending candidate list, then
+    ``teacher.place(v, timeline)`` on the committed placements so far
+    (heuristics.PlacementTimeline, timeline.py:19-58).  Returns [episodes, n,
+    2] (vertex, device) for the GPU rollout's FORCED mode, which recomputes the
+    log-probs / REINFORCE terms of these actions; one host pass per episode,
+    so stochastic teachers get independent episodes.  A vertex outside the
+    candidates raises TeacherActionError (reference policy.py:359-363); an
+    out-of-range device is reported by the kernel (FP_EP_BAD_ACTION)."""
+    from .heuristics import PlacementTimeline
+
+    n = len(graph)
+    preds = [len(graph.preds(v)) for v in range(n)]
+    out = np.empty((episodes, n, 2), dtype=np.int32)
+    for e in range(episodes):
+        left = list(preds)
+        cands = sorted(v for v in range(n) if left[v] == 0)
+        tl = PlacementTimeline(graph, cluster)
+        for t in range(n):
+            if not cands:
+                raise TeacherActionError("no candidate left (cyclic graph)")
+            v = int(teacher.select(list(cands)))
+            if v not in cands:
+                raise TeacherActionError(
+                    f"teacher selected vertex {v} outside candidates {cands}")
+            d = int(teacher.place(v, tl))
+            if not 0 <= d < cluster.device_count:
+                raise TeacherActionError(f"teacher placed vertex {v} on device {d}")
+            tl.commit(v, d)
+            out[e, t] = (v, d)
+            cands.remove(v)
+            for w in graph.succs(v):
+                left[w] -= 1
+                if left[w] == 0:
+                    cands.append(w)
+            cands.sort()
+    return out
 
 
 def _candidate_sets(graph: DataflowGraph, order) -> list[tuple[int, ...]]:
@@ -458,14 +506,12 @@ class PolicyContext:
         n = len(self.graph)
         mode, forced = ("greedy" if greedy else "sample"), None
         if teacher is not None:
-            if isinstance(teacher, CriticalPathRule) or type(teacher).__name__ == "CriticalPathRule":
+            if is_native_teacher(teacher):
                 mode = "teacher"
             elif isinstance(teacher, ForcedActions):
                 mode, forced = "forced", teacher.actions.reshape(1, n, 2)
-            else:
-                raise NotImplementedError(
-                    "the CUDA rollout executes CriticalPathRule natively or replays "
-                    "ForcedActions; arbitrary Python teachers are not supported")
+            else:  # any object with select(candidates) / place(v, timeline)
+                mode, forced = "forced", teacher_actions(self.graph, self.cluster, teacher)
         start = self.encode_count
         rb = self.rollout_batch(params, 1, epsilon, seed, mode=mode, forced=forced,
                                 simulate=False, trace_steps=True)

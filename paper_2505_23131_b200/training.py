@@ -28,9 +28,9 @@ import numpy as np
 from . import _native as N
 from .cluster import ClusterSpec
 from .graph import DataflowGraph
-from .heuristics import Assignment, CriticalPathRule
+from .heuristics import Assignment, CriticalPathRule  # noqa: F401
 from .params import (Params, init_policy_params, load_params, param_shapes, save_params)
-from .policy import PolicyConfig, PolicyContext
+from .policy import PolicyConfig, PolicyContext, is_native_teacher, teacher_actions
 from .simulate import exec_time_batch
 
 STAGES = ("imitation", "sim_rl", "system_rl")
@@ -160,7 +160,7 @@ class BatchedTrainer:
 
     def __init__(self, ctx: PolicyContext, params, config: TrainConfig, batch_size: int = 1024,
                  world: int = 1, rank: int = 0, group=None, stage: str = "sim_rl",
-                 executor=None):
+                 executor=None, teacher=None):
         import torch
 
         self.ctx = ctx
@@ -169,6 +169,9 @@ class BatchedTrainer:
         self.world, self.rank, self.group = world, rank, group
         self.stage = stage
         self.executor = executor
+        # imitation teacher: None / CriticalPathRule run in the kernel; any
+        # other select / place object is stepped on the host (FORCED replay)
+        self.teacher = None if teacher is None or is_native_teacher(teacher) else teacher
         self.Bg = self.B * world
         self.flat = ctx.flat_params(params).clone()
         self.upd = GlobalUpdate(ctx.layout.size, self.B, world, group)
@@ -242,9 +245,14 @@ class BatchedTrainer:
         if kernel_events is not None:
             kernel_events[0].record()
         mode = "teacher" if self.stage == "imitation" else "sample"
+        forced = None
+        if self.stage == "imitation" and self.teacher is not None and Bl:
+            mode = "forced"
+            forced = torch.from_numpy(
+                teacher_actions(ctx.graph, ctx.cluster, self.teacher, Bl)).cuda()
         if Bl:
-            ctx.rollout_batch(self.flat, Bl, eps, seed, mode=mode, grad=True, out=out,
-                              episode_base=self.rank * self.B, prepare=False,
+            ctx.rollout_batch(self.flat, Bl, eps, seed, mode=mode, forced=forced, grad=True,
+                              out=out, episode_base=self.rank * self.B, prepare=False,
                               simulate=self.executor is None, strategy=self.config.strategy)
         if kernel_events is not None:
             kernel_events[1].record()
@@ -310,12 +318,15 @@ def measure_teacher_agreement(ctx: PolicyContext, params, teacher, rollouts: int
     matches the teacher's, select and place counted separately
     (training.py:162-178).  All ``rollouts`` episodes run as one teacher-mode
     batch on the GPU (episode k keyed by seed + k, as the reference's seeds)."""
-    if teacher is not None and not isinstance(teacher, CriticalPathRule):
-        raise NotImplementedError("the CUDA rollout executes CriticalPathRule natively")
     if rollouts <= 0:
         return 1.0
-    rb = ctx.rollout_batch(params, rollouts, 0.0, seed, mode="teacher", simulate=False,
-                           trace_steps=True)
+    if teacher is None or is_native_teacher(teacher):
+        rb = ctx.rollout_batch(params, rollouts, 0.0, seed, mode="teacher", simulate=False,
+                               trace_steps=True)
+    else:  # duck-typed teacher: host-stepped actions, replayed in FORCED mode
+        acts = teacher_actions(ctx.graph, ctx.cluster, teacher, rollouts)
+        rb = ctx.rollout_batch(params, rollouts, 0.0, seed, mode="forced", forced=acts,
+                               simulate=False, trace_steps=True)
     st = rb.status.cpu().numpy()
     if (st != 0).any():
         raise RuntimeError(f"teacher rollout failed (status {sorted(set(st.tolist()))})")
@@ -327,10 +338,12 @@ def measure_teacher_agreement(ctx: PolicyContext, params, teacher, rollouts: int
 
 
 def _stage(stage: str, graph, cluster, config: TrainConfig, pconfig: PolicyConfig, params,
-           context=None, batch_size: int = 1, executor=None, world=1, rank=0, group=None):
+           context=None, batch_size: int = 1, executor=None, world=1, rank=0, group=None,
+           teacher=None):
     ctx = context or PolicyContext(graph, cluster, pconfig)
     start_enc = ctx.encode_count
-    tr = BatchedTrainer(ctx, params, config, batch_size, world, rank, group, stage, executor)
+    tr = BatchedTrainer(ctx, params, config, batch_size, world, rank, group, stage, executor,
+                        teacher=teacher)
     seeds = _episode_seeds(config, stage)
     curve = []
     best_mk, best_assign = None, None
@@ -367,9 +380,12 @@ def _stage(stage: str, graph, cluster, config: TrainConfig, pconfig: PolicyConfi
 
 def imitation_stage(graph, cluster, config, pconfig, params, teacher=None, context=None,
                     batch_size: int = 1, **kw):
-    """Teacher-forced behavioural cloning of CriticalPathRule (training.py:129-155)."""
-    if teacher is not None and not isinstance(teacher, CriticalPathRule):
-        raise NotImplementedError("the CUDA trainer imitates CriticalPathRule")
+    """Teacher-forced behavioural cloning (training.py:129-155): CriticalPathRule
+    (the default) runs inside the rollout kernel; any other teacher with the
+    reference's select / place interface is stepped on the host per episode
+    and its actions replayed in FORCED mode."""
+    if teacher is not None and not is_native_teacher(teacher):
+        kw["teacher"] = teacher
     return _stage("imitation", graph, cluster, config, pconfig, params, context, batch_size, **kw)
 
 

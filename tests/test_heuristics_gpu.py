@@ -61,3 +61,51 @@ def test_critical_path_assign_best_of_trials():
     assert critical_path_assign(g, cl, trials=1, seed=0).engine == "critical_path"
     with pytest.raises(ValueError):
         critical_path_assign(g, cl, trials=0)
+
+
+class _DuckRule:
+    """A teacher the kernel does not know: the reference select / place API."""
+
+    def __init__(self, rule):
+        self.rule = rule
+
+    def select(self, candidates):
+        return self.rule.select(candidates)
+
+    def place(self, v, timeline):
+        return self.rule.place(v, timeline)
+
+
+def test_duck_teacher_matches_native_teacher_mode():
+    """An arbitrary teacher object is stepped on the host and replayed in
+    FORCED mode: the same actions and log-probs as the native CriticalPathRule
+    teacher, and imitation training with it gives the same parameters."""
+    import torch
+
+    from paper_2505_23131_b200.heuristics import CriticalPathRule
+    from paper_2505_23131_b200.training import TrainConfig, imitation_stage, measure_teacher_agreement
+    g, cl = builders.build_ffnn(8, 4, 16, 4, 2), ClusterSpec.uniform(8, 1e6, 1e5)
+    pc = PolicyConfig()
+    params = init_policy_params(pc, seed=0)
+    ctx = PolicyContext(g, cl, pc)
+    rule = CriticalPathRule(g, cl, ctx.features)
+    duck = _DuckRule(rule)
+    a1, t1 = ctx.rollout(params, 0.0, 3, teacher=rule)
+    a2, t2 = ctx.rollout(params, 0.0, 3, teacher=duck)
+    assert tuple(a1) == tuple(a2)
+    assert [(s.vertex, s.device) for s in t1.steps] == [(s.vertex, s.device) for s in t2.steps]
+    assert np.allclose([s.sel_logprob for s in t1.steps], [s.sel_logprob for s in t2.steps],
+                       rtol=0, atol=1e-12)
+    assert np.allclose([s.plc_logprob for s in t1.steps], [s.plc_logprob for s in t2.steps],
+                       rtol=0, atol=1e-12)
+    assert measure_teacher_agreement(ctx, params, duck, rollouts=4) == \
+        measure_teacher_agreement(ctx, params, rule, rollouts=4)
+    cfg = TrainConfig(episodes=8, lr0=1e-3, lr1=1e-3)
+    r1 = imitation_stage(g, cl, cfg, pc, init_policy_params(pc, seed=0), teacher=rule,
+                         batch_size=4)
+    r2 = imitation_stage(g, cl, cfg, pc, init_policy_params(pc, seed=0), teacher=duck,
+                         batch_size=4)
+    for k in r1.params:
+        assert np.allclose(r1.params[k].data, r2.params[k].data, rtol=0, atol=1e-12), k
+    assert r1.final_loss == pytest.approx(r2.final_loss, rel=1e-12)
+    torch.cuda.synchronize()

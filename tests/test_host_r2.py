@@ -66,3 +66,45 @@ def test_host_critical_path_rule_replays_reference_teacher(policy_golden):
             cands.sort()
         want = [(s["vertex"], s["device"]) for s in case["teacher"]["trace"]]
         assert got == want, case["tag"]
+
+
+class _DuckTeacher:
+    """Any object with the reference teacher interface (select / place)."""
+
+    def __init__(self, rule):
+        self.rule = rule
+
+    def select(self, candidates):
+        return self.rule.select(candidates)
+
+    def place(self, v, timeline):
+        return self.rule.place(v, timeline)
+
+
+def test_duck_teacher_actions_replay_reference_teacher(policy_golden):
+    """policy.teacher_actions steps an arbitrary select / place teacher the
+    way the reference rollout does (policy.py:353-389): wrapping the rule
+    reproduces the reference teacher's (vertex, device) sequence."""
+    import pytest
+
+    from paper_2505_23131_b200.features import static_features
+    from paper_2505_23131_b200.policy import TeacherActionError, teacher_actions
+    for case in policy_golden["cases"]:
+        g = graph_from_golden(case["graph"])
+        cl = ClusterSpec.from_dict(case["cluster"])
+        duck = _DuckTeacher(CriticalPathRule(g, cl, static_features(g, cl.comm_factor)))
+        acts = teacher_actions(g, cl, duck, episodes=2)
+        want = [(s["vertex"], s["device"]) for s in case["teacher"]["trace"]]
+        assert acts.shape == (2, len(g), 2)
+        for e in range(2):
+            assert [tuple(map(int, a)) for a in acts[e]] == want, case["tag"]
+
+    class Bad:
+        def select(self, candidates):
+            return max(candidates) + 1
+
+        def place(self, v, timeline):
+            return 0
+
+    with pytest.raises(TeacherActionError):
+        teacher_actions(g, cl, Bad())
