@@ -277,6 +277,14 @@ int fp_pg_reduce(fp_policy *pol, const double *grad_rows, const double *grad_ep,
                  const int32_t *assign, const double *alpha, double beta, int32_t B,
                  void *stream);
 int fp_policy_backward(fp_policy *pol, double *grad, void *stream);
+/* per_step message passing (reference mp_mode="per_step"): the whole flat
+ * gradient of sum_e alpha[e] * sum lp_e + beta * sum ent_e for a per_step
+ * REINFORCE rollout (FP_FLAG_PER_STEP with grad_rows), backpropagated
+ * through the encode of every step, episodes and steps in order -- replaces
+ * fp_pg_reduce + fp_policy_backward for per_step rollouts. */
+int fp_pg_reduce_per_step(fp_policy *pol, const double *grad_rows, const double *grad_ep,
+                          const double *alpha, double beta, int32_t B, double *grad,
+                          void *stream);
 int fp_sgd_step(double *params, const double *grad, int64_t count, double lr, void *stream);
 /* as fp_sgd_step, skipped on the device when *skip != 0 (skip: device int32,
  * e.g. a sticky "some rollout of this batch failed" flag), so a trainer can

@@ -130,6 +130,6 @@ class FpRolloutArgs(ctypes.Structure):
 EXPORTED = EXPORTED + (
     "fp_policy_create", "fp_policy_destroy", "fp_policy_set_encoder", "fp_policy_prepare", "fp_policy_table",
     "fp_rollout_workspace_size", "fp_rollout_batch", "fp_grad_ep_stride", "fp_grad_rec_stride",
-    "fp_pg_reduce", "fp_policy_backward", "fp_sgd_step", "fp_sgd_step_masked",
+    "fp_pg_reduce", "fp_pg_reduce_per_step", "fp_policy_backward", "fp_sgd_step", "fp_sgd_step_masked",
     "fp_tc_gemm_selftest",
 )

@@ -17,9 +17,12 @@
 //      decision, timeline commit -- the per_episode kernels' math, with the
 //      episode state in the workspace between launches.
 //
-// After n steps the assignments are scored by the compact simulator.
-// Forward only (sampling / greedy / forced / teacher, log-probs, entropies):
-// the per_step REINFORCE backward would differentiate through n encodes.
+// After n steps the assignments are scored by the compact simulator.  With
+// grad_rows the step kernel also records each decision (normalised device
+// features, vertex / device, candidate bitset) for fp_pg_reduce_per_step,
+// which backpropagates through every step's encode (end of this file).
+#include <vector>
+
 #include "fp_rollout.cuh"
 
 namespace fp {
@@ -106,6 +109,7 @@ ps_step_kernel(DevProblem PR, DevPolicy PO, DevPolicy PB, fp_rollout_args A, PsS
     __shared__ double cs[1024];
     __shared__ int cid[1024];
     __shared__ int k_sm;
+    __shared__ uint32_t cw_sm[32];  // this step's candidate bitset (REINFORCE record)
     __shared__ double sd_part[kPsWarps - 1][MAXD * HPL <= 16 ? MAXD : 1][MAXD * HPL <= 16 ? 32 * HPL : 1];
     const int lane = lane_id(), warp = threadIdx.x >> 5;
     const int ep = blockIdx.x;
@@ -134,6 +138,7 @@ ps_step_kernel(DevProblem PR, DevPolicy PO, DevPolicy PB, fp_rollout_args A, PsS
             m &= m - 1;
             cid[q++] = lane * 32 + b;
         }
+        cw_sm[lane] = cw;
         if (lane == 31) k_sm = incl;
     }
     __syncthreads();
@@ -485,10 +490,16 @@ ps_step_kernel(DevProblem PR, DevPolicy PO, DevPolicy PB, fp_rollout_args A, PsS
         if (A.step_vd) A.step_vd[2 * o + 1] = jdx;
     }
     if (lane == 0 && A.step_argmax) A.step_argmax[2 * o + 1] = pam;
+    if (A.grad_rows) {  // REINFORCE record (replayed by fp_pg_reduce_per_step)
+        double *rec = A.grad_rows + o * grad_rec_stride(D, W);
+        for (int i = lane; i < 5 * D; i += 32) rec[i] = xn[i];
+        if (lane == 0) { *(int2 *)(rec + 6 * D) = make_int2(v, jdx); rec[6 * D + 3] = (double)v; }
+        if (lane < W) ((uint32_t *)(rec + 6 * D + 4))[lane] = cw_sm[lane];
+    }
 }
 
 // assignments out (unplaced -> 0 for the simulator, fixed up afterwards)
-__global__ void ps_finish_kernel(PsState S, fp_rollout_args A, int n, int fixup) {
+__global__ void ps_finish_kernel(PsState S, fp_rollout_args A, int n, int fixup, int64_t gstride) {
     const int64_t total = (int64_t)A.B * n;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -502,6 +513,11 @@ __global__ void ps_finish_kernel(PsState S, fp_rollout_args A, int n, int fixup)
                 A.status[ep] = S.stat[ep];
                 if (A.makespan) A.makespan[ep] = 0.0;
             }
+        }
+        if (fixup && A.grad_ep && i % n == 0) {  // replay header: chain completed, epsilon
+            double *g = A.grad_ep + (size_t)ep * gstride;
+            g[2 * n] = S.stat[ep] == FP_EP_OK ? 1.0 : 0.0;
+            g[2 * n + 1] = A.epsilon;
         }
     }
 }
@@ -521,10 +537,7 @@ int per_step_rollout(const fp_problem *p, const fp_policy *pol, const fp_rollout
         set_error("per_step message passing supports graphs up to 1024 ops");
         return FP_ERR_UNSUPPORTED;
     }
-    if (a.grad_rows) {
-        set_error("per_step rollouts are forward only (no REINFORCE rows)");
-        return FP_ERR_UNSUPPORTED;
-    }
+
     if (PO.h % 8 != 0 || PO.h > 64) {
         set_error("per_step message passing needs hidden in {8, 16, 32, 64}");
         return FP_ERR_UNSUPPORTED;
@@ -532,6 +545,10 @@ int per_step_rollout(const fp_problem *p, const fp_policy *pol, const fp_rollout
     const int n = PR.n, B = a.B;
     const PsLayout L = ps_layout(n, B, PO.h, PO.K, PO.n_enc, PR.W, PO.tc != 0);
     if (ws_needed) { *ws_needed = L.bytes; return FP_OK; }
+    if (a.grad_rows && !a.grad_ep) {
+        set_error("a per_step REINFORCE rollout needs grad_ep with grad_rows");
+        return FP_ERR_INVALID;
+    }
     if (!a.workspace || a.workspace_bytes < L.bytes) {
         set_error("workspace too small for the per_step rollout (see fp_rollout_workspace_size)");
         return FP_ERR_INVALID;
@@ -581,7 +598,7 @@ int per_step_rollout(const fp_problem *p, const fp_policy *pol, const fp_rollout
         if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FP_ERR_CUDA; }
     }
     const int fb = (int)std::min<int64_t>(((int64_t)B * n + 255) / 256, 4096);
-    ps_finish_kernel<<<fb, 256, 0, st>>>(S, a, n, 0);
+    ps_finish_kernel<<<fb, 256, 0, st>>>(S, a, n, 0, 0);
     // status of episodes that finished cleanly, then the simulator's verdict
     fp_rollout_args a2 = a;
     if (a.simulate) {
@@ -591,10 +608,282 @@ int per_step_rollout(const fp_problem *p, const fp_policy *pol, const fp_rollout
     } else {
         cudaMemsetAsync(a.status, 0, sizeof(int32_t) * B, st);
     }
-    ps_finish_kernel<<<fb, 256, 0, st>>>(S, a2, n, 1);
+    ps_finish_kernel<<<fb, 256, 0, st>>>(S, a2, n, 1, grad_ep_stride(n, PO.h, PR.d));
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FP_ERR_CUDA; }
     return FP_OK;
 }
 
 }  // namespace fp
+
+// ---------------------------------------------------------------------------
+// per_step REINFORCE (reference sim_rl_stage with mp_mode="per_step":
+// policy.py:353-371 + training.py:181-216, autodiff of nn.py): the log-probs
+// of step t depend on that step's encodes, so the gradient backpropagates
+// through one encode per step.  Per (episode, step), in order: the encoders'
+// dynamic input columns are set to the placements before the step, the
+// encode runs with its backward intermediates, ps_adjoint_kernel forms the
+// head-table adjoints of this step's two decisions (SEL logits of the
+// candidates; PLC A row, G rows via the per-device sums, M, w2, b2), folded
+// with (alpha_e, beta), and the per-snapshot backward (fp_policy_backward)
+// turns them into a flat gradient that is accumulated in (episode, step)
+// order.  Records come from the forward per_step rollout (normalised device
+// features, vertex / device, candidate bitset).  Sequential and launch-heavy
+// (about 30 launches per decision): the correctness path of the per_step
+// ablation, not a throughput path.
+// ---------------------------------------------------------------------------
+namespace fp {
+
+// dyn columns (H0 cols 5, 6 of every encoder) = placements of steps < t
+__global__ void ps_set_dyn_kernel(DevPolicy P, const double *rec, int rstride, int t, int D) {
+    extern __shared__ int dv[];
+    const int n = P.n;
+    for (int v = threadIdx.x; v < n; v += blockDim.x) dv[v] = -1;
+    __syncthreads();
+    for (int s = threadIdx.x; s < t; s += blockDim.x) {
+        const int2 vj = *(const int2 *)(rec + (size_t)s * rstride + 6 * D);
+        dv[vj.x] = vj.y;
+    }
+    __syncthreads();
+    for (int v = threadIdx.x; v < n; v += blockDim.x) {
+        const int d = dv[v];
+        for (int e = 0; e < P.n_enc; ++e) {
+            double *H0 = P.H[e][0];
+            H0[(size_t)v * 7 + 5] = d < 0 ? 0.0 : 1.0;
+            H0[(size_t)v * 7 + 6] = d < 0 ? 0.0 : __ddiv_rn((double)(d + 1), (double)D);
+        }
+    }
+}
+
+template <int MAXD, int HPL>
+__global__ void __launch_bounds__(32)
+ps_adjoint_kernel(DevProblem PR, DevPolicy P, const double *__restrict__ rec, int rstride, int t,
+                  double al, double beta, double eps) {
+    extern __shared__ int cl[];
+    const int lane = lane_id();
+    const int n = PR.n, D = PR.d, W = PR.W, h = P.h;
+    const double ome = 1.0 - eps, slope = P.slope;
+    for (int i = lane; i < n * h; i += 32) { P.dA[i] = 0.0; P.dG[i] = 0.0; }
+    for (int v = lane; v < n; v += 32) P.ds[v] = 0.0;
+    for (int k = lane; k < 6 * h + 1; k += 32) P.dsmall[h + k] = 0.0;
+    const double *r = rec + (size_t)t * rstride;
+    const int2 vj = *(const int2 *)(r + 6 * D);
+    const int v = vj.x, jdx = vj.y;
+    __syncwarp();
+    // ---- SEL: this step's candidates, logits from this step's encode ----
+    {
+        const uint32_t cw = lane < W ? ((const uint32_t *)(r + 6 * D + 4))[lane] : 0u;
+        const int pc = __popc(cw);
+        const int incl = warp_inclusive_scan(pc);
+        const int k = __shfl_sync(FP_FULL_MASK, incl, 31);
+        int o = incl - pc;
+        uint32_t m = cw;
+        while (m) {
+            const int b = __ffs(m) - 1;
+            m &= m - 1;
+            cl[o++] = lane * 32 + b;
+        }
+        __syncwarp();
+        double mx = -INFINITY;
+        for (int i = lane; i < k; i += 32) mx = fmax(mx, P.s[cl[i]]);
+        mx = warp_max(mx);
+        double tot = 0.0;
+        for (int i = lane; i < k; i += 32) tot += exp(P.s[cl[i]] - mx);
+        tot = warp_sum(tot);
+        const double ek = eps / (double)k;
+        double qp = 0.0;
+        for (int i = lane; i < k; i += 32) {
+            const double p = exp(P.s[cl[i]] - mx) / tot;
+            const double mix = __dadd_rn(__dmul_rn(p, ome), ek);
+            const double lm = log(__dadd_rn(mix, 1e-30));
+            qp += -ome * (lm + mix / __dadd_rn(mix, 1e-30)) * p;
+        }
+        qp = warp_sum(qp);
+        const double pv = exp(P.s[v] - mx) / tot;
+        const double mv = __dadd_rn(__dmul_rn(pv, ome), ek);
+        const double c1 = ome * pv / __dadd_rn(mv, 1e-30);
+        for (int i = lane; i < k; i += 32) {
+            const int u = cl[i];
+            const double p = exp(P.s[u] - mx) / tot;
+            const double mix = __dadd_rn(__dmul_rn(p, ome), ek);
+            const double lm = log(__dadd_rn(mix, 1e-30));
+            const double q = -ome * (lm + mix / __dadd_rn(mix, 1e-30));
+            P.ds[u] = al * (c1 * ((u == v ? 1.0 : 0.0) - p)) + beta * (p * (q - qp));
+        }
+    }
+    // ---- PLC: pre-activations from this step's tables, lane = hidden column ----
+    double Sd[MAXD][HPL], pre[MAXD][HPL];
+#pragma unroll
+    for (int d = 0; d < MAXD; ++d)
+#pragma unroll
+        for (int q = 0; q < HPL; ++q) Sd[d][q] = 0.0;
+    for (int s = 0; s < t; ++s) {
+        const int2 us = *(const int2 *)(rec + (size_t)s * rstride + 6 * D);
+#pragma unroll
+        for (int q = 0; q < HPL; ++q) {
+            const int j = lane + 32 * q;
+            const double g = j < h ? P.G[(size_t)us.x * h + j] : 0.0;
+#pragma unroll
+            for (int d = 0; d < MAXD; ++d)
+                if (d == us.y) Sd[d][q] += g;
+        }
+    }
+    const double *w2p = P.W(PR_PLC_H2_W);
+    const double b2p = P.W(PR_PLC_H2_B)[0];
+    double lg[MAXD];
+#pragma unroll
+    for (int d = 0; d < MAXD; ++d) {
+        double part = 0.0;
+#pragma unroll
+        for (int q = 0; q < HPL; ++q) {
+            const int j = lane + 32 * q;
+            pre[d][q] = 0.0;
+            if (j >= h || d >= D) continue;
+            double a = P.A[(size_t)v * h + j] + Sd[d][q] + P.c[j];
+            for (int c = 0; c < 5; ++c) a = fma(r[d * 5 + c], P.M[c * h + j], a);
+            pre[d][q] = a;
+            part = fma(lk(a, slope), w2p[j], part);
+        }
+        lg[d] = d < D ? warp_sum(part) + b2p : -INFINITY;
+    }
+    double mx = -INFINITY;
+#pragma unroll
+    for (int d = 0; d < MAXD; ++d) mx = fmax(mx, lg[d]);
+    double ed[MAXD], tot = 0.0;
+#pragma unroll
+    for (int d = 0; d < MAXD; ++d) { ed[d] = d < D ? exp(lg[d] - mx) : 0.0; tot += ed[d]; }
+    const double ekd = eps / (double)D;
+    double pd[MAXD], qd[MAXD], qp = 0.0, pj = 0.0, mj = 0.0;
+#pragma unroll
+    for (int d = 0; d < MAXD; ++d) {
+        pd[d] = qd[d] = 0.0;
+        if (d >= D) continue;
+        pd[d] = ed[d] / tot;
+        const double mix = __dadd_rn(__dmul_rn(pd[d], ome), ekd);
+        const double lm = log(__dadd_rn(mix, 1e-30));
+        qd[d] = -ome * (lm + mix / __dadd_rn(mix, 1e-30));
+        qp += qd[d] * pd[d];
+        if (d == jdx) { pj = pd[d]; mj = mix; }
+    }
+    const double g0 = ome * pj / __dadd_rn(mj, 1e-30);
+    double cd[MAXD], db2 = 0.0;
+#pragma unroll
+    for (int d = 0; d < MAXD; ++d) {
+        cd[d] = d < D ? al * (g0 * ((d == jdx ? 1.0 : 0.0) - pd[d])) + beta * (pd[d] * (qd[d] - qp))
+                      : 0.0;
+        db2 += cd[d];
+    }
+#pragma unroll
+    for (int q = 0; q < HPL; ++q) {
+        const int j = lane + 32 * q;
+        if (j >= h) continue;
+        double dA = 0.0, dw = 0.0, dM[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+        double dS[MAXD];
+#pragma unroll
+        for (int d = 0; d < MAXD; ++d) {
+            dS[d] = 0.0;
+            if (d >= D) continue;
+            dS[d] = cd[d] * w2p[j] * lkd(pre[d][q], slope);
+            dA += dS[d];
+            dw = fma(cd[d], lk(pre[d][q], slope), dw);
+            for (int c = 0; c < 5; ++c) dM[c] = fma(r[d * 5 + c], dS[d], dM[c]);
+        }
+        P.dA[(size_t)v * h + j] = dA;
+        for (int c = 0; c < 5; ++c) P.dsmall[h + c * h + j] = dM[c];
+        P.dsmall[6 * h + j] = dw;
+        for (int s = 0; s < t; ++s) {  // G rows of the placed vertices, through S_d
+            const int2 us = *(const int2 *)(rec + (size_t)s * rstride + 6 * D);
+#pragma unroll
+            for (int d = 0; d < MAXD; ++d)
+                if (d == us.y) P.dG[(size_t)us.x * h + j] = dS[d];
+        }
+    }
+    if (lane == 0) P.dsmall[7 * h] = db2;
+}
+
+__global__ void axpy_kernel(double *y, const double *x, int64_t count) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < count) y[i] += x[i];
+}
+
+template <int MAXD, int HPL>
+static void ps_adjoint_launch(const DevProblem &PR, const DevPolicy &P, const double *rec,
+                              int rstride, int t, double al, double beta, double eps,
+                              cudaStream_t st) {
+    ps_adjoint_kernel<MAXD, HPL><<<1, 32, 4 * PR.n, st>>>(PR, P, rec, rstride, t, al, beta, eps);
+}
+
+}  // namespace fp
+
+extern "C" int fp_policy_backward(fp_policy *pol, double *grad, void *stream);
+
+#define FP_PS_CUDA(call)                                                   \
+    do {                                                                   \
+        cudaError_t e_ = (call);                                           \
+        if (e_ != cudaSuccess) {                                           \
+            fp::set_error(std::string(#call) + ": " + cudaGetErrorString(e_)); \
+            return FP_ERR_CUDA;                                            \
+        }                                                                  \
+    } while (0)
+
+extern "C" int fp_pg_reduce_per_step(fp_policy *pol, const double *grad_rows,
+                                     const double *grad_ep, const double *alpha, double beta,
+                                     int32_t B, double *grad, void *stream) {
+    using namespace fp;
+    if (!pol || !grad_rows || !grad_ep || !alpha || !grad || B <= 0) {
+        set_error("bad pg_reduce_per_step arguments");
+        return FP_ERR_INVALID;
+    }
+    DevPolicy &P = pol->dev;
+    const DevProblem &PR = pol->problem->dev;
+    if (P.forest || P.tc || pol->fused_encoder) {
+        set_error("per_step REINFORCE needs the fp64 split encoder with explicit path lists");
+        return FP_ERR_UNSUPPORTED;
+    }
+    if (!P.params) { set_error("fp_policy_prepare must run before the backward"); return FP_ERR_INVALID; }
+    cudaStream_t st = (cudaStream_t)stream;
+    const int n = PR.n, D = PR.d, h = P.h;
+    const int rstride = grad_rec_stride(D, PR.W);
+    const int64_t gstride = grad_ep_stride(n, h, D);
+    std::vector<double> hdr((size_t)B * 2), al((size_t)B);
+    FP_PS_CUDA(cudaMemcpy2DAsync(hdr.data(), 2 * sizeof(double), grad_ep + 2 * n,
+                              gstride * sizeof(double), 2 * sizeof(double), B,
+                              cudaMemcpyDeviceToHost, st));
+    FP_PS_CUDA(cudaMemcpyAsync(al.data(), alpha, sizeof(double) * B, cudaMemcpyDeviceToHost, st));
+    FP_PS_CUDA(cudaStreamSynchronize(st));
+    double *tmp = nullptr;
+    FP_PS_CUDA(cudaMallocAsync((void **)&tmp, sizeof(double) * pol->n_params, st));
+    FP_PS_CUDA(cudaMemsetAsync(grad, 0, sizeof(double) * pol->n_params, st));
+    const int ab = (int)((pol->n_params + 255) / 256);
+    int rc = FP_OK;
+    for (int e = 0; e < B && rc == FP_OK; ++e) {
+        if (hdr[2 * e] == 0.0) continue;  // failed chain: no contribution
+        const double eps = hdr[2 * e + 1];
+        const double *rec = grad_rows + (size_t)e * n * rstride;
+        for (int t = 0; t < n && rc == FP_OK; ++t) {
+            ps_set_dyn_kernel<<<1, 256, 4 * n, st>>>(P, rec, rstride, t, D);
+            rc = gnn_encode_rows(P, st, true, true);
+            if (rc) break;
+            if (h <= 32) {
+                if (D <= 4) ps_adjoint_launch<4, 1>(PR, P, rec, rstride, t, al[e], beta, eps, st);
+                else if (D <= 8) ps_adjoint_launch<8, 1>(PR, P, rec, rstride, t, al[e], beta, eps, st);
+                else if (D <= 16) ps_adjoint_launch<16, 1>(PR, P, rec, rstride, t, al[e], beta, eps, st);
+                else ps_adjoint_launch<32, 1>(PR, P, rec, rstride, t, al[e], beta, eps, st);
+            } else {
+                if (D <= 8) ps_adjoint_launch<8, 2>(PR, P, rec, rstride, t, al[e], beta, eps, st);
+                else if (D <= 16) ps_adjoint_launch<16, 2>(PR, P, rec, rstride, t, al[e], beta, eps, st);
+                else ps_adjoint_launch<32, 2>(PR, P, rec, rstride, t, al[e], beta, eps, st);
+            }
+            rc = fp_policy_backward(pol, tmp, st);
+            if (rc) break;
+            axpy_kernel<<<ab, 256, 0, st>>>(grad, tmp, pol->n_params);
+        }
+    }
+    // the policy's own tables back to the per-episode encode (dyn = 0)
+    ps_set_dyn_kernel<<<1, 256, 4 * n, st>>>(P, grad_rows, rstride, 0, D);
+    if (rc == FP_OK) rc = gnn_encode_rows(P, st, true, true);
+    cudaFreeAsync(tmp, st);
+    cudaError_t err = cudaGetLastError();
+    if (rc == FP_OK && err != cudaSuccess) { set_error(cudaGetErrorString(err)); return FP_ERR_CUDA; }
+    return rc;
+}

@@ -455,12 +455,25 @@ class PolicyContext:
         alpha = torch.as_tensor(alpha, dtype=torch.float64, device="cuda").reshape(B).contiguous()
         if grad is None:
             grad = torch.empty(self.layout.size, dtype=torch.float64, device="cuda")
-        N.check(N.lib().fp_pg_reduce(self.handle, N.ptr(batch.grad_rows), N.ptr(batch.grad_ep),
-                                     N.ptr(batch.assign), N.ptr(alpha), ctypes.c_double(beta),
-                                     ctypes.c_int32(B), N.stream_ptr(stream)))
-        N.check(N.lib().fp_policy_backward(self.handle, N.ptr(grad), N.stream_ptr(stream)))
+        self.reduce_gradient(batch.grad_rows, batch.grad_ep, batch.assign, alpha, beta, B, grad,
+                             stream)
         batch._alpha = alpha
         return grad
+
+    def reduce_gradient(self, grad_rows, grad_ep, assign, alpha, beta: float, B: int, grad,
+                        stream=None) -> None:
+        """Flat gradient of a REINFORCE rollout's decision records: the
+        replay + episode reduction + backward (per_episode), or the
+        backpropagation through every step's encode (per_step)."""
+        if self.per_step:
+            N.check(N.lib().fp_pg_reduce_per_step(
+                self.handle, N.ptr(grad_rows), N.ptr(grad_ep), N.ptr(alpha),
+                ctypes.c_double(beta), ctypes.c_int32(B), N.ptr(grad), N.stream_ptr(stream)))
+            return
+        N.check(N.lib().fp_pg_reduce(self.handle, N.ptr(grad_rows), N.ptr(grad_ep), N.ptr(assign),
+                                     N.ptr(alpha), ctypes.c_double(beta), ctypes.c_int32(B),
+                                     N.stream_ptr(stream)))
+        N.check(N.lib().fp_policy_backward(self.handle, N.ptr(grad), N.stream_ptr(stream)))
 
     def grad_rec_stride(self) -> int:
         s = ctypes.c_int64()

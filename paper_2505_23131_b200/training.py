@@ -284,10 +284,8 @@ class BatchedTrainer:
             self.upd.alpha(mk, alpha, ng)
             beta = -self.config.entropy_weight / ng
         if Bl:
-            N.check(N.lib().fp_pg_reduce(ctx.handle, N.ptr(out.grad_rows), N.ptr(out.grad_ep),
-                                         N.ptr(out.assign), N.ptr(alpha), ctypes.c_double(beta),
-                                         ctypes.c_int32(Bl), N.stream_ptr()))
-            N.check(N.lib().fp_policy_backward(ctx.handle, N.ptr(self.grad), N.stream_ptr()))
+            ctx.reduce_gradient(out.grad_rows, out.grad_ep, out.assign, alpha, beta, Bl,
+                                self.grad)
         else:
             self.grad.zero_()
         self.upd.finish(mk, ng)

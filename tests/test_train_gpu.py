@@ -170,3 +170,59 @@ def test_trainer_failed_rollout_masks_update_and_raises(torch_cuda):
     assert (tr.flat == before).all()   # masked on the device
     with pytest.raises(RuntimeError, match="rollout failed"):
         tr.check()
+
+
+@pytest.fixture(scope="module")
+def per_step_grad_golden():
+    import json
+    from pathlib import Path
+    return json.loads((Path(__file__).parent / "golden" / "per_step_grad.json").read_text())
+
+
+def test_per_step_rl_gradient_matches_reference(per_step_grad_golden, torch_cuda):
+    """per_step REINFORCE: the reference's sampled per_step episode, forced on
+    the GPU, gives the reference's full parameter gradient (backpropagated
+    through one encode per step, reference autodiff) within 1e-8."""
+    for case in per_step_grad_golden["cases"]:
+        g, cl, pc, ctx = _ctx(case)
+        assert ctx.per_step
+        params = init_policy_params(pc, seed=0)
+        rg = case["rl_grad"]
+        acts = [(x["vertex"], x["device"]) for x in rg["trace"]]
+        rb = ctx.rollout_batch(params, 1, rg["epsilon"], 0, mode="forced",
+                               forced=np.asarray(acts).reshape(1, -1, 2), grad=True,
+                               trace_steps=True)
+        assert int(rb.status.cpu()[0]) == 0, case["tag"]
+        assert float(rb.makespan.cpu()[0]) == rg["makespan"], case["tag"]
+        lp = rb.step_lp.cpu().numpy()[0]
+        np.testing.assert_allclose(lp[:, 0], [x["sel_logprob"] for x in rg["trace"]],
+                                   rtol=0, atol=1e-9)
+        grad = ctx.policy_gradient(rb, [-rg["advantage"]], -rg["entropy_weight"])
+        _compare(ctx, grad, rg["grads"])
+
+
+def test_per_step_imitation_gradient_matches_reference(per_step_grad_golden, torch_cuda):
+    for case in per_step_grad_golden["cases"]:
+        g, cl, pc, ctx = _ctx(case)
+        rb = ctx.rollout_batch(init_policy_params(pc, seed=0), 1, 0.0, 0, mode="teacher",
+                               grad=True)
+        assert int(rb.status.cpu()[0]) == 0, case["tag"]
+        grad = ctx.policy_gradient(rb, [-1.0], 0.0)
+        _compare(ctx, grad, case["imitation_grad"]["grads"])
+
+
+def test_per_step_sim_rl_stage_trains(torch_cuda):
+    """sim_rl_stage with mp_mode="per_step" (the reference's acceptance
+    criterion 8 setup): trains, n x the encoder invocations of per_episode."""
+    from helpers import cluster2, fixture6
+    from paper_2505_23131_b200.training import TrainConfig, sim_rl_stage
+    g, cl = fixture6(), cluster2()
+    res = {}
+    for mode in ("per_episode", "per_step"):
+        pc = PolicyConfig(hidden=16, k_rounds=2, mp_mode=mode)
+        res[mode] = sim_rl_stage(g, cl, TrainConfig(episodes=8, seed=0), pc,
+                                 init_policy_params(pc, seed=0), batch_size=1)
+        assert np.isfinite(res[mode].best_makespan)
+    # reference criterion 8's counts at one episode per update
+    assert res["per_episode"].encoder_invocations == 2 * 8
+    assert res["per_step"].encoder_invocations == len(g) * res["per_episode"].encoder_invocations
