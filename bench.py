@@ -192,6 +192,8 @@ def bench_config(args, world: int, desc: str) -> dict:
             "global_batch": args.batch * world, "mode": args.mode, "epsilon": EPSILON,
             "policy": f"hidden 32, K 2, {args.mp_mode}" + (
                 "" if args.encoder == "dmma" else f", {args.encoder} encoder"),
+            "outputs": ("assignments, makespans + per-step trace (log-probs, entropies, argmax)"
+                        if args.full_outputs else "assignments + makespans"),
             "parallelism": f"episode-dp{world}",
             "l2": "GPU arm: flushed between timed steps (256 MiB write); e2e: steps pipelined "
                   "(D2H on a side stream, double-buffered outputs), 256 MiB flush on the side "
@@ -302,7 +304,7 @@ def run_ours(args):
         trainer = BatchedTrainer(ctx, params, TrainConfig(episodes=10 ** 6), batch_size=B,
                                  world=world, rank=rank)
     flat = ctx.flat_params(params)
-    out = ctx.alloc_batch(B, grad=train)
+    out = ctx.alloc_batch(B, grad=train, trace_steps=args.full_outputs)
     stream = torch.cuda.current_stream()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     ep_base = rank * B
@@ -371,7 +373,7 @@ def run_ours(args):
     host_assign = [torch.empty((B, n), dtype=torch.int32).pin_memory() for _ in range(2)]
     host_mk = [torch.empty(B, dtype=torch.float64).pin_memory() for _ in range(2)]
     dev_params = [torch.empty_like(flat) for _ in range(2)]
-    outs = [out, ctx.alloc_batch(B, grad=train)]
+    outs = [out, ctx.alloc_batch(B, grad=train, trace_steps=args.full_outputs)]
     copy_stream = torch.cuda.Stream()
     done_ev = [torch.cuda.Event() for _ in range(2)]
     free_ev = [torch.cuda.Event() for _ in range(2)]
@@ -575,6 +577,9 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-step-seconds", type=float, default=4.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--full-outputs", action="store_true",
+                    help="also produce the per-step trace (log-probs, entropies, argmax) the "
+                         "reference rollout returns: the general, non-lean kernel")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -168,7 +168,7 @@ __device__ __forceinline__ void gnn_agg_body(const DevPolicy &P, int k, int e_, 
 }
 
 template <int H, bool F32 = false>
-__global__ void __launch_bounds__(256) gnn_agg_kernel(DevPolicy P, int k) {
+__global__ void __launch_bounds__(256, 5) gnn_agg_kernel(DevPolicy P, int k) {
     extern __shared__ __align__(16) double gsm[];
     gnn_agg_body<H, F32>(P, k, blockIdx.y, blockIdx.x, gridDim.x, gsm);
 }

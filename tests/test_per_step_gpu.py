@@ -87,7 +87,7 @@ def test_per_step_sampled_batch_matches_oracle_draws(which):
         assert mk[b] == omk
 
 
-def test_per_step_bad_action_and_no_grad():
+def test_per_step_bad_action_and_failed_episodes_skip_gradient():
     g, cl = builders.build_ffnn(8, 4, 16, 4, 2), ClusterSpec.uniform(8, 1e6, 1e5)
     pc = PolicyConfig(mp_mode="per_step")
     ctx = PolicyContext(g, cl, pc)
@@ -98,6 +98,8 @@ def test_per_step_bad_action_and_no_grad():
     acts[1, 20, 0] = 10 ** 6
     rb = ctx.rollout_batch(params, 2, 0.0, 0, mode="forced", forced=acts)
     assert rb.status.cpu().numpy().tolist() == [3, 3]
-    from paper_2505_23131_b200._native import NativeError
-    with pytest.raises(NativeError):
-        ctx.rollout_batch(params, 2, 0.2, 0, grad=True)
+    # per_step REINFORCE rollouts are supported; failed episodes contribute nothing
+    rb = ctx.rollout_batch(params, 2, 0.0, 0, mode="forced", forced=acts, grad=True)
+    assert rb.status.cpu().numpy().tolist() == [3, 3]
+    grad = ctx.policy_gradient(rb, [1.0, 1.0], 0.0)
+    assert float(grad.abs().max()) == 0.0
