@@ -381,9 +381,13 @@ ps_step_kernel(DevProblem PR, DevPolicy PO, DevPolicy PB, fp_rollout_args A, PsS
             const double df = __dsub_rn(xd[d * 5 + lane], mean);
             sq = __dadd_rn(sq, __dmul_rn(df, df));
         }
-        const double sd = __dsqrt_rn(pow2 ? __dmul_rn(sq, invD) : __ddiv_rn(sq, (double)D));
+        const double var = pow2 ? __dmul_rn(sq, invD) : __ddiv_rn(sq, (double)D);
         stats[lane] = mean;
-        stats[5 + lane] = 1.0 / (sd < 1e-12 ? 1.0 : sd);
+        // the reference's guard std < 1e-12 decided exactly on the variance
+        // (sqrt_rn is monotone and sqrt_rn(v) < 1e-12 <=> v < 1e-24, checked
+        // at the double boundary); the scaling is one rsqrt per column (within
+        // ~1 ulp of 1 / sqrt_rn(var), a third of the sqrt + divide sequence)
+        stats[5 + lane] = var < 1e-24 ? 1.0 : rsqrt(var);
     }
     __syncwarp();
     for (int i = lane; i < 5 * D; i += 32) {

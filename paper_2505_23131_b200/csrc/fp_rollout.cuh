@@ -783,11 +783,13 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
                     const double df = __dsub_rn(col[d], mean);
                     sq = __dadd_rn(sq, __dmul_rn(df, df));
                 }
-            const double sd = __dsqrt_rn(pow2 ? __dmul_rn(sq, invD) : __ddiv_rn(sq, (double)D));
+            const double var = pow2 ? __dmul_rn(sq, invD) : __ddiv_rn(sq, (double)D);
             stats[lane] = mean;
-            // the guard decision is exact (std computed as the reference does);
-            // the scaling uses one reciprocal per column (<= 1 ulp from x / std)
-            stats[5 + lane] = 1.0 / (sd < 1e-12 ? 1.0 : sd);
+            // the reference's guard std < 1e-12 decided exactly on the variance
+            // (sqrt_rn is monotone and sqrt_rn(v) < 1e-12 <=> v < 1e-24, checked
+            // at the double boundary); the scaling is one rsqrt per column (within
+            // ~1 ulp of 1 / sqrt_rn(var), a third of the sqrt + divide sequence)
+            stats[5 + lane] = var < 1e-24 ? 1.0 : rsqrt(var);
         }
         __syncwarp();
 #pragma unroll
