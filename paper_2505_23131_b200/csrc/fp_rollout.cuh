@@ -634,14 +634,16 @@ __device__ __forceinline__ void sel_chain_wide(const DevProblem &PR, const DevPo
 // ---------------------------------------------------------------------------
 // PLC warp
 // ---------------------------------------------------------------------------
-template <int MAXD, int HPL, bool GRAD, bool WIDE = false, bool LEAN = false>
+// FULLD: the cluster has exactly MAXD devices, so every `d < D` / `lane < D`
+// test folds away at compile time (the hot LEAN instantiations).
+template <int MAXD, int HPL, bool GRAD, bool WIDE = false, bool LEAN = false, bool FULLD = false>
 __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &PO,
                                          const fp_rollout_args &A, uint8_t *nb, uint8_t *sb,
                                          const EpLayout &L, int ep, bool want_lp,
                                          bool want_amax) {
     static_assert(!(WIDE && GRAD), "REINFORCE rows are produced by the compact path only");
     const int lane = lane_id();
-    const int n = PR.n, D = PR.d, h = PO.h;
+    const int n = PR.n, D = FULLD ? MAXD : PR.d, h = PO.h;
     constexpr int LOGD = PlcLog<MAXD>::v;
     double *tstart = (double *)(nb + L.tstart);
     double *tend = (double *)(nb + L.tend);
@@ -1045,7 +1047,7 @@ __device__ __forceinline__ bool plc_role(unsigned *slots, int warp) {
 // LEAN: the sampling-only instantiation (no forced / teacher / greedy modes,
 // no per-step outputs, no traces) -- a smaller kernel for the throughput path
 // (fewer instruction-fetch stalls with SEL, PLC and simulator code resident).
-template <int MAXD, int HPL, bool GRAD, int EPB, bool SM1, bool LEAN = false>
+template <int MAXD, int HPL, bool GRAD, int EPB, bool SM1, bool LEAN = false, bool FULLD = false>
 __global__ void __launch_bounds__(EPB * 64, 8 / EPB)
 rollout_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
     extern __shared__ __align__(16) uint8_t smem[];
@@ -1131,7 +1133,7 @@ rollout_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
             }
         }
     } else {
-        status = plc_chain<MAXD, HPL, GRAD, false, LEAN>(PR, PO, A, base, base, L, ep, want_out,
+        status = plc_chain<MAXD, HPL, GRAD, false, LEAN, FULLD>(PR, PO, A, base, base, L, ep, want_out,
                                                          want_amax);
         FP_MARK(41, t0_);
         if (status != FP_EP_OK && lane == 0) flag[1] = 1;  // release a waiting simulator
@@ -1564,7 +1566,8 @@ int launch_rollout(const fp_problem *p, const fp_policy *pol, const fp_rollout_a
     const bool lean = a.mode == FP_MODE_SAMPLE && !a.step_vd && !a.step_lp && !a.step_ent &&
                       !a.step_argmax && !a.step_ncand && !a.trace &&
                       !(a.flags & FP_FLAG_TIE_RANDOM);
-    auto kern = PR.SM == 1 ? (lean ? rollout_kernel<MAXD, HPL, GRAD, EPB, true, true>
+    auto kern = PR.SM == 1 ? (lean ? (PR.d == MAXD ? rollout_kernel<MAXD, HPL, GRAD, EPB, true, true, true>
+                                                   : rollout_kernel<MAXD, HPL, GRAD, EPB, true, true>)
                                    : rollout_kernel<MAXD, HPL, GRAD, EPB, true>)
                            : rollout_kernel<MAXD, HPL, GRAD, EPB, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
