@@ -1115,7 +1115,7 @@ rollout_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
             }
             iw = __reduce_max_sync(FP_FULL_MASK, iw);
             __syncwarp();
-            SimOut o = sim_episode<RPL, false, SM1, true>(
+            SimOut o = sim_episode<RPL, false, SM1, true, FULLD ? MAXD : 0>(
                 PR, base, base, L, A.strategy, nullptr,
                 (!LEAN && A.trace) ? A.trace + (size_t)ep * A.trace_cap : nullptr, A.trace_cap,
                 nullptr,

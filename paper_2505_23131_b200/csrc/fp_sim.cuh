@@ -119,7 +119,9 @@ __device__ __forceinline__ bool sim_wait_placed(const SimSync &S, int need) {
     return ok != 0;
 }
 
-template <int RPL, bool HIER = false, bool SM1 = false, bool OVL = false>
+// FD > 0: the cluster's device count as a compile-time constant (resources,
+// link decompositions and loop bounds fold); SM1 likewise fixes one slot.
+template <int RPL, bool HIER = false, bool SM1 = false, bool OVL = false, int FD = 0>
 __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *nb, uint8_t *sb,
                                               const EpLayout &L, int strategy,
                                               const double *__restrict__ jit,
@@ -127,7 +129,8 @@ __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *nb, 
                                               uint8_t *__restrict__ blocked,
                                               SimSync sync = SimSync{nullptr, nullptr, nullptr, -1}) {
     const int lane = lane_id();
-    const int n = P.n, d = P.d, R = P.R, SM = P.SM, BW = L.BW;
+    const int n = P.n, d = FD ? FD : P.d, R = FD ? FD + FD * FD : P.R, SM = SM1 ? 1 : P.SM,
+              BW = L.BW;
     uint32_t *rdy = (uint32_t *)(nb + L.rdy);
     uint32_t *cons = (uint32_t *)(nb + L.cons);
     int *missing = (int *)(nb + L.missing);
