@@ -634,8 +634,9 @@ __device__ __forceinline__ void sel_chain_wide(const DevProblem &PR, const DevPo
 // ---------------------------------------------------------------------------
 // PLC warp
 // ---------------------------------------------------------------------------
-// FULLD: the cluster has exactly MAXD devices, so every `d < D` / `lane < D`
-// test folds away at compile time (the hot LEAN instantiations).
+// FULLD: the cluster has exactly MAXD devices and the hidden width is 32 * HPL,
+// so every `d < D` / `lane < D` / `j < h` test folds away at compile time (the
+// hot LEAN instantiations).
 template <int MAXD, int HPL, bool GRAD, bool WIDE = false, bool LEAN = false, bool FULLD = false>
 __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &PO,
                                          const fp_rollout_args &A, uint8_t *nb, uint8_t *sb,
@@ -643,7 +644,7 @@ __device__ __forceinline__ int plc_chain(const DevProblem &PR, const DevPolicy &
                                          bool want_amax) {
     static_assert(!(WIDE && GRAD), "REINFORCE rows are produced by the compact path only");
     const int lane = lane_id();
-    const int n = PR.n, D = FULLD ? MAXD : PR.d, h = PO.h;
+    const int n = PR.n, D = FULLD ? MAXD : PR.d, h = FULLD ? 32 * HPL : PO.h;
     constexpr int LOGD = PlcLog<MAXD>::v;
     double *tstart = (double *)(nb + L.tstart);
     double *tend = (double *)(nb + L.tend);
@@ -1115,7 +1116,7 @@ rollout_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
             }
             iw = __reduce_max_sync(FP_FULL_MASK, iw);
             __syncwarp();
-            SimOut o = sim_episode<RPL, false, SM1, true, FULLD ? MAXD : 0>(
+            SimOut o = sim_episode<RPL, false, SM1, true, FULLD ? MAXD : 0, LEAN>(
                 PR, base, base, L, A.strategy, nullptr,
                 (!LEAN && A.trace) ? A.trace + (size_t)ep * A.trace_cap : nullptr, A.trace_cap,
                 nullptr,
@@ -1566,7 +1567,8 @@ int launch_rollout(const fp_problem *p, const fp_policy *pol, const fp_rollout_a
     const bool lean = a.mode == FP_MODE_SAMPLE && !a.step_vd && !a.step_lp && !a.step_ent &&
                       !a.step_argmax && !a.step_ncand && !a.trace &&
                       !(a.flags & FP_FLAG_TIE_RANDOM);
-    auto kern = PR.SM == 1 ? (lean ? (PR.d == MAXD ? rollout_kernel<MAXD, HPL, GRAD, EPB, true, true, true>
+    const bool full = PR.d == MAXD && pol->dev.h == 32 * HPL;
+    auto kern = PR.SM == 1 ? (lean ? (full ? rollout_kernel<MAXD, HPL, GRAD, EPB, true, true, true>
                                                    : rollout_kernel<MAXD, HPL, GRAD, EPB, true, true>)
                                    : rollout_kernel<MAXD, HPL, GRAD, EPB, true>)
                            : rollout_kernel<MAXD, HPL, GRAD, EPB, false>;

@@ -121,7 +121,10 @@ __device__ __forceinline__ bool sim_wait_placed(const SimSync &S, int need) {
 
 // FD > 0: the cluster's device count as a compile-time constant (resources,
 // link decompositions and loop bounds fold); SM1 likewise fixes one slot.
-template <int RPL, bool HIER = false, bool SM1 = false, bool OVL = false, int FD = 0>
+// PLAIN: no trace, no jitter table, no blocked-task output (the fused
+// sampling rollout) -- those branches compile away.
+template <int RPL, bool HIER = false, bool SM1 = false, bool OVL = false, int FD = 0,
+          bool PLAIN = false>
 __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *nb, uint8_t *sb,
                                               const EpLayout &L, int strategy,
                                               const double *__restrict__ jit,
@@ -213,7 +216,8 @@ __device__ __forceinline__ SimOut sim_episode(const DevProblem &P, uint8_t *nb, 
     int remaining = P.n_nonentry;
     double t = 0.0;
     int seq = 0;
-    const bool tracing = trace != nullptr;
+    const bool tracing = !PLAIN && trace != nullptr;
+    if constexpr (PLAIN) { jit = nullptr; blocked = nullptr; }
 
     while (remaining > 0) {
         // ---------------- start phase: each lane serves its resources --------
