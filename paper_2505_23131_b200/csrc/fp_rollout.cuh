@@ -1586,7 +1586,7 @@ int launch_rollout(const fp_problem *p, const fp_policy *pol, const fp_rollout_a
 // n-sized state in the HBM workspace slice of this block, small scratch and
 // the hand-off ring in shared memory.  After the PLC chain the same warp
 // scores the assignment with the hierarchical-bitset simulator.
-template <int MAXD, int HPL, bool SM1, bool LEAN = false>
+template <int MAXD, int HPL, bool SM1, bool LEAN = false, bool FULLD = false>
 __global__ void __launch_bounds__(64, 8)
 rollout_wide_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
     extern __shared__ __align__(16) uint8_t smem[];
@@ -1609,7 +1609,7 @@ rollout_wide_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) 
         if (!is_plc) {
             sel_chain_wide<LEAN>(PR, PO, A, nb, sb, L, ep, want_lp, want_amax);
         } else {
-            int status = plc_chain<MAXD, HPL, false, true, LEAN>(PR, PO, A, nb, sb, L, ep,
+            int status = plc_chain<MAXD, HPL, false, true, LEAN, FULLD>(PR, PO, A, nb, sb, L, ep,
                                                                  want_lp, want_amax);
             const uint8_t *dev = nb + L.assign;
             for (int v = lane; v < n; v += 32)
@@ -1617,7 +1617,7 @@ rollout_wide_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) 
             double mk = 0.0;
             if (status == FP_EP_OK && A.simulate) {
                 __syncwarp();
-                SimOut o = sim_episode<RPL, true, SM1>(
+                SimOut o = sim_episode<RPL, true, SM1, false, FULLD ? MAXD : 0, LEAN>(
                     PR, nb, sb, L, A.strategy, nullptr,
                     (!LEAN && A.trace) ? A.trace + (size_t)ep * A.trace_cap : nullptr,
                     A.trace_cap, nullptr);
@@ -1646,7 +1646,9 @@ int launch_rollout_wide(const fp_problem *p, const fp_policy *pol,
     }
     const bool lean = a.mode == FP_MODE_SAMPLE && !a.step_vd && !a.step_lp && !a.step_ent &&
                       !a.step_argmax && !a.step_ncand && !a.trace && !(a.flags & FP_FLAG_TIE_RANDOM);
-    auto kern = PR.SM == 1 ? (lean ? rollout_wide_kernel<MAXD, HPL, true, true>
+    const bool full = PR.d == MAXD && pol->dev.h == 32 * HPL;
+    auto kern = PR.SM == 1 ? (lean ? (full ? rollout_wide_kernel<MAXD, HPL, true, true, true>
+                                           : rollout_wide_kernel<MAXD, HPL, true, true>)
                                    : rollout_wide_kernel<MAXD, HPL, true>)
                            : rollout_wide_kernel<MAXD, HPL, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
