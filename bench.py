@@ -333,6 +333,8 @@ def run_ours(args):
     if clk:
         clk.__enter__()
         time.sleep(0.3)
+    from paper_2505_23131_b200 import _native as N
+    N.agg_timer(True)  # event pair around every aggregation launch (its own stream)
     for i in range(args.steps):
         flush.fill_(float(i))
         ev[i][0].record(stream)
@@ -346,6 +348,8 @@ def run_ours(args):
             kev[i][1].record(stream)
         ev[i][1].record(stream)
     torch.cuda.synchronize()
+    agg_ms, agg_launches = N.agg_timer_read()
+    N.agg_timer(False)
     if world > 1:
         dist.barrier()
     if clk:
@@ -432,11 +436,28 @@ def run_ours(args):
         per_step = args.mp_mode == "per_step"
         K = pc.k_rounds
         prep_launches = ctx.encode_launches()
+        # GNN aggregation kernel (north star: >= 60% of HBM), timed on its own
+        # launching stream over the timed region (fp_agg_timer_*).  Algorithmic
+        # bytes per launch and encoder: every row's P (gathered; each row is
+        # needed once), Q and agg rows once -- 3 x 8h B per row in fp64, fp32
+        # P/Q + bf16 hi/lo agg planes (3 x 4h B) for the tc encoder -- plus
+        # the message CSR (ptr 4 B per vertex, source 4 B + edge scalar 8 B per
+        # message), read once per encoder
+        rows = B * n if per_step else n
+        M = 2 * len(g.edges)
+        row_b = 3 * (4 if args.encoder == "tc" else 8) * h
+        n_enc = 1 if pc.shared_encoder else 2
+        agg_alg = n_enc * (rows * row_b + (n + 1) * 4 + M * 12)
+        agg = None
+        if agg_launches:
+            agg_kms = agg_ms / agg_launches
+            agg_ach = agg_alg / (agg_kms * 1e-3) / 1e9
+            agg = {"kernel": "gnn_agg_staged_kernel" if per_step else "gnn_agg_kernel",
+                   "rows_per_encoder": rows, "encoders": n_enc,
+                   "alg_bytes_per_launch": agg_alg, "kernel_ms": agg_kms,
+                   "launches_timed": agg_launches, "achieved": agg_ach, "peak": peak,
+                   "unit": "GB/s", "frac": agg_ach / peak}
         if per_step:
-            # per step: 2 encoders x K rounds of aggregation over B*n rows (the
-            # HBM-bound part) -- node MLP traffic not counted
-            M = 2 * len(g.edges)
-            alg = n * K * 2 * (B * M * (8 * h + 12) + B * n * (16 * h + 4))
             launches = prep_launches + 1 + n * (2 + 2 * K) + 3
         else:
             launches = prep_launches + 1
@@ -468,13 +489,27 @@ def run_ours(args):
                          "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "kernel_ms": kms, "alg_bytes_per_launch": alg,
-                         "note": ("B x n batched encodes per step; aggregation bytes over the "
-                                  "whole rollout" if per_step else
+                         "note": ("B x n batched encodes per step; per-launch aggregation "
+                                  "bytes summed over the whole rollout" if per_step else
                                   "latency-bound: each episode is a dependent chain of n "
                                   "decisions + the overlapped simulation (DESIGN.md section 4); "
                                   "GNN kernels' rooflines in profiles/r1_ncu_*"),
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
         }
+        if agg:
+            if per_step:
+                # per_step: the aggregation kernel IS the HBM-bound kernel of
+                # the step (B x n rows per launch); its own roofline heads the
+                # line, the rollout-wide figure stays beside it
+                blended = line["roofline"]
+                line["roofline"] = dict(agg, bound="hbm", traffic=None,
+                                        peak_source=blended["peak_source"],
+                                        note="gnn aggregation kernel, event-timed per launch "
+                                             "over the timed region; algorithmic bytes = "
+                                             "P, Q, agg rows once + the message CSR",
+                                        rollout=blended)
+            else:
+                line["roofline"]["aggregation"] = agg
         line["rates"] = _episode_rates(g, out.assign.cpu().numpy(), value)
         if clk:
             line["clocks"] = clk.summary(local)

@@ -292,6 +292,13 @@ int fp_sgd_step(double *params, const double *grad, int64_t count, double lr, vo
 int fp_sgd_step_masked(double *params, const double *grad, int64_t count, double lr,
                        const int32_t *skip, void *stream);
 
+/* Measurement hook (bench.py): while enabled, every GNN aggregation launch
+ * is bracketed by an event pair on its own stream; fp_agg_timer_read syncs
+ * those events, returns the summed kernel time and launch count since the
+ * last read / enable, and resets.  No effect on results. */
+int fp_agg_timer_enable(int32_t on);
+int fp_agg_timer_read(double *total_ms, int64_t *launches);
+
 /* Tensor-core (tcgen05 + TMA) path self test: out[M][N] (fp32) = X . W with
  * X [M][64] given as bf16 hi / lo planes (device, row pitch 128 bytes) and W
  * [64][N] fp64 (device), N in {32, 64}; the three split products accumulate

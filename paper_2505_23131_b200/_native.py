@@ -131,5 +131,18 @@ EXPORTED = EXPORTED + (
     "fp_policy_create", "fp_policy_destroy", "fp_policy_set_encoder", "fp_policy_prepare", "fp_policy_table",
     "fp_rollout_workspace_size", "fp_rollout_batch", "fp_grad_ep_stride", "fp_grad_rec_stride",
     "fp_pg_reduce", "fp_pg_reduce_per_step", "fp_policy_backward", "fp_sgd_step", "fp_sgd_step_masked",
-    "fp_tc_gemm_selftest",
+    "fp_tc_gemm_selftest", "fp_agg_timer_enable", "fp_agg_timer_read",
 )
+
+
+def agg_timer(on: bool) -> None:
+    """Bracket every GNN aggregation launch with an event pair on its stream
+    (measurement hook for bench.py; fp_agg_timer_enable)."""
+    check(lib().fp_agg_timer_enable(ctypes.c_int32(1 if on else 0)))
+
+
+def agg_timer_read() -> tuple[float, int]:
+    """(summed aggregation-kernel ms, launches) since the last read / enable."""
+    ms, cnt = ctypes.c_double(), ctypes.c_int64()
+    check(lib().fp_agg_timer_read(ctypes.byref(ms), ctypes.byref(cnt)))
+    return ms.value, cnt.value

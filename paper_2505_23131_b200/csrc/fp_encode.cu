@@ -444,6 +444,73 @@ __global__ void __launch_bounds__(kEncWarps * 32, 3) encode_sel_kernel(DevPolicy
         }                                                                             \
     } while (0)
 
+// ---------------------------------------------------------------------------
+// Aggregation-kernel timer (measurement only, fp_agg_timer_*): when enabled,
+// an event pair is recorded on the launching stream around every aggregation
+// launch, so bench.py can report the kernel's own average duration over its
+// timed region.  Host-side bookkeeping, one encoder thread at a time.
+// ---------------------------------------------------------------------------
+namespace {
+struct AggTimer {
+    bool on = false;
+    std::vector<cudaEvent_t> ev;  // pairs
+    size_t used = 0;
+};
+AggTimer &agg_timer() {
+    static AggTimer t;
+    return t;
+}
+}  // namespace
+
+// FP_AGG_STAGED=0 turns the staged batched aggregation off (A/B runs only)
+bool agg_staged_enabled() {
+    static const bool on = !(getenv("FP_AGG_STAGED") && atoi(getenv("FP_AGG_STAGED")) == 0);
+    return on;
+}
+
+void agg_timer_begin(cudaStream_t st) {
+    AggTimer &t = agg_timer();
+    if (!t.on) return;
+    if (t.used + 2 > t.ev.size()) {
+        for (int i = 0; i < 2; ++i) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            t.ev.push_back(e);
+        }
+    }
+    cudaEventRecord(t.ev[t.used], st);
+}
+
+void agg_timer_end(cudaStream_t st) {
+    AggTimer &t = agg_timer();
+    if (!t.on) return;
+    cudaEventRecord(t.ev[t.used + 1], st);
+    t.used += 2;
+}
+
+int agg_timer_enable(int on) {
+    AggTimer &t = agg_timer();
+    t.on = on != 0;
+    t.used = 0;
+    return FP_OK;
+}
+
+int agg_timer_read(double *total_ms, int64_t *launches) {
+    AggTimer &t = agg_timer();
+    double tot = 0.0;
+    for (size_t i = 0; i < t.used; i += 2) {
+        FP_CUDA_RET(cudaEventSynchronize(t.ev[i + 1]));
+        float ms = 0.f;
+        FP_CUDA_RET(cudaEventElapsedTime(&ms, t.ev[i], t.ev[i + 1]));
+        tot += ms;
+    }
+    if (total_ms) *total_ms = tot;
+    if (launches) *launches = (int64_t)(t.used / 2);
+    t.used = 0;
+    return FP_OK;
+}
+
+
 template <int HPL, int HC, bool STAGE, bool BWD>
 static int launch_encode(DevPolicy &P, cudaStream_t st) {
     int dev = 0, sms = 148;
@@ -537,7 +604,29 @@ static int launch_gnn_tc(DevPolicy &P, cudaStream_t st, bool sel_head = true) {
     const int agg_blocks = (P.rows + 8 * VPW - 1) / (8 * VPW);
     for (int k = 0; k < P.K; ++k) {
         const bool last = k == P.K - 1;
-        {
+        int agg_S = 0;  // staged batched path: stages that fit one block per SM
+        if (P.rows >= 2 * P.n && P.rows % P.n == 0 && agg_staged_enabled()) {
+            int optin = 0;
+            cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+            for (int S = 4; S >= 2 && !agg_S; --S)
+                if (agg_staged_smem(P.n, P.n_msgs, H, P.tc, S) <= optin &&
+                    (S == 2 || 2LL * P.n * H * (P.tc ? 4 : 8) * S <= 160 * 1024))
+                    agg_S = S;
+        }
+        if (agg_S) {
+            const int64_t smem = agg_staged_smem(P.n, P.n_msgs, H, P.tc, agg_S);
+            const void *kern = P.tc ? (const void *)gnn_agg_staged_kernel<H, true>
+                                    : (const void *)gnn_agg_staged_kernel<H, false>;
+            FP_CUDA_RET(set_smem(kern, smem));
+            const int B = P.rows / P.n;
+            const dim3 grid(std::max(1, std::min(B, sms / P.n_enc)), P.n_enc);
+            agg_timer_begin(st);
+            if (P.tc) gnn_agg_staged_kernel<H, true><<<grid, 1024, smem, st>>>(P, k, agg_S);
+            else gnn_agg_staged_kernel<H, false><<<grid, 1024, smem, st>>>(P, k, agg_S);
+            FP_CUDA_RET(cudaGetLastError());
+            agg_timer_end(st);
+        } else {
+            agg_timer_begin(st);
             if (P.tc) {
                 const void *kern = (const void *)gnn_agg_kernel<H, true>;
                 gnn_agg_kernel<H, true><<<dim3(grid_for(kern, 0, agg_blocks), P.n_enc), 256, 0, st>>>(P, k);
@@ -546,6 +635,7 @@ static int launch_gnn_tc(DevPolicy &P, cudaStream_t st, bool sel_head = true) {
                 gnn_agg_kernel<H><<<dim3(grid_for(kern, 0, agg_blocks), P.n_enc), 256, 0, st>>>(P, k);
             }
             FP_CUDA_RET(cudaGetLastError());
+            agg_timer_end(st);
         }
         if (P.tc) {  // bf16 node MLPs on tcgen05, operands by TMA
             const int rc = tc_node_launch(P, k, last, st);
@@ -791,6 +881,7 @@ int fp_policy_create(const fp_problem *p, const fp_policy_desc *desc, fp_policy 
     P.x = (const double *)(b + o_x);
     P.adj_ptr = (const int *)(b + o_ap); P.adj_nbr = (const int *)(b + o_an);
     P.adj_e = (const double *)(b + o_ae);
+    P.n_msgs = (int)M;
     P.bp_ptr = (const int *)(b + o_bp); P.bp_idx = (const int *)(b + o_bi);
     P.tp_ptr = (const int *)(b + o_tp); P.tp_idx = (const int *)(b + o_ti);
     P.n_bpath = forest ? 0 : (int)Lb;
@@ -840,6 +931,12 @@ int fp_policy_destroy(fp_policy *pol) {
     if (pol->tc_planes) cudaFree(pol->tc_planes);
     delete pol;
     return FP_OK;
+}
+
+int fp_agg_timer_enable(int32_t on) { return fp::agg_timer_enable(on); }
+
+int fp_agg_timer_read(double *total_ms, int64_t *launches) {
+    return fp::agg_timer_read(total_ms, launches);
 }
 
 int fp_policy_set_encoder(fp_policy *pol, int32_t mode) {

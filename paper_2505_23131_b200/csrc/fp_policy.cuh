@@ -58,6 +58,7 @@ struct DevPolicy {
     const double *adj_e;           // standardized edge cost per message
     const int *bp_ptr, *bp_idx, *tp_ptr, *tp_idx;     // SEL b/t paths
     int n_bpath, n_tpath;                             // their total lengths
+    int n_msgs;                                       // adj_ptr[n] (host copy)
     const int *ibp_ptr, *ibp_idx, *itp_ptr, *itp_idx; // inverse paths (u -> v with u in path(v))
     // forest form (large graphs): next pointers + pointer-jumping buffers
     int forest, jump_rounds;
@@ -88,6 +89,8 @@ struct DevPolicy {
 // GNN encode of every row of P (fp_encode.cu): aggregation + DMMA node MLPs
 // (+ forest path sums and the SEL head when sel_head).  0 or FP_ERR_*.
 int gnn_encode_rows(DevPolicy &P, cudaStream_t st, bool bwd, bool sel_head);
+int agg_timer_enable(int on);
+int agg_timer_read(double *total_ms, int64_t *launches);
 
 // bf16 tensor-core node MLPs of round k (fp_tc_node.cu); needs P.tc planes.
 int tc_node_launch(const DevPolicy &P, int k, bool last, cudaStream_t st);

@@ -59,6 +59,16 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, u
         : "memory");
 }
 
+// 1-D bulk copy global -> shared (TMA engine, no tensor map): bytes % 16 == 0,
+// both addresses 16-byte aligned, completion counted on `bar` in bytes.
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"((uint64_t)src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
 // ---- proxies / fences -----------------------------------------------------
 // shared-memory writes by threads -> visible to the tensor core (async proxy)
 __device__ __forceinline__ void fence_proxy_async_smem() {
