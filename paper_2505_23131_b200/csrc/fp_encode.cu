@@ -882,6 +882,7 @@ int fp_policy_create(const fp_problem *p, const fp_policy_desc *desc, fp_policy 
     P.adj_ptr = (const int *)(b + o_ap); P.adj_nbr = (const int *)(b + o_an);
     P.adj_e = (const double *)(b + o_ae);
     P.n_msgs = (int)M;
+    P.n_params = desc->n_params;
     P.bp_ptr = (const int *)(b + o_bp); P.bp_idx = (const int *)(b + o_bi);
     P.tp_ptr = (const int *)(b + o_tp); P.tp_idx = (const int *)(b + o_ti);
     P.n_bpath = forest ? 0 : (int)Lb;

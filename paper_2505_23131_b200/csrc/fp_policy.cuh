@@ -59,6 +59,7 @@ struct DevPolicy {
     const int *bp_ptr, *bp_idx, *tp_ptr, *tp_idx;     // SEL b/t paths
     int n_bpath, n_tpath;                             // their total lengths
     int n_msgs;                                       // adj_ptr[n] (host copy)
+    int64_t n_params;                                 // doubles in the flat params
     const int *ibp_ptr, *ibp_idx, *itp_ptr, *itp_idx; // inverse paths (u -> v with u in path(v))
     // forest form (large graphs): next pointers + pointer-jumping buffers
     int forest, jump_rounds;
