@@ -334,7 +334,9 @@ def run_ours(args):
         clk.__enter__()
         time.sleep(0.3)
     from paper_2505_23131_b200 import _native as N
-    N.agg_timer(True)  # event pair around every aggregation launch (its own stream)
+    # per_step: an event pair around every aggregation launch (its own stream);
+    # not in per_episode, where the events would sit between PDL-chained kernels
+    N.agg_timer(args.mp_mode == "per_step")
     for i in range(args.steps):
         flush.fill_(float(i))
         ev[i][0].record(stream)

@@ -1,6 +1,8 @@
 // Shared device helpers for the flowplace B200 kernels (sm_100a).
 #pragma once
 
+#include <cstdlib>
+
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -52,6 +54,43 @@ static __device__ unsigned long long g_phase_count[64];
 namespace fp {
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+// Programmatic dependent launch (PDL): a kernel launched with
+// programmatic stream serialization may start while its predecessor drains;
+// griddep_wait() blocks until the predecessor grid has completed and its
+// writes are visible (a no-op for an ordinary launch), griddep_launch() lets
+// the successor start its prologue.  Every PDL-launched kernel calls
+// griddep_wait() before touching its predecessors' outputs (and so keeps the
+// completion order transitive).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
+#ifndef __CUDACC_RTC__
+// host: launch `kern` with programmatic stream serialization (FP_PDL=0: off)
+inline bool pdl_enabled() {
+    static const bool on = !(getenv("FP_PDL") && atoi(getenv("FP_PDL")) == 0);
+    return on;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args... args) {
+    if (!pdl_enabled()) {
+        kern<<<grid, block, smem, st>>>(args...);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+#endif
 
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {

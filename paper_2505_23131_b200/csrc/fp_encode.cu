@@ -632,7 +632,8 @@ static int launch_gnn_tc(DevPolicy &P, cudaStream_t st, bool sel_head = true) {
                 gnn_agg_kernel<H, true><<<dim3(grid_for(kern, 0, agg_blocks), P.n_enc), 256, 0, st>>>(P, k);
             } else {
                 const void *kern = (const void *)gnn_agg_kernel<H>;
-                gnn_agg_kernel<H><<<dim3(grid_for(kern, 0, agg_blocks), P.n_enc), 256, 0, st>>>(P, k);
+                FP_CUDA_RET(launch_pdl(gnn_agg_kernel<H>, dim3(grid_for(kern, 0, agg_blocks), P.n_enc),
+                                       dim3(256), 0, st, P, k));
             }
             FP_CUDA_RET(cudaGetLastError());
             agg_timer_end(st);
@@ -648,14 +649,15 @@ static int launch_gnn_tc(DevPolicy &P, cudaStream_t st, bool sel_head = true) {
         FP_CUDA_RET(set_smem(kern, smem));
         const dim3 grid(grid_for(kern, smem, tile_blocks), P.n_enc);
         if (k == 0)
-            gnn_node_kernel<H, true, BWD><<<grid, threads, smem, st>>>(P, k, last);
+            FP_CUDA_RET(launch_pdl(gnn_node_kernel<H, true, BWD>, grid, dim3(threads), (size_t)smem, st, P, k, (int)last));
         else
-            gnn_node_kernel<H, false, BWD><<<grid, threads, smem, st>>>(P, k, last);
+            FP_CUDA_RET(launch_pdl(gnn_node_kernel<H, false, BWD>, grid, dim3(threads), (size_t)smem, st, P, k, (int)last));
         FP_CUDA_RET(cudaGetLastError());
     }
     if (!sel_head) return FP_OK;
     if (!P.forest) {
-        gnn_pathsum_kernel<H><<<std::max(1, std::min((P.n + 7) / 8, sms * 8)), 256, 0, st>>>(P);
+        FP_CUDA_RET(launch_pdl(gnn_pathsum_kernel<H>, dim3(std::max(1, std::min((P.n + 7) / 8, sms * 8))),
+                               dim3(256), 0, st, P));
         FP_CUDA_RET(cudaGetLastError());
     }
     if (P.forest)
@@ -672,7 +674,7 @@ static int launch_gnn_tc(DevPolicy &P, cudaStream_t st, bool sel_head = true) {
         int occ = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, (size_t)smem);
         const int gx = std::max(1, std::min(tile_blocks, sms * std::max(occ, 1)));
-        gnn_sel_kernel<H, BWD><<<gx, threads, smem, st>>>(P);
+        FP_CUDA_RET(launch_pdl(gnn_sel_kernel<H, BWD>, dim3(gx), dim3(threads), (size_t)smem, st, P));
         FP_CUDA_RET(cudaGetLastError());
     }
     return FP_OK;

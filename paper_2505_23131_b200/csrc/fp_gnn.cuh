@@ -136,6 +136,7 @@ __device__ __forceinline__ void gnn_agg_body(const DevPolicy &P, int k, int e_, 
     const double s = P.slope;
     const int warps = blockDim.x >> 5;
     const int gw = bx_ * warps + (threadIdx.x >> 5);
+    griddep_wait();  // P / Q come from the previous kernel
     for (int vb = gw * VPW; vb < rows; vb += gx_ * warps * VPW) {
         const int r = vb + sub;  // row = episode * n + vertex
         if (r >= rows || (HL < 32 && lane >= VPW * HL)) continue;
@@ -281,6 +282,7 @@ inline int64_t agg_staged_smem(int n, int M, int H, bool f32, int S) {
 template <int H, bool F32 = false>
 __global__ void __launch_bounds__(256, 5) gnn_agg_kernel(DevPolicy P, int k) {
     extern __shared__ __align__(16) double gsm[];
+    griddep_launch();
     gnn_agg_body<H, F32>(P, k, blockIdx.y, blockIdx.x, gridDim.x, gsm);
 }
 
@@ -381,6 +383,7 @@ __device__ __forceinline__ void gnn_proj0_body(const DevPolicy &P, int e_, int b
 template <int H>
 __global__ void __launch_bounds__(256) gnn_proj0_kernel(DevPolicy P) {
     extern __shared__ __align__(16) double gsm[];
+    griddep_launch();
     if (P.n_params)  // the encode's first kernel warms L2 for the later ones
         prefetch_encode_inputs(P, (blockIdx.y * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x,
                                gridDim.x * gridDim.y * blockDim.x);
@@ -460,6 +463,7 @@ __device__ __forceinline__ void gnn_node_body(const DevPolicy &P, int k, int las
         }
     }
     __syncthreads();
+    griddep_wait();  // H_k / agg_k come from the previous kernels
 
     const double *Hk = P.H[e][k];
     const double *agg = P.AG[e][k];
@@ -591,6 +595,7 @@ __device__ __forceinline__ void gnn_node_body(const DevPolicy &P, int k, int las
 template <int H, bool K0, bool BWD>
 __global__ void __launch_bounds__(256, 2) gnn_node_kernel(DevPolicy P, int k, int last) {
     extern __shared__ __align__(16) double gsm[];
+    griddep_launch();
     gnn_node_body<H, K0, BWD>(P, k, last, blockIdx.y, blockIdx.x, gridDim.x, gsm);
 }
 
@@ -644,6 +649,8 @@ __device__ __forceinline__ void gnn_pathsum_body(const DevPolicy &P, int bx_, in
 
 template <int H>
 __global__ void __launch_bounds__(256) gnn_pathsum_kernel(DevPolicy P) {
+    griddep_launch();
+    griddep_wait();
     gnn_pathsum_body<H>(P, blockIdx.x, gridDim.x);
 }
 
@@ -692,6 +699,7 @@ __device__ __forceinline__ void gnn_sel_body(const DevPolicy &P, int e_, int bx_
     double *Fw = gsm;
     stage_frag(Fw, 4 * H, KT, NT, [&](int kk, int j) { return w1[kk * H + j]; });
     __syncthreads();
+    griddep_wait();  // H_sel and the path sums come from the previous kernels
     const double *Hs = Hs_copy ? Hs_copy : P.H[0][P.K];
     const int rb = P.jump_rounds;
     // path sums: pointer-jumped (forest) or gnn_pathsum (explicit lists)
@@ -748,6 +756,7 @@ __device__ __forceinline__ void gnn_sel_body(const DevPolicy &P, int e_, int bx_
 template <int H, bool BWD>
 __global__ void __launch_bounds__(256, 2) gnn_sel_kernel(DevPolicy P) {
     extern __shared__ __align__(16) double gsm[];
+    griddep_launch();
     gnn_sel_body<H, BWD>(P, blockIdx.y, blockIdx.x, gridDim.x, gsm);
 }
 
@@ -770,6 +779,9 @@ __global__ void __launch_bounds__(256, 1) gnn_small_kernel(DevPolicy P) {
 #else
 #define TT() do {} while (0)
 #endif
+    // no early griddep_launch here: the rollout's blocks would sit on every SM
+    // for the whole encode (starving concurrent work on other streams); the
+    // implicit trigger at block exit still hides the rollout's launch latency
     if (P.n_params) prefetch_encode_inputs(P, threadIdx.x, blockDim.x);
     TT();
     gnn_proj0_body<H>(P, e, 0, 1, gsm);

@@ -1066,9 +1066,7 @@ rollout_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
     const bool is_plc = plc_role(hw_slot, warp);
     const int ep = blockIdx.x * EPB + slot;
     const int n = PR.n;
-    // block-shared SEL logits (every episode of the batch uses one snapshot)
     double *s_sm = (double *)smem;
-    for (int v = threadIdx.x; v < n; v += blockDim.x) s_sm[v] = PO.s[v];
     uint8_t *base = smem + fp_align(8 * n, 16) + (size_t)slot * L.bytes;
     volatile int *flag = (volatile int *)(base + L.flag);  // [0] placed, [1] PLC abort
     if (!is_plc) {
@@ -1077,6 +1075,10 @@ rollout_kernel(DevProblem PR, DevPolicy PO, fp_rollout_args A, EpLayout L) {
         for (int t = lane; t < n; t += 32) order[t] = -3;  // hand-off sentinel
         if (lane == 0) { flag[0] = 0; flag[1] = 0; }
     }
+    // (PDL) everything above overlaps the encoder's tail; its tables from here
+    griddep_wait();
+    // block-shared SEL logits (every episode of the batch uses one snapshot)
+    for (int v = threadIdx.x; v < n; v += blockDim.x) s_sm[v] = PO.s[v];
     __syncthreads();
     if (ep >= A.B) return;
     const bool want_out = !LEAN && (A.step_lp != nullptr || A.step_ent != nullptr);
@@ -1576,8 +1578,7 @@ int launch_rollout(const fp_problem *p, const fp_policy *pol, const fp_rollout_a
                                          (int)smem);
     if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FP_ERR_CUDA; }
     const int grid = (a.B + EPB - 1) / EPB;
-    kern<<<grid, EPB * 64, smem, st>>>(PR, pol->dev, a, L);
-    e = cudaGetLastError();
+    e = launch_pdl(kern, dim3(grid), dim3(EPB * 64), (size_t)smem, st, PR, pol->dev, a, L);
     if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FP_ERR_CUDA; }
     return FP_OK;
 }
