@@ -495,7 +495,8 @@ def run_ours(args):
                                   "bytes summed over the whole rollout" if per_step else
                                   "latency-bound: each episode is a dependent chain of n "
                                   "decisions + the overlapped simulation (DESIGN.md section 4); "
-                                  "GNN kernels' rooflines in profiles/r1_ncu_*"),
+                                  "GNN aggregation roofline: --mp-mode per_step, "
+                                  "profiles/r2/final/ncu_agg_staged_*"),
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
         }
         if agg:

@@ -1,0 +1,11 @@
+#!/bin/bash
+set -x
+F=gpurun_out/pdl3
+mkdir -p $F
+for rep in 1 2; do
+for V in 1 0; do
+  for w in ffnn llama_layer; do
+  FP_PDL=$V timeout 300 python bench.py --workload $w --mode train --no-cpu --steps 10 > $F/bench_${w}_P${V}_$rep.json 2>/dev/null
+  done
+done
+done
