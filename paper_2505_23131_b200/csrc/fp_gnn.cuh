@@ -670,7 +670,7 @@ __device__ __forceinline__ void gnn_plc_consts_body(const DevPolicy &P) {
                  *b1 = P.W(PR_PLC_H1_B);
     for (int j = lane; j < H; j += 32) {
         double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-#pragma unroll 4
+#pragma unroll 8
         for (int i = 0; i < H; ++i) {
             const double w = w1[(2 * H + i) * H + j];
 #pragma unroll
@@ -693,12 +693,16 @@ __device__ __forceinline__ void gnn_sel_body(const DevPolicy &P, int e_, int bx_
     const int lane = lane_id(), warp = threadIdx.x >> 5;
     const int warps = blockDim.x >> 5, n = P.n;
     const double s = P.slope;
-    if (consts && bx_ == 0 && warp == 0) gnn_plc_consts_body<H>(P);
     const double *w1 = P.W(PR_SEL_H1_W), *b1 = P.W(PR_SEL_H1_B), *w2 = P.W(PR_SEL_H2_W),
                  *b2 = P.W(PR_SEL_H2_B);
     double *Fw = gsm;
     stage_frag(Fw, 4 * H, KT, NT, [&](int kk, int j) { return w1[kk * H + j]; });
     __syncthreads();
+    // PLC constants (params only) on the grid's LAST warp -- the one with the
+    // fewest tiles -- after the block barrier and before the dependency wait,
+    // i.e. overlapping the previous kernel's tail instead of holding block 0
+    // at its barrier
+    if (consts && bx_ == gx_ - 1 && warp == warps - 1) gnn_plc_consts_body<H>(P);
     griddep_wait();  // H_sel and the path sums come from the previous kernels
     const double *Hs = Hs_copy ? Hs_copy : P.H[0][P.K];
     const int rb = P.jump_rounds;
