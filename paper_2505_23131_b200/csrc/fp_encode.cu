@@ -587,9 +587,20 @@ static int launch_gnn_tc(DevPolicy &P, cudaStream_t st, bool sel_head = true) {
                        4LL * (2 * (P.n + 1) + P.n_bpath + P.n_tpath);
         for (int k = 0; k < P.K; ++k)
             smem = std::max<int64_t>(smem, 8LL * node_smem_doubles(H, k, k == P.K - 1));
-        const void *kern = (const void *)gnn_small_kernel<H, BWD>;
-        FP_CUDA_RET(set_smem(kern, smem));
-        gnn_small_kernel<H, BWD><<<P.n_enc, threads, smem, st>>>(P);
+        // 512 threads for h <= 32: the aggregation / path-sum / weight-staging
+        // phases spread over 16 warps (FFNN 44.6 -> 38.4 us, 128 registers, no
+        // spills; h = 64 would spill at 128 and keeps 256).  FP_SMALL_THREADS=256
+        // for A/B runs.
+        static const bool env256 = getenv("FP_SMALL_THREADS") && atoi(getenv("FP_SMALL_THREADS")) == 256;
+        if (H <= 32 && !env256) {
+            const void *kern = (const void *)gnn_small_kernel<H, BWD, 512>;
+            FP_CUDA_RET(set_smem(kern, smem));
+            gnn_small_kernel<H, BWD, 512><<<P.n_enc, 512, smem, st>>>(P);
+        } else {
+            const void *kern = (const void *)gnn_small_kernel<H, BWD>;
+            FP_CUDA_RET(set_smem(kern, smem));
+            gnn_small_kernel<H, BWD><<<P.n_enc, threads, smem, st>>>(P);
+        }
         FP_CUDA_RET(cudaGetLastError());
         return FP_OK;
     }

@@ -773,8 +773,8 @@ __global__ void __launch_bounds__(256, 2) gnn_sel_kernel(DevPolicy P) {
 // ---------------------------------------------------------------------------
 constexpr int kSmallEncodeRows = 64;  // one 8-row tile per warp
 
-template <int H, bool BWD>
-__global__ void __launch_bounds__(256, 1) gnn_small_kernel(DevPolicy P) {
+template <int H, bool BWD, int NTH = 256>
+__global__ void __launch_bounds__(NTH, 1) gnn_small_kernel(DevPolicy P) {
     extern __shared__ __align__(16) double gsm[];
     const int e = blockIdx.x;
 #ifdef FP_SMALL_TIMING
