@@ -149,51 +149,77 @@ ps_step_kernel(DevProblem PR, DevPolicy PO, DevPolicy PB, fp_rollout_args A, PsS
     }
     const double *w1 = PO.W(PR_SEL_H1_W), *b1 = PO.W(PR_SEL_H1_B), *w2 = PO.W(PR_SEL_H2_W);
     const double b2 = PO.W(PR_SEL_H2_B)[0];
-    for (int i = warp; i < k; i += kPsWarps) {
-        const int v = cid[i];
-        double em[4][HPL];
+    // Candidates in groups of PSG per warp (candidates i0 + c * kPsWarps): each
+    // head-1 weight w1[.][j] is loaded once per group and feeds PSG independent
+    // FMA chains (the per-candidate chain order is unchanged, so every logit
+    // is the one-candidate loop's); the group's embedding loads are in flight
+    // together.  (One candidate per trip was bound by the w1 loads on its
+    // 128-long dependent chain: 48% of the kernel's stall samples.)
+    constexpr int PSG = 4;
+    for (int i0 = warp; i0 < k; i0 += kPsWarps * PSG) {
+        double em[PSG][4][HPL];
 #pragma unroll
-        for (int t = 0; t < HPL; ++t) {
-            const int j = lane + 32 * t;
-            em[0][t] = em[1][t] = em[2][t] = em[3][t] = 0.0;
-            if (j >= h) continue;
-            em[0][t] = Hs[(base + v) * h + j];
-            double hb = 0.0, ht = 0.0;
+        for (int c = 0; c < PSG; ++c) {
+            const int i = i0 + c * kPsWarps;
+            const int v = i < k ? cid[i] : -1;
+#pragma unroll
+            for (int t = 0; t < HPL; ++t) {
+                const int j = lane + 32 * t;
+                em[c][0][t] = em[c][1][t] = em[c][2][t] = em[c][3][t] = 0.0;
+                if (j >= h || v < 0) continue;
+                em[c][0][t] = Hs[(base + v) * h + j];
+                double hb = 0.0, ht = 0.0;
 #pragma unroll 4
-            for (int q = PO.bp_ptr[v]; q < PO.bp_ptr[v + 1]; ++q) hb += Hs[(base + PO.bp_idx[q]) * h + j];
+                for (int q = PO.bp_ptr[v]; q < PO.bp_ptr[v + 1]; ++q) hb += Hs[(base + PO.bp_idx[q]) * h + j];
 #pragma unroll 4
-            for (int q = PO.tp_ptr[v]; q < PO.tp_ptr[v + 1]; ++q) ht += Hs[(base + PO.tp_idx[q]) * h + j];
-            em[1][t] = hb;
-            em[2][t] = ht;
-            em[3][t] = PB.Zs[(base + v) * h + j];
+                for (int q = PO.tp_ptr[v]; q < PO.tp_ptr[v + 1]; ++q) ht += Hs[(base + PO.tp_idx[q]) * h + j];
+                em[c][1][t] = hb;
+                em[c][2][t] = ht;
+                em[c][3][t] = PB.Zs[(base + v) * h + j];
+            }
         }
-        double acc[HPL];
+        double acc[PSG][HPL];
 #pragma unroll
-        for (int t = 0; t < HPL; ++t) acc[t] = 0.0;
+        for (int c = 0; c < PSG; ++c)
+#pragma unroll
+            for (int t = 0; t < HPL; ++t) acc[c][t] = 0.0;
 #pragma unroll
         for (int b = 0; b < 4; ++b)
-#pragma unroll 8
+#pragma unroll 4
             for (int ii = 0; ii < h; ++ii) {
-                double ev = 0.0;
-#pragma unroll
-                for (int t = 0; t < HPL; ++t) {
-                    const double x = __shfl_sync(FP_FULL_MASK, em[b][t], ii & 31);
-                    if ((ii >> 5) == t) ev = x;
-                }
+                double w[HPL];
 #pragma unroll
                 for (int t = 0; t < HPL; ++t) {
                     const int j = lane + 32 * t;
-                    if (j < h) acc[t] = fma(ev, w1[(b * h + ii) * h + j], acc[t]);
+                    w[t] = j < h ? w1[(b * h + ii) * h + j] : 0.0;
+                }
+#pragma unroll
+                for (int c = 0; c < PSG; ++c) {
+                    double ev = 0.0;
+#pragma unroll
+                    for (int t = 0; t < HPL; ++t) {
+                        const double x = __shfl_sync(FP_FULL_MASK, em[c][b][t], ii & 31);
+                        if ((ii >> 5) == t) ev = x;
+                    }
+#pragma unroll
+                    for (int t = 0; t < HPL; ++t) {
+                        const int j = lane + 32 * t;
+                        if (j < h) acc[c][t] = fma(ev, w[t], acc[c][t]);
+                    }
                 }
             }
-        double part = 0.0;
 #pragma unroll
-        for (int t = 0; t < HPL; ++t) {
-            const int j = lane + 32 * t;
-            if (j < h) part = fma(lk(acc[t] + b1[j], slope), w2[j], part);
+        for (int c = 0; c < PSG; ++c) {
+            const int i = i0 + c * kPsWarps;
+            double part = 0.0;
+#pragma unroll
+            for (int t = 0; t < HPL; ++t) {
+                const int j = lane + 32 * t;
+                if (j < h) part = fma(lk(acc[c][t] + b1[j], slope), w2[j], part);
+            }
+            part = warp_sum(part);
+            if (lane == 0 && i < k) cs[i] = part + b2;
         }
-        part = warp_sum(part);
-        if (lane == 0) cs[i] = part + b2;
     }
     // h_d partial sums: h_d = sum of this step's G rows over the vertices
     // placed on d (before this step) -- independent of this step's choices,
