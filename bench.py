@@ -196,7 +196,8 @@ def bench_config(args, world: int, desc: str) -> dict:
                         if args.full_outputs else "assignments + makespans"),
             "parallelism": f"episode-dp{world}",
             "l2": "GPU arm: flushed between timed steps (256 MiB write); e2e: steps pipelined "
-                  "(D2H on a side stream, double-buffered outputs), L2 evicted every step by a "
+                  "(H2D of the parameters and D2H of the results on side streams, double-buffered), "
+                  "L2 evicted every step by a "
                   "128 MiB device-to-device copy (copy engine, 256 MiB through L2) on the side "
                   "stream"}
 
@@ -382,13 +383,23 @@ def run_ours(args):
     dev_params = [torch.empty_like(flat) for _ in range(2)]
     outs = [out, ctx.alloc_batch(B, grad=train, trace_steps=args.full_outputs)]
     copy_stream = torch.cuda.Stream()
+    h2d_stream = torch.cuda.Stream()
+    h2d_ev = [torch.cuda.Event() for _ in range(2)]
     done_ev = [torch.cuda.Event() for _ in range(2)]
     free_ev = [torch.cuda.Event() for _ in range(2)]
 
     def e2e_step(i):
         sl = i % 2
         comp = torch.cuda.current_stream()
-        dev_params[sl].copy_(host_params, non_blocking=True)
+        # H2D of this step's parameters on its own stream, double-buffered, so
+        # it overlaps the previous step's kernels (step i-2 must be done with
+        # the buffer); the step's kernels wait for it
+        with torch.cuda.stream(h2d_stream):
+            if i >= 2:
+                h2d_stream.wait_event(done_ev[sl])
+            dev_params[sl].copy_(host_params, non_blocking=True)
+            h2d_ev[sl].record(h2d_stream)
+        comp.wait_event(h2d_ev[sl])
         if i >= 2:
             comp.wait_event(free_ev[sl])  # step i-2's results are on the host
         if train:
