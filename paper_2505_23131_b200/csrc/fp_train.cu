@@ -36,6 +36,8 @@ __device__ __forceinline__ double lk_t(double x, double s) { return x > 0.0 ? x 
 // head backward, warp per vertex, lane = hidden column
 // ---------------------------------------------------------------------------
 __global__ void head_bwd_kernel(DevPolicy P) {
+    griddep_launch();  // PDL chain of the backward: launch latency hidden,
+    griddep_wait();    // the predecessor complete before any access
     const int lane = lane_id();
     const int v = blockIdx.x * 4 + (threadIdx.x >> 5);
     const int n = P.n, h = P.h;
@@ -91,6 +93,8 @@ __global__ void head_bwd_kernel(DevPolicy P) {
 // dH of each encoder's output: SEL = direct + path scatters (inverse paths);
 // PLC = head part; shared encoder = both.
 __global__ void path_gather_kernel(DevPolicy P) {
+    griddep_launch();  // PDL chain of the backward: launch latency hidden,
+    griddep_wait();    // the predecessor complete before any access
     const int lane = lane_id();
     const int u = blockIdx.x * 4 + (threadIdx.x >> 5);
     const int n = P.n, h = P.h;
@@ -118,6 +122,8 @@ __global__ void path_gather_kernel(DevPolicy P) {
 // node part: dU = dH (.) leaky'(U); dH_k(direct) = dU @ phi[0:dk]^T;
 // dagg = dU @ phi[dk:dk+h]^T
 __global__ void gnn_bwd_node(DevPolicy P, int e, int k) {
+    griddep_launch();  // PDL chain of the backward: launch latency hidden,
+    griddep_wait();    // the predecessor complete before any access
     const int lane = lane_id();
     const int v = blockIdx.x * 4 + (threadIdx.x >> 5);
     const int n = P.n, h = P.h;
@@ -154,6 +160,8 @@ __global__ void gnn_bwd_node(DevPolicy P, int e, int k) {
 //   De[v]   = sum_{w->v} e * dagg[v] (.) leaky'(...)
 // then dH_k = dH_k(direct) + Dsrc @ Ws^T + Ddst @ Wd^T   (k > 0)
 __global__ void gnn_bwd_msg(DevPolicy P, int e, int k) {
+    griddep_launch();  // PDL chain of the backward: launch latency hidden,
+    griddep_wait();    // the predecessor complete before any access
     const int lane = lane_id();
     const int v = blockIdx.x * 4 + (threadIdx.x >> 5);
     const int n = P.n, h = P.h;
@@ -205,6 +213,8 @@ __global__ void gnn_bwd_msg(DevPolicy P, int e, int k) {
 }
 
 __global__ void copy_kernel(double *dst, const double *src, int count) {
+    griddep_launch();  // PDL chain of the backward: launch latency hidden,
+    griddep_wait();    // the predecessor complete before any access
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < count) dst[i] = src[i];
 }
@@ -228,6 +238,8 @@ struct OuterJob {
 constexpr int kOuterWarps = 8;
 
 __global__ void __launch_bounds__(kOuterWarps * 32) outer_kernel(const OuterJob *jobs) {
+    griddep_launch();  // PDL chain of the backward: launch latency hidden,
+    griddep_wait();    // the predecessor complete before any access
     __shared__ double part[kOuterWarps][64];
     const OuterJob J = jobs[blockIdx.y];
     const int i = blockIdx.x;
@@ -258,6 +270,8 @@ __global__ void __launch_bounds__(kOuterWarps * 32) outer_kernel(const OuterJob 
 // PLC small terms + SEL head2 (single block): dWy = dM @ W1c^T, dby = dc @ W1c^T,
 // db1 = dc, dw2/db2 from the reduction, SEL w2 / b2.
 __global__ void __launch_bounds__(256) small_bwd_kernel(DevPolicy P, double *grad) {
+    griddep_launch();  // PDL chain of the backward: launch latency hidden,
+    griddep_wait();    // the predecessor complete before any access
     __shared__ double part[8][65];  // [warp][column | sum of ds]
     const int h = P.h, n = P.n;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -405,7 +419,8 @@ static void launch_outer(fp_train_state *ts, int stage, cudaStream_t st) {
     int maxk = 0;
     for (auto &j : b) maxk = std::max(maxk, j.K);
     dim3 grid(maxk, (unsigned)b.size());
-    outer_kernel<<<grid, kOuterWarps * 32, 0, st>>>(ts->jobs_dev + ts->stage_offset[stage]);
+    launch_pdl(outer_kernel, grid, dim3(kOuterWarps * 32), 0, st,
+               (const OuterJob *)(ts->jobs_dev + ts->stage_offset[stage]));
 }
 
 }  // namespace fp
@@ -455,18 +470,20 @@ int fp_policy_backward(fp_policy *pol, double *grad, void *stream) {
     const int n = P.n, h = P.h;
     const int g4 = (n + 3) / 4;
     cudaMemsetAsync(grad, 0, sizeof(double) * pol->n_params, st);
-    head_bwd_kernel<<<g4, 128, 0, st>>>(P);
-    path_gather_kernel<<<g4, 128, 0, st>>>(P);
+    launch_pdl(head_bwd_kernel, dim3(g4), dim3(128), 0, st, P);
+    launch_pdl(path_gather_kernel, dim3(g4), dim3(128), 0, st, P);
     launch_outer(ts, 0, st);  // dc
-    small_bwd_kernel<<<1, 256, 0, st>>>(P, grad);
+    launch_pdl(small_bwd_kernel, dim3(1), dim3(256), 0, st, P, grad);
     launch_outer(ts, 1, st);  // head weight gradients
     int stage = 2;
     for (int e = 0; e < P.n_enc; ++e)
         for (int k = P.K - 1; k >= 0; --k) {
-            gnn_bwd_node<<<g4, 128, 0, st>>>(P, e, k);
-            gnn_bwd_msg<<<g4, 128, 0, st>>>(P, e, k);
+            launch_pdl(gnn_bwd_node, dim3(g4), dim3(128), 0, st, P, e, k);
+            launch_pdl(gnn_bwd_msg, dim3(g4), dim3(128), 0, st, P, e, k);
             launch_outer(ts, stage++, st);
-            if (k > 0) copy_kernel<<<(n * h + 255) / 256, 256, 0, st>>>(P.dH[e], P.dHn[0], n * h);
+            if (k > 0)
+                launch_pdl(copy_kernel, dim3((n * h + 255) / 256), dim3(256), 0, st, P.dH[e],
+                           (const double *)P.dHn[0], n * h);
         }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FP_ERR_CUDA; }
