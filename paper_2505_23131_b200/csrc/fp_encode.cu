@@ -632,8 +632,8 @@ static int launch_gnn_tc(DevPolicy &P, cudaStream_t st, bool sel_head = true) {
             const int B = P.rows / P.n;
             const dim3 grid(std::max(1, std::min(B, sms / P.n_enc)), P.n_enc);
             agg_timer_begin(st);
-            if (P.tc) gnn_agg_staged_kernel<H, true><<<grid, 1024, smem, st>>>(P, k, agg_S);
-            else gnn_agg_staged_kernel<H, false><<<grid, 1024, smem, st>>>(P, k, agg_S);
+            if (P.tc) FP_CUDA_RET(launch_pdl(gnn_agg_staged_kernel<H, true>, grid, dim3(1024), (size_t)smem, st, P, k, agg_S));
+            else FP_CUDA_RET(launch_pdl(gnn_agg_staged_kernel<H, false>, grid, dim3(1024), (size_t)smem, st, P, k, agg_S));
             FP_CUDA_RET(cudaGetLastError());
             agg_timer_end(st);
         } else {

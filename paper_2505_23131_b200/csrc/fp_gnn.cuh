@@ -202,6 +202,15 @@ __global__ void __launch_bounds__(NT, 1) gnn_agg_staged_kernel(DevPolicy P, int 
     int *s_nbr = s_ptr + n + 1;
     const T *Pg = (const T *)P.Pm[e][k];
     const T *Qg = (const T *)P.Qm[e][k];
+    griddep_launch();
+    // prologue on constant tables (message CSR), overlapping the previous
+    // kernel under PDL; P / Q only after the dependency wait
+    for (int i = threadIdx.x; i < M; i += blockDim.x) {
+        s_e[i] = P.adj_e[i];
+        s_nbr[i] = P.adj_nbr[i] * HL;  // row offset in T2 units
+    }
+    for (int i = threadIdx.x; i <= n; i += blockDim.x) s_ptr[i] = P.adj_ptr[i];
+    griddep_wait();
     if (threadIdx.x == 0) {
         for (int i = 0; i < S; ++i) tc::mbar_init(&bar[i], 1);
         tc::fence_mbar_init();
@@ -214,11 +223,6 @@ __global__ void __launch_bounds__(NT, 1) gnn_agg_staged_kernel(DevPolicy P, int 
             tc::bulk_load(dst + slice, Qg + (size_t)ep * n * H, slice, &bar[i]);
         }
     }
-    for (int i = threadIdx.x; i < M; i += blockDim.x) {
-        s_e[i] = P.adj_e[i];
-        s_nbr[i] = P.adj_nbr[i] * HL;  // row offset in T2 units
-    }
-    for (int i = threadIdx.x; i <= n; i += blockDim.x) s_ptr[i] = P.adj_ptr[i];
     const int l = threadIdx.x % HL, unit = threadIdx.x / HL, units = blockDim.x / HL;
     const int dk = k == 0 ? 7 : H;
     const double *psw = P.W(gnn_role(e, k, 0)), *psb = P.W(gnn_role(e, k, 1));

@@ -113,6 +113,7 @@ ps_step_kernel(DevProblem PR, DevPolicy PO, DevPolicy PB, fp_rollout_args A, PsS
     __shared__ double sd_part[kPsWarps - 1][MAXD * HPL <= 16 ? MAXD : 1][MAXD * HPL <= 16 ? 32 * HPL : 1];
     const int lane = lane_id(), warp = threadIdx.x >> 5;
     const int ep = blockIdx.x;
+    griddep_wait();  // (PDL) this step's encode complete
     if (ep >= A.B || S.stat[ep] != FP_EP_OK) return;  // block-uniform
     const int n = PR.n, W = PR.W, D = PR.d, h = PO.h;
     const size_t base = (size_t)ep * n;
@@ -556,7 +557,8 @@ template <int MAXD, int HPL>
 static void ps_launch_step(const fp_problem *p, const fp_policy *pol, const DevPolicy &PB,
                            const fp_rollout_args &a, const PsState &S, int step,
                            cudaStream_t st) {
-    ps_step_kernel<MAXD, HPL><<<a.B, kPsWarps * 32, 0, st>>>(p->dev, pol->dev, PB, a, S, step);
+    launch_pdl(ps_step_kernel<MAXD, HPL>, dim3(a.B), dim3(kPsWarps * 32), 0, st, p->dev, pol->dev, PB, a,
+               S, step);
 }
 
 int per_step_rollout(const fp_problem *p, const fp_policy *pol, const fp_rollout_args &a,

@@ -1208,6 +1208,8 @@ plc_replay_kernel(DevProblem PR, DevPolicy PO, const double *__restrict__ rec, i
                   const double *__restrict__ alpha, double beta, int B, double *__restrict__ cbuf,
                   double *__restrict__ slab, double *__restrict__ tbuf, double *__restrict__ sbuf,
                   int *__restrict__ posbuf) {
+    griddep_launch();
+    griddep_wait();  // (PDL) predecessor complete before any access
     constexpr int K = kChunkWarps;
     __shared__ double stage[K][2][6 * MAXD];
     // dynamic: rtot[K][D][h] | rsm[K][6h+1] | vt[n] jt[n]
@@ -1462,6 +1464,8 @@ static __global__ void pg_rows_kernel(DevPolicy P, int D, int B, int L,
                                       const int32_t *__restrict__ assign,
                                       const double *__restrict__ alpha, double beta,
                                       double *__restrict__ part) {
+    griddep_launch();
+    griddep_wait();  // (PDL) predecessor complete before any access
     const int n = P.n, h = P.h, nh = n * h;
     const int64_t PSt = pg_part_stride(n, h);
     const int item = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1502,6 +1506,8 @@ static __global__ void pg_rows_kernel(DevPolicy P, int D, int B, int L,
 
 // chunk partials -> dA, dG, [dM | dw2 | db2], ds, summed in chunk order
 static __global__ void pg_final_kernel(DevPolicy P, const double *__restrict__ part) {
+    griddep_launch();
+    griddep_wait();  // (PDL) predecessor complete before any access
     const int n = P.n, h = P.h, nh = n * h;
     const int64_t PSt = pg_part_stride(n, h);
     const int item = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1539,13 +1545,14 @@ int launch_plc_replay(const fp_problem *p, const fp_policy *pol, const double *r
     cudaError_t e0 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)dyn);
     if (e0 != cudaSuccess) { set_error(cudaGetErrorString(e0)); return FP_ERR_CUDA; }
-    kern<<<B, K * 32, dyn, st>>>(PR, PO, rec, grad_rec_stride(D, PR.W), gep, gstride, alpha, beta,
-                                 B, cbuf, slab, tbuf, sbuf, posbuf);
+    launch_pdl(kern, dim3(B), dim3(K * 32), (size_t)dyn, st, PR, PO, rec, grad_rec_stride(D, PR.W),
+               gep, gstride, alpha, beta, B, cbuf, slab, tbuf, sbuf, posbuf);
     const int items = n * h + 6 * h + 1 + n;
-    pg_rows_kernel<<<dim3((items + 127) / 128, kPgChunks), 128, 0, st>>>(
-        PO, D, B, (n + K - 1) / K, slab, tbuf, sbuf, posbuf, gep, gstride, assign, alpha, beta,
-        part);
-    pg_final_kernel<<<(int)((PSt + 127) / 128), 128, 0, st>>>(PO, part);
+    launch_pdl(pg_rows_kernel, dim3((items + 127) / 128, kPgChunks), dim3(128), 0, st, PO, D, B,
+               (n + K - 1) / K, (const double *)slab, (const double *)tbuf, (const double *)sbuf,
+               (const int *)posbuf, gep, gstride, assign, alpha, beta, part);
+    launch_pdl(pg_final_kernel, dim3((int)((PSt + 127) / 128)), dim3(128), 0, st, PO,
+               (const double *)part);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FP_ERR_CUDA; }
     return FP_OK;

@@ -320,6 +320,7 @@ __global__ void __launch_bounds__(256) small_bwd_kernel(DevPolicy P, double *gra
 
 __global__ void sgd_kernel(double *params, const double *grad, int64_t count, double lr,
                            const int32_t *skip) {
+    griddep_wait();  // (PDL) the gradient complete
     if (skip && *skip) return;  // a failed rollout in this (or an earlier) batch: no update
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < count) params[i] = params[i] - lr * grad[i];
@@ -494,8 +495,8 @@ int fp_sgd_step_masked(double *params, const double *grad, int64_t count, double
                        const int32_t *skip, void *stream) {
     if (!params || !grad || count < 0) { set_error("bad sgd arguments"); return FP_ERR_INVALID; }
     if (count == 0) return FP_OK;
-    sgd_kernel<<<(unsigned)((count + 255) / 256), 256, 0, (cudaStream_t)stream>>>(params, grad,
-                                                                                  count, lr, skip);
+    launch_pdl(sgd_kernel, dim3((unsigned)((count + 255) / 256)), dim3(256), 0, (cudaStream_t)stream,
+               params, grad, count, lr, skip);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { set_error(cudaGetErrorString(e)); return FP_ERR_CUDA; }
     return FP_OK;
