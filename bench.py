@@ -557,8 +557,7 @@ PLC_CHAIN_OPS = {          # op: (dependent count per decision, latency cycles)
     "SHFL (transpose reduction 5, device scan 3, broadcasts 3)": (11, 7),
     "REDUX (fp64 max as two 32-bit reductions) x2": (2, 20),
     "fp64 exp (device softmax)": (1, 154),
-    "fp64 sqrt_rn (column std)": (1, 93),
-    "fp64 reciprocal (column std)": (1, 70),
+    "fp64 rsqrt (column scale, one per column since the rsqrt statistics)": (1, 64),
 }
 
 

@@ -1,6 +1,6 @@
 // Dependent-chain latencies on this GPU, in cycles per loop trip (about 19 of
 // which are the loop itself): DFMA, DADD, FFMA, SHFL (32-bit and a double),
-// LDS, exp / log / sqrt_rn / rcp / div_rn (fp64), fmax, REDUX.  One warp,
+// LDS, exp / log / sqrt_rn / rcp / div_rn / rsqrt (fp64), fmax, REDUX.  One warp,
 // clock64 around 256-long chains.  Measured on B200.
 // build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/micro/lat tools/micro/lat.cu
 #include <cstdio>
@@ -29,6 +29,7 @@ __global__ void k(double *out, long long *cyc, double x0, float f0) {
     TIME(12, {long long b = __double_as_longlong(x); x = __longlong_as_double(b ^ 1);} x = x + 0.0);
     TIME(13, { unsigned v = __reduce_max_sync(0xffffffffu, (unsigned)i0); i0 = v + 1; });
     TIME(14, loop_empty:;);
+    TIME(15, x = rsqrt(x + 1.0));
     out[threadIdx.x] = x + f + i0;
 }
 int main() {
@@ -37,7 +38,8 @@ int main() {
     k<<<1, 32>>>(o, c, 1.0, 1.0f); cudaDeviceSynchronize();
     long long h[16]; cudaMemcpy(h, c, 16 * 8, cudaMemcpyDeviceToHost);
     const char *nm[] = {"dfma", "dadd", "ffma", "shfl32", "shfl_f64", "lds_f64", "exp_f64", "log_f64",
-                        "sqrt_rn_f64", "rcp_f64", "div_rn_f64", "fmax_f64", "xor+dadd", "redux_max", "loop"};
-    for (int i = 0; i < 15; ++i) printf("%-12s %6.1f cyc/iter\n", nm[i], (double)h[i] / N);
+                        "sqrt_rn_f64", "rcp_f64", "div_rn_f64", "fmax_f64", "xor+dadd", "redux_max", "loop",
+                        "rsqrt_f64"};
+    for (int i = 0; i < 16; ++i) printf("%-12s %6.1f cyc/iter\n", nm[i], (double)h[i] / N);
     return 0;
 }
