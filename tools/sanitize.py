@@ -40,3 +40,19 @@ ps = PolicyContext(g, cl, PolicyConfig(hidden=16, mp_mode="per_step"))
 ps.rollout_batch(params, 2, 0.2, 6)                                    # per_step
 torch.cuda.synchronize()
 print("sanitize workload done")
+# round-2 additions: per_step staged aggregation under the bf16 encoder too,
+# and a > 64-op graph so the PDL-chained multi-kernel encode + rollout and the
+# PDL backward / replay / SGD chain run
+ps.set_encoder("tc")
+ps.rollout_batch(params, 2, 0.2, 7)                                    # per_step, tc + staged
+gl = builders.build_llama_block()
+cll = ClusterSpec.uniform(8, rate=1e9, bandwidth=1e7)
+pcl = PolicyConfig()
+pl = init_policy_params(pcl, seed=0)
+cx = PolicyContext(gl, cll, pcl)
+cx.rollout_batch(pl, 2, 0.2, 8)                                        # PDL encode chain + rollout
+trl = BatchedTrainer(cx, pl, TrainConfig(episodes=64), batch_size=2)
+trl.step(seed=9)                                                       # PDL backward chain
+trl.check()
+torch.cuda.synchronize()
+print("sanitize workload done")
